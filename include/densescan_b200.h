@@ -1,0 +1,135 @@
+/*
+ * densescan_b200 — C ABI of the sm_100a DBSCAN hot path.
+ *
+ * This is the drop-in boundary for the reference package's CPU path
+ * `run_dbscan(points, validate_params(eps, min_pts), default_config())`
+ * (reference pkg/src/densescan/pipeline.py:70-92). The reference has no FFI
+ * of its own (it is pure Python); the Python mirror in
+ * paper_1506_02226_b200/ binds these symbols with ctypes, and INTEGRATION.md
+ * shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Host buffers are caller-owned; the context
+ *    owns device workspaces and streams. Inputs are never written.
+ *  - Coordinates are float64, point-major (n x d), exactly the reference
+ *    PointSet.coords_aos layout (core.py:43-70). The library narrows them to
+ *    float32 round-to-nearest once (kernels.py:148-150).
+ *  - eps_sq is the float64 eps*eps of DbscanParams (core.py:93); the kernel
+ *    threshold is float32(eps_sq) (kernels.py:355, 385).
+ *  - Every entry point returns a ds_status; on failure ds_last_error() gives a
+ *    thread-local message and, for DS_ECAPACITY, ds_last_capacity() gives the
+ *    (required, cap) byte pair that the Python shim re-raises as
+ *    CapacityExceeded(required_bytes, cap_bytes) (kernels.py:55-63).
+ *  - Labels are int64, canonical: clusters numbered 0,1,2,... by lowest member
+ *    index, noise = -1 (core.py:116-132). Results do not depend on thread
+ *    scheduling, atomics order or GPU count.
+ *  - A context is not thread-safe; use one context per host thread.
+ */
+#ifndef DENSESCAN_B200_H
+#define DENSESCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+
+typedef struct ds_ctx ds_ctx;
+
+typedef enum {
+  DS_OK = 0,
+  DS_EINVAL = 1,        /* -> InvalidParams / ValueError (core.py:22-27, 53-58)      */
+  DS_ECAPACITY = 2,     /* -> CapacityExceeded(required, cap) (kernels.py:55-79)    */
+  DS_ECUDA = 3,         /* -> DeviceError                                            */
+  DS_EINCONSISTENT = 4, /* -> InconsistentInput (merge.py:36-37, 141-145)            */
+  DS_ENCCL = 5          /* -> DeviceError (multi-GPU exchange)                       */
+} ds_status;
+
+typedef enum {
+  DS_FORMULA_DIRECT = 0,    /* FUSED and the four materialising rungs (kernels.py:197-210) */
+  DS_FORMULA_ALGEBRAIC = 1  /* FUSED_ALGEBRAIC, the default (kernels.py:374-417)          */
+} ds_formula;
+
+/* Per-call measurements; mirrors StageTimings (pipeline.py:52-67) plus the
+ * counters the benchmark needs. All times are device (CUDA event) times
+ * except total_ms, which covers the whole call including copies. */
+typedef struct {
+  double fused_ms;          /* stage 1+2: prep + eps-tile kernel (+ core flags)      */
+  double merge_ms;          /* stage 3: union-find, borders, canonical labels        */
+  double total_ms;          /* whole call, host wall clock                           */
+  double tile_ms;           /* the eps-tile kernel alone                             */
+  double h2d_ms;            /* host->device copy of the coordinates                  */
+  double d2h_ms;            /* device->host copy of the labels                       */
+  int64_t pairs_evaluated;  /* ordered pair evaluations executed by the tile kernel  */
+  int64_t tiles_total;      /* tile pairs processed (upper triangle incl. diagonal)  */
+  int64_t tiles_nonempty;   /* tile pairs with at least one in-range pair            */
+  int64_t words_emitted;    /* 32-bit adjacency words kept for stage 3               */
+  int64_t core_count;
+  int64_t cluster_count;
+  int64_t device_bytes;     /* device workspace held by the context after the call   */
+  int32_t unsafe_range;     /* 1 if coordinates needed the overflow-safe compare     */
+  int32_t tile_launches;    /* eps-tile kernel launches (>1 after a capacity regrow) */
+} ds_timings;
+
+/* Library / build identification. */
+int ds_abi_version(void);
+const char* ds_build_info(void);
+
+/* Last error of the calling thread. */
+const char* ds_last_error(void);
+void ds_last_capacity(int64_t* required_bytes, int64_t* cap_bytes);
+
+/* Context on one CUDA device (ordinal). */
+ds_status ds_ctx_create(int device, ds_ctx** out);
+void ds_ctx_destroy(ds_ctx* ctx);
+
+/*
+ * run_dbscan (pipeline.py:70-92): host float64 coords in, host int64
+ * canonical labels out. mem_cap bounds the device workspace in bytes
+ * (<= 0: no bound). counts_out (int64[n]) is optional (NULL to skip).
+ */
+ds_status ds_run_dbscan(ds_ctx* ctx, const double* coords, int64_t n, int32_t d,
+                        double eps_sq, int64_t min_pts, int32_t formula, int64_t mem_cap,
+                        int64_t* labels_out, int64_t* counts_out, ds_timings* timings);
+
+/*
+ * Same pipeline on device-resident buffers: d_coords is a device float64
+ * n x d array, d_labels a device int64[n]. `stream` is a cudaStream_t (NULL:
+ * the legacy default stream); all work is enqueued on it and the call returns
+ * after the stream has completed it.
+ */
+ds_status ds_run_dbscan_device(ds_ctx* ctx, const double* d_coords, int64_t n, int32_t d,
+                               double eps_sq, int64_t min_pts, int32_t formula,
+                               int64_t mem_cap, int64_t* d_labels, void* stream,
+                               ds_timings* timings);
+
+/*
+ * Stage 1+2 in the reference's NeighborhoodMatrix / ValidVector layout
+ * (kernels.py:120-145, 311-337, 420-442): bits_out is n x ceil(n/8) bytes,
+ * numpy packbits MSB-first rows (_bitmat.py:4-7) or NULL; counts_out int64[n]
+ * (incl. self); valid_out uint8[n] (counts >= min_pts).
+ */
+ds_status ds_fused_build(ds_ctx* ctx, const double* coords, int64_t n, int32_t d,
+                         double eps_sq, int64_t min_pts, int32_t formula, int64_t mem_cap,
+                         uint8_t* bits_out, int64_t* counts_out, uint8_t* valid_out,
+                         ds_timings* timings);
+
+/*
+ * Stage 3 from a reference-layout NeighborhoodMatrix (merge_iterative,
+ * merge.py:133-166, and merge_warshall, merge.py:218-238, which are
+ * label-equivalent): bits n x ceil(n/8) MSB-first, counts int64[n], valid
+ * uint8[n]. Checks valid == (counts >= min_pts) first (DS_EINCONSISTENT,
+ * merge.py:141-145). Writes canonical int64 labels.
+ */
+ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
+                        const uint8_t* valid, int64_t n, int64_t min_pts,
+                        int64_t* labels_out, ds_timings* timings);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DENSESCAN_B200_H */

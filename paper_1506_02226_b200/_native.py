@@ -1,0 +1,220 @@
+"""ctypes binding of the sm_100a library (include/densescan_b200.h).
+
+There is no CPU fallback: if the shared library is missing or cannot reach a
+CUDA device, every entry point raises. Build it with `make -C
+paper_1506_02226_b200/csrc` (or `python -c "import __graft_entry__ as g;
+g.build()"`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .core import DensescanError, DeviceError, InvalidParams
+
+LIB_NAME = "libdensescan_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
+FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
+
+# every symbol the header declares; tests/test_abi.py checks the .so exports them
+EXPORTS = (
+    "ds_abi_version", "ds_build_info", "ds_last_error", "ds_last_capacity",
+    "ds_ctx_create", "ds_ctx_destroy", "ds_run_dbscan", "ds_run_dbscan_device",
+    "ds_fused_build", "ds_merge_bits",
+)
+
+
+class Timings(ctypes.Structure):
+    """Mirror of ds_timings."""
+
+    _fields_ = [
+        ("fused_ms", ctypes.c_double),
+        ("merge_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+        ("tile_ms", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("pairs_evaluated", ctypes.c_int64),
+        ("tiles_total", ctypes.c_int64),
+        ("tiles_nonempty", ctypes.c_int64),
+        ("words_emitted", ctypes.c_int64),
+        ("core_count", ctypes.c_int64),
+        ("cluster_count", ctypes.c_int64),
+        ("device_bytes", ctypes.c_int64),
+        ("unsafe_range", ctypes.c_int32),
+        ("tile_launches", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_i64_p = ctypes.POINTER(ctypes.c_int64)
+_c_u8_p = ctypes.POINTER(ctypes.c_uint8)
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and prototype the library (no CUDA call is made here)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(
+                f"{path} is missing: the densescan sm_100a library is not built "
+                "(run `make -C paper_1506_02226_b200/csrc`); there is no CPU fallback")
+        lib = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        lib.ds_abi_version.restype = ctypes.c_int
+        lib.ds_build_info.restype = ctypes.c_char_p
+        lib.ds_last_error.restype = ctypes.c_char_p
+        lib.ds_last_capacity.argtypes = [_c_i64_p, _c_i64_p]
+        lib.ds_last_capacity.restype = None
+        lib.ds_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+        lib.ds_ctx_create.restype = ctypes.c_int
+        lib.ds_ctx_destroy.argtypes = [vp]
+        lib.ds_ctx_destroy.restype = None
+        lib.ds_run_dbscan.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
+                                      ctypes.POINTER(Timings)]
+        lib.ds_run_dbscan.restype = ctypes.c_int
+        lib.ds_run_dbscan_device.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32,
+                                             ctypes.c_double, ctypes.c_int64, ctypes.c_int32,
+                                             ctypes.c_int64, vp, vp, ctypes.POINTER(Timings)]
+        lib.ds_run_dbscan_device.restype = ctypes.c_int
+        lib.ds_fused_build.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                       ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp, vp,
+                                       ctypes.POINTER(Timings)]
+        lib.ds_fused_build.restype = ctypes.c_int
+        lib.ds_merge_bits.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
+                                      ctypes.POINTER(Timings)]
+        lib.ds_merge_bits.restype = ctypes.c_int
+        if lib.ds_abi_version() != 1:
+            raise ImportError(f"{path}: unexpected ABI version {lib.ds_abi_version()}")
+        _lib = lib
+        return lib
+
+
+def raise_for(status: int, lib=None) -> None:
+    if status == DS_OK:
+        return
+    lib = lib or load_library()
+    msg = (lib.ds_last_error() or b"").decode("utf-8", "replace")
+    if status == DS_ECAPACITY:
+        from .kernels import CapacityExceeded
+        req, cap = ctypes.c_int64(), ctypes.c_int64()
+        lib.ds_last_capacity(ctypes.byref(req), ctypes.byref(cap))
+        raise CapacityExceeded(int(req.value), int(cap.value))
+    if status == DS_EINCONSISTENT:
+        from .merge import InconsistentInput
+        raise InconsistentInput(msg)
+    if status == DS_EINVAL:
+        field, _, rest = msg.partition(":")
+        raise InvalidParams(field.strip() or "argument", rest.strip() or msg)
+    if status in (DS_ECUDA, DS_ENCCL):
+        raise DeviceError(msg)
+    raise DensescanError(f"densescan status {status}: {msg}")
+
+
+class Context:
+    """One ds_ctx (device workspace + stream) per (host thread, device)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        self.device = int(device)
+        handle = ctypes.c_void_p()
+        raise_for(self.lib.ds_ctx_create(self.device, ctypes.byref(handle)), self.lib)
+        self.handle = handle
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.ds_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- entry points --------------------------------------------------------
+    def run_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
+                   mem_cap: int, want_counts: bool = False):
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n, d = coords.shape
+        labels = np.empty(n, dtype=np.int64)
+        counts = np.empty(n, dtype=np.int64) if want_counts else None
+        t = Timings()
+        st = self.lib.ds_run_dbscan(self.handle, coords.ctypes.data, n, d, float(eps_sq),
+                                    int(min_pts), int(formula), int(mem_cap),
+                                    labels.ctypes.data,
+                                    counts.ctypes.data if counts is not None else None,
+                                    ctypes.byref(t))
+        raise_for(st, self.lib)
+        return labels, counts, t
+
+    def run_dbscan_device(self, coords_ptr: int, n: int, d: int, eps_sq: float, min_pts: int,
+                          formula: int, mem_cap: int, labels_ptr: int, stream_ptr: int = 0):
+        t = Timings()
+        st = self.lib.ds_run_dbscan_device(self.handle, ctypes.c_void_p(coords_ptr), int(n),
+                                           int(d), float(eps_sq), int(min_pts), int(formula),
+                                           int(mem_cap), ctypes.c_void_p(labels_ptr),
+                                           ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
+        raise_for(st, self.lib)
+        return t
+
+    def fused_build(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
+                    mem_cap: int, want_bits: bool = True):
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n, d = coords.shape
+        bits = np.empty((n, (n + 7) // 8), dtype=np.uint8) if want_bits else None
+        counts = np.empty(n, dtype=np.int64)
+        valid = np.empty(n, dtype=np.uint8)
+        t = Timings()
+        st = self.lib.ds_fused_build(self.handle, coords.ctypes.data, n, d, float(eps_sq),
+                                     int(min_pts), int(formula), int(mem_cap),
+                                     bits.ctypes.data if bits is not None else None,
+                                     counts.ctypes.data, valid.ctypes.data, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return bits, counts, valid.astype(bool), t
+
+    def merge_bits(self, bits: np.ndarray, counts: np.ndarray, valid: np.ndarray, min_pts: int):
+        n = counts.shape[0]
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        if bits.shape != (n, (n + 7) // 8):
+            raise ValueError(f"bits must have shape {(n, (n + 7) // 8)}, got {bits.shape}")
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        valid8 = np.ascontiguousarray(valid, dtype=np.uint8)
+        labels = np.empty(n, dtype=np.int64)
+        t = Timings()
+        st = self.lib.ds_merge_bits(self.handle, bits.ctypes.data, counts.ctypes.data,
+                                    valid8.ctypes.data, n, int(min_pts), labels.ctypes.data,
+                                    ctypes.byref(t))
+        raise_for(st, self.lib)
+        return labels, t
+
+
+_ctx_local = threading.local()
+
+
+def context(device: int | None = None) -> Context:
+    """The calling thread's context on `device` (default: $DENSESCAN_DEVICE or 0)."""
+    if device is None:
+        device = int(os.environ.get("DENSESCAN_DEVICE", "0"))
+    cache = getattr(_ctx_local, "ctxs", None)
+    if cache is None:
+        cache = _ctx_local.ctxs = {}
+    ctx = cache.get(device)
+    if ctx is None:
+        ctx = cache[device] = Context(device)
+    return ctx

@@ -1,0 +1,514 @@
+// C ABI of densescan_b200 (include/densescan_b200.h): context, device workspace,
+// and the three-stage pipeline composition that replaces the reference's
+// run_dbscan (pkg/src/densescan/pipeline.py:70-92), fused_build[_algebraic]
+// (kernels.py:420-442) and merge_iterative (merge.py:133-166).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ds_internal.cuh"
+
+namespace ds {
+
+static thread_local std::string g_error;
+static thread_local int64_t g_required = 0, g_cap = 0;
+
+void set_error(const std::string& msg) { g_error = msg; }
+void set_capacity(int64_t required, int64_t cap) {
+  g_required = required;
+  g_cap = cap;
+}
+
+}  // namespace ds
+
+using namespace ds;
+
+#define DS_CK(expr)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      set_error(std::string(#expr) + " failed: " + cudaGetErrorString(e_));           \
+      return DS_ECUDA;                                                                \
+    }                                                                                 \
+  } while (0)
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Scalars {
+  unsigned long long work_ctr;
+  unsigned long long words_count;
+  unsigned long long nonempty_count;
+  unsigned long long ncore;
+  uint32_t unsafe_flag;
+  int32_t nclusters;
+};
+
+}  // namespace
+
+struct ds_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
+      words, scalars, dense;
+  unsigned long long words_cap = 0;  // in words (uint4 records)
+  Scalars* h_scalars = nullptr;      // pinned
+};
+
+namespace {
+
+cudaError_t ensure(Buf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
+  b.bytes = bytes;
+  return cudaSuccess;
+}
+
+size_t held_bytes(const ds_ctx* c) {
+  const Buf* all[] = {&c->coords64, &c->rec, &c->cnt,   &c->core,     &c->corew,   &c->parent,
+                      &c->bmin,     &c->cmin, &c->root, &c->flag,     &c->partials, &c->labels,
+                      &c->counts64, &c->words, &c->scalars, &c->dense};
+  size_t s = 0;
+  for (const Buf* b : all) s += b->bytes;
+  return s;
+}
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+ds_status check_args(int64_t n, int32_t d, int64_t min_pts, int32_t formula) {
+  if (n < 1) {
+    set_error("n: a PointSet needs at least one point");
+    return DS_EINVAL;
+  }
+  if (n >= (int64_t)0x7fffffff - 1024) {
+    set_error("n: more than 2^31 points is not supported");
+    return DS_EINVAL;
+  }
+  if (d < 1 || d > MAX_D) {
+    set_error("d: dimension must be in [1, 64]");
+    return DS_EINVAL;
+  }
+  if (min_pts < 1) {
+    set_error("min_pts: threshold must be an integer >= 1");
+    return DS_EINVAL;
+  }
+  if (formula != DS_FORMULA_DIRECT && formula != DS_FORMULA_ALGEBRAIC) {
+    set_error("formula: must be 0 (direct) or 1 (algebraic)");
+    return DS_EINVAL;
+  }
+  return DS_OK;
+}
+
+// Bytes of every device buffer the pipeline needs except the adjacency words.
+size_t base_bytes(int64_t n, int d) {
+  const size_t N = (size_t)n;
+  return N * rec_stride(d) * 4      // rec
+         + N * 4 * 6                // cnt parent bmin cmin root flag
+         + N                        // core
+         + ((N + 31) / 32) * 4      // corew
+         + (size_t)scan_partials_len(n) * 4 + sizeof(Scalars) + N * 8;  // labels
+}
+
+MergeWs merge_ws(ds_ctx* c, int64_t n) {
+  MergeWs w;
+  Scalars* sc = (Scalars*)c->scalars.p;
+  w.n = n;
+  w.cnt = (const int32_t*)c->cnt.p;
+  w.core = (uint8_t*)c->core.p;
+  w.corew = (uint32_t*)c->corew.p;
+  w.parent = (int32_t*)c->parent.p;
+  w.bmin = (int32_t*)c->bmin.p;
+  w.cmin = (int32_t*)c->cmin.p;
+  w.root = (int32_t*)c->root.p;
+  w.flag = (int32_t*)c->flag.p;
+  w.partials = (int32_t*)c->partials.p;
+  w.nclusters = &sc->nclusters;
+  w.ncore = &sc->ncore;
+  return w;
+}
+
+ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
+  const size_t N = (size_t)n;
+  DS_CK(ensure(c->rec, N * rec_stride(d) * 4));
+  DS_CK(ensure(c->cnt, N * 4));
+  DS_CK(ensure(c->core, N));
+  DS_CK(ensure(c->corew, ((N + 31) / 32) * 4));
+  DS_CK(ensure(c->parent, N * 4));
+  DS_CK(ensure(c->bmin, N * 4));
+  DS_CK(ensure(c->cmin, N * 4));
+  DS_CK(ensure(c->root, N * 4));
+  DS_CK(ensure(c->flag, N * 4));
+  DS_CK(ensure(c->partials, (size_t)scan_partials_len(n) * 4));
+  DS_CK(ensure(c->scalars, sizeof(Scalars)));
+  return DS_OK;
+}
+
+// Stage 1+2: prep + eps-tile kernel (+ capacity regrow). On return the words,
+// counts and scalars are valid on `s` (the stream has been synchronised once to
+// read the word count).
+ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq, int formula,
+                  int64_t mem_cap, cudaStream_t s, ds_timings* t) {
+  ds_status st = alloc_common(c, n, d);
+  if (st != DS_OK) return st;
+  const int64_t T = n_tiles(n);
+  const int64_t items = n_items(T);
+  const size_t base = base_bytes(n, d);
+
+  // first guess for the adjacency words: keep what earlier calls needed
+  unsigned long long want = std::max<unsigned long long>(c->words_cap, (unsigned long long)n * 8 + (1ull << 20));
+  if (mem_cap > 0) {
+    const int64_t room = mem_cap - (int64_t)base;
+    if (room < 16 * 1024) {
+      set_capacity((int64_t)base + 16 * 1024, mem_cap);
+      set_error("device workspace exceeds the memory cap");
+      return DS_ECAPACITY;
+    }
+    want = std::min<unsigned long long>(want, (unsigned long long)(room / 16));
+  }
+  if (c->words.bytes < want * 16) DS_CK(ensure(c->words, want * 16));
+  c->words_cap = c->words.bytes / 16;
+  if (mem_cap > 0) {  // a buffer kept from an earlier, larger call must not bypass the cap
+    const unsigned long long room_words = (unsigned long long)((mem_cap - (int64_t)base) / 16);
+    c->words_cap = std::min(c->words_cap, room_words);
+  }
+
+  Scalars* sc = (Scalars*)c->scalars.p;
+  const float eps32 = (float)eps_sq;  // float32(float64 eps^2), RN (kernels.py:355/385)
+
+  DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
+  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, s));
+
+  int launches = 0;
+  for (;;) {
+    DS_CK(cudaMemsetAsync(c->cnt.p, 0, (size_t)n * 4, s));
+    DS_CK(cudaMemsetAsync(&sc->work_ctr, 0, 3 * sizeof(unsigned long long), s));
+    TileArgs a;
+    a.rec = (const float*)c->rec.p;
+    a.n = n;
+    a.T = (int32_t)T;
+    a.d = d;
+    a.item_lo = 0;
+    a.item_hi = items;
+    a.work_ctr = &sc->work_ctr;
+    a.eps32 = eps32;
+    a.cnt = (int32_t*)c->cnt.p;
+    a.words = (uint4*)c->words.p;
+    a.words_cap = c->words_cap;
+    a.words_count = &sc->words_count;
+    a.nonempty_count = &sc->nonempty_count;
+    a.unsafe_flag = &sc->unsafe_flag;
+    DS_CK(cudaEventRecord(c->ev[1], s));
+    DS_CK(launch_tile(a, formula, c->sm_count, s));
+    DS_CK(cudaEventRecord(c->ev[2], s));
+    ++launches;
+    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    DS_CK(cudaStreamSynchronize(s));
+    const unsigned long long need = c->h_scalars->words_count;
+    if (need <= c->words_cap) break;
+    // regrow to the exact requirement (+6%) and evaluate the tiles again
+    const unsigned long long grow = need + need / 16 + 1024;
+    const int64_t required = (int64_t)(base + grow * 16);
+    if (mem_cap > 0 && required > mem_cap) {
+      set_capacity((int64_t)(base + need * 16), mem_cap);
+      set_error("adjacency words exceed the memory cap");
+      return DS_ECAPACITY;
+    }
+    if (c->words.bytes < grow * 16) {
+      if (c->words.p) cudaFree(c->words.p);
+      c->words.p = nullptr;
+      c->words.bytes = 0;
+      DS_CK(ensure(c->words, grow * 16));
+    }
+    c->words_cap = grow;
+  }
+  if (t) {
+    t->tile_launches = launches;
+    t->tiles_total = items;
+    t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;
+    t->words_emitted = (int64_t)c->h_scalars->words_count;
+    t->unsafe_range = c->h_scalars->unsafe_flag ? 1 : 0;
+    // every item evaluates the full 512 x 512 pair block (ragged edges masked)
+    t->pairs_evaluated = items * (int64_t)TILE * TILE;
+  }
+  return DS_OK;
+}
+
+ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
+                   int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
+                   int64_t* d_counts64, cudaStream_t s, ds_timings* t) {
+  DS_CK(cudaEventRecord(c->ev[0], s));
+  ds_status st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, t);
+  if (st != DS_OK) return st;
+  MergeWs w = merge_ws(c, n);
+  Scalars* sc = (Scalars*)c->scalars.p;
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(launch_union_words(w, (const uint4*)c->words.p, &sc->words_count, c->words_cap, s));
+  DS_CK(launch_finalize(w, d_labels, s));
+  if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, d_counts64, s));
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  if (t) {
+    float f = 0, m = 0, k = 0;
+    DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
+    DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
+    DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    t->fused_ms = f;
+    t->merge_ms = m;
+    t->tile_ms = k;
+    t->core_count = (int64_t)c->h_scalars->ncore;
+    t->cluster_count = c->h_scalars->nclusters;
+    t->device_bytes = (int64_t)held_bytes(c);
+  }
+  return DS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ds_abi_version(void) { return DS_ABI_VERSION; }
+
+const char* ds_build_info(void) {
+  return "densescan_b200 sm_100a; eps-tile kernel TILE=512, TMA bulk staging, sign-bit packing; "
+         "union-find merge; built with nvcc " __DATE__;
+}
+
+const char* ds_last_error(void) { return g_error.c_str(); }
+
+void ds_last_capacity(int64_t* required_bytes, int64_t* cap_bytes) {
+  if (required_bytes) *required_bytes = g_required;
+  if (cap_bytes) *cap_bytes = g_cap;
+}
+
+ds_status ds_ctx_create(int device, ds_ctx** out) {
+  if (!out) {
+    set_error("out: NULL");
+    return DS_EINVAL;
+  }
+  *out = nullptr;
+  int count = 0;
+  DS_CK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) {
+    set_error("device: ordinal out of range");
+    return DS_EINVAL;
+  }
+  DS_CK(cudaSetDevice(device));
+  ds_ctx* c = new ds_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  for (int i = 0; e == cudaSuccess && i < 8; ++i) e = cudaEventCreate(&c->ev[i]);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scalars, sizeof(Scalars));
+  if (e != cudaSuccess) {
+    set_error(std::string("context creation failed: ") + cudaGetErrorString(e));
+    ds_ctx_destroy(c);
+    return DS_ECUDA;
+  }
+  *out = c;
+  return DS_OK;
+}
+
+void ds_ctx_destroy(ds_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  Buf* all[] = {&c->coords64, &c->rec,    &c->cnt,    &c->core,   &c->corew,    &c->parent,
+                &c->bmin,     &c->cmin,   &c->root,   &c->flag,   &c->partials, &c->labels,
+                &c->counts64, &c->words,  &c->scalars, &c->dense};
+  for (Buf* b : all)
+    if (b->p) cudaFree(b->p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->h_scalars) cudaFreeHost(c->h_scalars);
+  delete c;
+}
+
+ds_status ds_run_dbscan_device(ds_ctx* c, const double* d_coords, int64_t n, int32_t d,
+                               double eps_sq, int64_t min_pts, int32_t formula, int64_t mem_cap,
+                               int64_t* d_labels, void* stream, ds_timings* t) {
+  if (!c || !d_coords || !d_labels) {
+    set_error("ctx, d_coords and d_labels must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, min_pts, formula);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  ds_timings local{};
+  st = pipeline(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap, d_labels, nullptr,
+                (cudaStream_t)stream, &local);
+  local.total_ms = now_ms() - t0;
+  if (t) *t = local;
+  return st;
+}
+
+ds_status ds_run_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, double eps_sq,
+                        int64_t min_pts, int32_t formula, int64_t mem_cap, int64_t* labels_out,
+                        int64_t* counts_out, ds_timings* t) {
+  if (!c || !coords || !labels_out) {
+    set_error("ctx, coords and labels_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, min_pts, formula);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  ds_timings local{};
+  const size_t in_bytes = (size_t)n * d * 8;
+  DS_CK(ensure(c->coords64, in_bytes));
+  DS_CK(ensure(c->labels, (size_t)n * 8));
+  if (counts_out) DS_CK(ensure(c->counts64, (size_t)n * 8));
+  cudaStream_t s = c->stream;
+  DS_CK(cudaEventRecord(c->ev[5], s));
+  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
+  DS_CK(cudaEventRecord(c->ev[6], s));
+  st = pipeline(c, (const double*)c->coords64.p, n, d, eps_sq, min_pts, formula, mem_cap,
+                (int64_t*)c->labels.p, counts_out ? (int64_t*)c->counts64.p : nullptr, s, &local);
+  if (st != DS_OK) return st;
+  DS_CK(cudaEventRecord(c->ev[6], s));
+  DS_CK(cudaMemcpyAsync(labels_out, c->labels.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  if (counts_out)
+    DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaEventRecord(c->ev[7], s));
+  DS_CK(cudaStreamSynchronize(s));
+  float h2d = 0, d2h = 0;
+  DS_CK(cudaEventElapsedTime(&h2d, c->ev[5], c->ev[0]));
+  DS_CK(cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]));
+  local.h2d_ms = h2d;
+  local.d2h_ms = d2h;
+  local.total_ms = now_ms() - t0;
+  if (t) *t = local;
+  return DS_OK;
+}
+
+ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, double eps_sq,
+                         int64_t min_pts, int32_t formula, int64_t mem_cap, uint8_t* bits_out,
+                         int64_t* counts_out, uint8_t* valid_out, ds_timings* t) {
+  if (!c || !coords || !counts_out) {
+    set_error("ctx, coords and counts_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, min_pts, formula);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  ds_timings local{};
+  cudaStream_t s = c->stream;
+  const size_t in_bytes = (size_t)n * d * 8;
+  DS_CK(ensure(c->coords64, in_bytes));
+  DS_CK(ensure(c->counts64, (size_t)n * 8));
+  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
+  DS_CK(cudaEventRecord(c->ev[0], s));
+  st = stage12(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, &local);
+  if (st != DS_OK) return st;
+  DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, (int64_t*)c->counts64.p, s));
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  if (bits_out) {
+    const int64_t stride = (n + 31) / 32;  // words per row
+    const size_t dense = (size_t)n * stride * 4;
+    DS_CK(ensure(c->dense, dense));
+    DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
+    Scalars* sc = (Scalars*)c->scalars.p;
+    DS_CK(launch_export_bits((const uint4*)c->words.p, &sc->words_count, c->words_cap,
+                             (uint32_t*)c->dense.p, stride, s));
+    DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
+    const size_t row_bytes = (size_t)(n + 7) / 8;
+    DS_CK(cudaMemcpy2DAsync(bits_out, row_bytes, c->dense.p, stride * 4, row_bytes, (size_t)n,
+                            cudaMemcpyDeviceToHost, s));
+  }
+  DS_CK(cudaStreamSynchronize(s));
+  if (valid_out)
+    for (int64_t i = 0; i < n; ++i) valid_out[i] = counts_out[i] >= min_pts ? 1 : 0;
+  float f = 0, k = 0;
+  DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
+  DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+  local.fused_ms = f;
+  local.tile_ms = k;
+  local.device_bytes = (int64_t)held_bytes(c);
+  local.total_ms = now_ms() - t0;
+  if (t) *t = local;
+  return DS_OK;
+}
+
+ds_status ds_merge_bits(ds_ctx* c, const uint8_t* bits, const int64_t* counts, const uint8_t* valid,
+                        int64_t n, int64_t min_pts, int64_t* labels_out, ds_timings* t) {
+  if (!c || !bits || !counts || !valid || !labels_out) {
+    set_error("ctx, bits, counts, valid and labels_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  for (int64_t i = 0; i < n; ++i) {
+    if ((counts[i] >= min_pts) != (valid[i] != 0)) {  // merge.py:141-145
+      set_error("valid[" + std::to_string(i) + "] disagrees with neighbor_count[" +
+                std::to_string(i) + "] >= min_pts");
+      return DS_EINCONSISTENT;
+    }
+  }
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  ds_timings local{};
+  cudaStream_t s = c->stream;
+  st = alloc_common(c, n, 1);
+  if (st != DS_OK) return st;
+  std::vector<int32_t> cnt32((size_t)n);
+  for (int64_t i = 0; i < n; ++i) cnt32[i] = (int32_t)std::min<int64_t>(counts[i], 0x7fffffff);
+  const int64_t stride = (n + 31) / 32;
+  const size_t dense = (size_t)n * stride * 4;
+  const size_t row_bytes = (size_t)(n + 7) / 8;
+  DS_CK(ensure(c->dense, dense));
+  DS_CK(ensure(c->labels, (size_t)n * 8));
+  DS_CK(cudaEventRecord(c->ev[0], s));
+  DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
+  DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
+  DS_CK(cudaMemcpy2DAsync(c->dense.p, stride * 4, bits, row_bytes, row_bytes, (size_t)n,
+                          cudaMemcpyHostToDevice, s));
+  DS_CK(cudaMemcpyAsync(c->cnt.p, cnt32.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
+  MergeWs w = merge_ws(c, n);
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(launch_union_dense(w, (const uint32_t*)c->dense.p, stride, s));
+  DS_CK(launch_finalize(w, (int64_t*)c->labels.p, s));
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  DS_CK(cudaMemcpyAsync(labels_out, c->labels.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  float m = 0;
+  DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
+  local.merge_ms = m;
+  local.core_count = (int64_t)c->h_scalars->ncore;
+  local.cluster_count = c->h_scalars->nclusters;
+  local.device_bytes = (int64_t)held_bytes(c);
+  local.total_ms = now_ms() - t0;
+  if (t) *t = local;
+  return DS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// Internal declarations shared by the densescan_b200 translation units.
+//
+// Data layout in HBM:
+//   rec      float32 [n][S]      S = roundup4(d+1): d narrowed coordinates, then the
+//                                squared norm P (algebraic formula), zero pad.
+//   cnt      int32   [n]         neighbour counts incl. self (kernels.py:331)
+//   core     uint8   [n]         cnt >= min_pts            (kernels.py:335)
+//   corew    uint32  [ceil(n/32)] core flags as adjacency words (bit 31-t <-> point 32w+t)
+//   words    uint4   [cap]       {row i, column word jw, 32-bit adjacency word, 0}:
+//                                the non-zero words of the upper-triangle tiles, i.e. the
+//                                bit-packed neighbourhood matrix without its empty part
+//   parent   int32   [n]         union-find forest over core points (root = min index)
+//   bmin     int32   [n]         lowest in-range core of each non-core point
+//   root/cmin/flag/id int32 [n]  canonical relabel workspace
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/densescan_b200.h"
+
+namespace ds {
+
+// ---- tile geometry of the eps-tile kernel ---------------------------------------
+constexpr int TILE = 512;             // points per tile side
+constexpr int NT = 128;               // threads per CTA
+constexpr int KPT = TILE / NT;        // lane points owned by one thread
+constexpr int WPR = TILE / 32;        // adjacency words per point per tile
+constexpr int BSTRIDE = TILE + 8;     // smem stride of one word column (bank padding)
+constexpr int MAX_D = 64;
+constexpr int32_t NONE = 0x7fffffff;  // "no core" marker in bmin / cmin
+
+int padded_dim(int d);  // tile kernels are instantiated for d in {1,2,3,4,8,16,32,64}
+inline int rec_stride(int d) { return ((padded_dim(d) + 1) + 3) / 4 * 4; }
+inline int64_t n_tiles(int64_t n) { return (n + TILE - 1) / TILE; }
+inline int64_t n_items(int64_t T) { return T * (T + 1) / 2; }
+
+// coordinates beyond this magnitude could overflow float32 inside the pair
+// arithmetic (|d2| <= 4*d*max|c|^2); such inputs take the compare-based path
+constexpr float SAFE_ABS = 1.0e17f;
+
+struct TileArgs {
+  const float* rec;
+  int64_t n;
+  int32_t T;               // tiles per side
+  int32_t d;               // runtime dimension (generic instantiation only)
+  int64_t item_lo, item_hi;
+  unsigned long long* work_ctr;
+  float eps32;
+  int32_t* cnt;
+  uint4* words;
+  unsigned long long words_cap;
+  unsigned long long* words_count;
+  unsigned long long* nonempty_count;
+  const uint32_t* unsafe_flag;
+};
+
+// ---- launchers (ds_tile.cu) ---------------------------------------------------
+cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
+                        cudaStream_t s);
+cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream_t s);
+size_t tile_smem_bytes(int d);
+
+// ---- launchers (ds_merge.cu) --------------------------------------------------
+struct MergeWs {
+  int64_t n;
+  const int32_t* cnt;
+  uint8_t* core;
+  uint32_t* corew;
+  int32_t* parent;
+  int32_t* bmin;
+  int32_t* cmin;
+  int32_t* root;
+  int32_t* flag;          // flags, then exclusive scan (cluster ids)
+  int32_t* partials;      // scan block partials
+  int32_t* nclusters;     // device scalar
+  unsigned long long* ncore;
+};
+int64_t scan_partials_len(int64_t n);
+cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
+cudaError_t launch_union_words(const MergeWs& w, const uint4* words, const unsigned long long* count,
+                               unsigned long long cap, cudaStream_t s);
+cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
+                               cudaStream_t s);
+cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
+cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s);
+cudaError_t launch_export_bits(const uint4* words, const unsigned long long* count,
+                               unsigned long long cap, uint32_t* bits32, int64_t stride_words,
+                               cudaStream_t s);
+cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
+
+// ---- error plumbing (ds_api.cu) -----------------------------------------------
+void set_error(const std::string& msg);
+void set_capacity(int64_t required, int64_t cap);
+
+}  // namespace ds

@@ -1,0 +1,422 @@
+// Stage 2-3 of the densescan hot path on sm_100a: core flags, primitive-cluster
+// merge and canonical labels.
+//
+// Replaces merge_iterative (pkg/src/densescan/merge.py:133-166) and the
+// border rule _attach_borders (merge.py:116-130) plus canonicalize
+// (core.py:116-132). merge_iterative's clusters are the connected components
+// of the core-core in-range relation (SPEC.md merge contract),
+// so the merge is a lock-free union-find over core-core adjacency words:
+// atomicCAS hooks the larger root under the smaller one and finds halve the
+// path, hence every root is the minimum core index of its component and the
+// result is independent of atomic order. Non-core points take the label of
+// their lowest-indexed in-range core (atomicMin), exactly the reference tie
+// rule. Canonical ids (first appearance, i.e. lowest member index incl.
+// borders) come from an atomicMin per root plus an exclusive prefix scan.
+//
+// All kernels here are HBM/L2 bound: they stream the adjacency words once and
+// touch O(n) int32 arrays that stay L2-resident (4n <= 8 MB at C5).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ds_internal.cuh"
+
+namespace ds {
+namespace {
+
+constexpr int SCAN_T = 1024;
+constexpr int SCAN_PER = 4;
+constexpr int SCAN_BLK = SCAN_T * SCAN_PER;
+
+__device__ __forceinline__ int find_root(int32_t* parent, int v) {
+  volatile int32_t* p = parent;
+  int par = p[v];
+  if (par != v) {
+    int prev = v, next;
+    while (par > (next = p[par])) {  // parents only ever point to smaller indices
+      p[prev] = next;                // path halving (benign race: next is an ancestor)
+      prev = par;
+      par = next;
+    }
+  }
+  return par;
+}
+
+// Read-only find for the compress pass: a path-halving write racing with the
+// compress store could otherwise re-point an already compressed node at a
+// non-root ancestor.
+__device__ __forceinline__ int find_root_ro(const int32_t* parent, int v) {
+  const volatile int32_t* p = parent;
+  int par = p[v];
+  while (true) {
+    const int next = p[par];
+    if (next == par) return par;
+    par = next;
+  }
+}
+
+__device__ __forceinline__ void unite(int32_t* parent, int a, int b) {
+  int ra = find_root(parent, a);
+  int rb = find_root(parent, b);
+  while (ra != rb) {
+    if (ra < rb) {
+      const int t = ra;
+      ra = rb;
+      rb = t;
+    }
+    const int old = atomicCAS(&parent[ra], ra, rb);  // hook the larger root
+    if (old == ra) return;
+    ra = find_root(parent, old);
+    rb = find_root(parent, rb);
+  }
+}
+
+__global__ void core_init_kernel(const int32_t* __restrict__ cnt, int64_t n, int64_t min_pts,
+                                 uint8_t* __restrict__ core, uint32_t* __restrict__ corew,
+                                 int32_t* __restrict__ parent, int32_t* __restrict__ bmin,
+                                 int32_t* __restrict__ cmin, unsigned long long* ncore) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool c = i < n && (int64_t)cnt[i] >= min_pts;  // kernels.py:335
+  const uint32_t ballot = __ballot_sync(0xffffffffu, c);
+  if (i < n) {
+    core[i] = c ? 1 : 0;
+    parent[i] = (int32_t)i;
+    bmin[i] = NONE;
+    cmin[i] = NONE;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t w = i >> 5;
+    if (w * 32 < n) corew[w] = __brev(ballot);  // bit 31 - t <-> point 32w + t
+    if (ballot) atomicAdd(ncore, (unsigned long long)__popc(ballot));
+  }
+}
+
+// ---- union over adjacency words ---------------------------------------------------
+// Loads here are plain (L1-cacheable). An L1 copy of parent[] may be stale, but a
+// stale entry is still an ancestor (parents only move toward smaller indices), so
+// equal stale roots imply the same set, and every failed CAS returns a strictly
+// smaller fresh root: correctness and termination do not depend on coherence.
+__device__ __forceinline__ int find_plain(int32_t* parent, int v) {
+  int par = parent[v];
+  if (par != v) {
+    int prev = v, next;
+    while (par > (next = parent[par])) {
+      parent[prev] = next;  // path halving
+      prev = par;
+      par = next;
+    }
+  }
+  return par;
+}
+
+// Link the set holding root `r` with the set of node j; returns a root of the union.
+__device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
+  int rj = find_plain(parent, j);
+  while (r != rj) {
+    const int hi = r > rj ? r : rj;
+    const int lo = r > rj ? rj : r;
+    const int old = atomicCAS(&parent[hi], hi, lo);  // hook the larger root
+    if (old == hi) return lo;
+    r = find_plain(parent, old);
+    rj = find_plain(parent, lo);
+  }
+  return r;
+}
+
+// mode 0: every core-core bit; mode 1: only the first core-core bit of each word
+// (Afforest-style sampling: cheap links that make most later checks one load);
+// borders are resolved in mode 0 only.
+template <int MODE>
+__global__ void union_words_kernel(const uint4* __restrict__ words,
+                                   const unsigned long long* __restrict__ count,
+                                   unsigned long long cap, const uint8_t* __restrict__ core,
+                                   const uint32_t* __restrict__ corew, int32_t* parent,
+                                   int32_t* bmin) {
+  unsigned long long total = *count;
+  if (total > cap) total = cap;
+  for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+       r += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 rec = words[r];
+    const int i = (int)rec.x;
+    const int jw = (int)rec.y;
+    const uint32_t x = rec.z;
+    const uint32_t cw = corew[jw];
+    if (core[i]) {
+      uint32_t um = x & cw;  // core-core: same cluster (merge.py:149-159)
+      if (um) {
+        int ri = find_plain(parent, i);
+        if (MODE == 1) um &= 0x80000000u >> __clz(um);
+        while (um) {
+          const int t = __clz(um);
+          um &= ~(0x80000000u >> t);
+          const int j = jw * 32 + t;
+          if (parent[j] == ri) continue;  // already linked: one (usually L1) load
+          ri = link_root(parent, ri, j);
+        }
+      }
+      if (MODE == 0) {
+        uint32_t bm = x & ~cw;  // core i in range of non-core j: border candidate
+        while (bm) {
+          const int t = __clz(bm);
+          bm &= ~(0x80000000u >> t);
+          atomicMin(&bmin[jw * 32 + t], i);
+        }
+      }
+    } else if (MODE == 0) {
+      const uint32_t cm = x & cw;  // lowest in-range core of non-core i (merge.py:116-130)
+      if (cm) atomicMin(&bmin[i], jw * 32 + __clz(cm));
+    }
+  }
+}
+
+// Dense rows (reference NeighborhoodMatrix converted to native words): one warp per row.
+__global__ void union_dense_kernel(const uint32_t* __restrict__ bits32, int64_t stride_words,
+                                   int64_t n, const uint8_t* __restrict__ core,
+                                   const uint32_t* __restrict__ corew, int32_t* parent,
+                                   int32_t* bmin) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (n + 31) / 32;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t* row = bits32 + i * stride_words;
+    const bool ci = core[i] != 0;
+    int best = NONE;
+    for (int64_t k = lane; k < nw; k += 32) {
+      const uint32_t m = row[k] & corew[k];
+      if (!m) continue;
+      if (ci) {
+        uint32_t um = m;
+        while (um) {
+          const int t = __clz(um);
+          um &= ~(0x80000000u >> t);
+          unite(parent, (int)i, (int)(k * 32 + t));
+        }
+      } else if (best == NONE) {
+        best = (int)(k * 32 + __clz(m));
+      }
+    }
+    if (!ci) {
+#pragma unroll
+      for (int off = 16; off; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
+      if (lane == 0 && best != NONE) bmin[i] = best;
+    }
+  }
+}
+
+__global__ void compress_kernel(const uint8_t* __restrict__ core, int64_t n, int32_t* parent) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && core[i]) parent[i] = find_root_ro(parent, (int)i);
+}
+
+__global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __restrict__ parent,
+                             const int32_t* __restrict__ bmin, int64_t n,
+                             int32_t* __restrict__ root, int32_t* cmin) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int r = -1;
+  if (core[i]) {
+    r = parent[i];
+  } else {
+    const int b = bmin[i];
+    if (b != NONE) r = parent[b];
+  }
+  root[i] = r;
+  if (r >= 0) atomicMin(&cmin[r], (int)i);  // first appearance of the cluster
+}
+
+__global__ void flags_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
+                             int64_t n, int32_t* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = root[i];
+  flag[i] = (r >= 0 && cmin[r] == (int)i) ? 1 : 0;
+}
+
+// block-wide exclusive scan of one int per thread; also returns the block total
+__device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
+  __shared__ int warp_sums[32];
+  __shared__ int tot;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int s = lane < nw ? warp_sums[lane] : 0;
+    int si = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, si, off);
+      if (lane >= off) si += y;
+    }
+    if (lane < nw) warp_sums[lane] = si - s;
+    if (lane == nw - 1) tot = si;
+  }
+  __syncthreads();
+  total = tot;
+  const int excl = warp_sums[wid] + incl - v;
+  __syncthreads();  // the shared slots may be reused by the caller's next call
+  return excl;
+}
+
+__global__ void scan_partials_kernel(const int32_t* __restrict__ flag, int64_t n,
+                                     int32_t* __restrict__ partials) {
+  const int64_t base = (int64_t)blockIdx.x * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k)
+    if (base + k < n) s += flag[base + k];
+  int total;
+  block_exclusive_scan(s, total);
+  if (threadIdx.x == 0) partials[blockIdx.x] = total;
+}
+
+__global__ void scan_top_kernel(int32_t* partials, int64_t np, int32_t* total_out) {
+  int carry = 0;
+  for (int64_t c0 = 0; c0 < np; c0 += SCAN_T) {
+    const int64_t idx = c0 + threadIdx.x;
+    const int v = idx < np ? partials[idx] : 0;
+    int total;
+    const int excl = block_exclusive_scan(v, total);
+    if (idx < np) partials[idx] = carry + excl;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total_out = carry;
+}
+
+__global__ void scan_apply_kernel(int32_t* flag, int64_t n, const int32_t* __restrict__ partials) {
+  const int64_t base = (int64_t)blockIdx.x * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
+  int v[SCAN_PER];
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    v[k] = base + k < n ? flag[base + k] : 0;
+    s += v[k];
+  }
+  int total;
+  int run = block_exclusive_scan(s, total) + partials[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    if (base + k < n) flag[base + k] = run;
+    run += v[k];
+  }
+}
+
+__global__ void label_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
+                             const int32_t* __restrict__ id, int64_t n, int64_t* __restrict__ labels) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int r = root[i];
+  labels[i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
+}
+
+__global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = cnt[i];
+}
+
+// words -> dense native-word rows, both orientations (the tile list only holds a <= b)
+__global__ void export_bits_kernel(const uint4* __restrict__ words,
+                                   const unsigned long long* __restrict__ count,
+                                   unsigned long long cap, uint32_t* bits32, int64_t stride_words) {
+  unsigned long long total = *count;
+  if (total > cap) total = cap;
+  for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+       r += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 rec = words[r];
+    const int64_t i = rec.x;
+    const int64_t jw = rec.y;
+    uint32_t x = rec.z;
+    atomicOr(&bits32[i * stride_words + jw], x);
+    while (x) {
+      const int t = __clz(x);
+      x &= ~(0x80000000u >> t);
+      const int64_t j = jw * 32 + t;
+      atomicOr(&bits32[j * stride_words + (i >> 5)], 0x80000000u >> (i & 31));
+    }
+  }
+}
+
+// native word (bit 31 = first column) <-> little-endian bytes of numpy packbits rows
+__global__ void bswap_kernel(uint32_t* bits32, int64_t total) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x)
+    bits32[k] = __byte_perm(bits32[k], 0, 0x0123);
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+int64_t scan_partials_len(int64_t n) { return (n + SCAN_BLK - 1) / SCAN_BLK; }
+
+cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) {
+  const int t = 256;
+  core_init_kernel<<<blocks_for(w.n, t), t, 0, s>>>(w.cnt, w.n, min_pts, w.core, w.corew,
+                                                    w.parent, w.bmin, w.cmin, w.ncore);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_union_words(const MergeWs& w, const uint4* words,
+                               const unsigned long long* count, unsigned long long cap,
+                               cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int t = 256;
+  union_words_kernel<1><<<sms * 8, t, 0, s>>>(words, count, cap, w.core, w.corew, w.parent, w.bmin);
+  compress_kernel<<<blocks_for(w.n, t), t, 0, s>>>(w.core, w.n, w.parent);
+  union_words_kernel<0><<<sms * 8, t, 0, s>>>(words, count, cap, w.core, w.corew, w.parent, w.bmin);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
+                               cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  union_dense_kernel<<<sms * 8, 256, 0, s>>>(bits32, stride_words, w.n, w.core, w.corew, w.parent,
+                                             w.bmin);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
+  const int t = 256;
+  const unsigned b = blocks_for(w.n, t);
+  compress_kernel<<<b, t, 0, s>>>(w.core, w.n, w.parent);
+  roots_kernel<<<b, t, 0, s>>>(w.core, w.parent, w.bmin, w.n, w.root, w.cmin);
+  flags_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.n, w.flag);
+  const int64_t np = scan_partials_len(w.n);
+  scan_partials_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
+  scan_top_kernel<<<1, SCAN_T, 0, s>>>(w.partials, np, w.nclusters);
+  scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
+  label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, labels);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s) {
+  counts_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(cnt, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_bits(const uint4* words, const unsigned long long* count,
+                               unsigned long long cap, uint32_t* bits32, int64_t stride_words,
+                               cudaStream_t s) {
+  export_bits_kernel<<<148 * 8, 256, 0, s>>>(words, count, cap, bits32, stride_words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s) {
+  const int64_t total = n * stride_words;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  bswap_kernel<<<(unsigned)blocks, 256, 0, s>>>(bits32, total);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

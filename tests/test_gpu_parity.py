@@ -1,0 +1,218 @@
+"""GPU parity: the sm_100a path against the reference's golden outputs and the oracle.
+
+Bar: bit-exact. Neighbourhood bits, int64 counts and canonical
+labels must be identical to what the reference package computes with the same
+formula (FUSED_ALGEBRAIC -> algebraic, FUSED -> direct), including exact ties,
+large offsets where the two formulas disagree, ragged tile edges and
+unfiltered eps.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden, pad3, random_specs
+
+pytestmark = pytest.mark.gpu
+
+FORMULAS = {"alg": 1, "dir": 0}
+
+
+@pytest.fixture(scope="module")
+def ds():
+    import paper_1506_02226_b200 as pkg
+    from paper_1506_02226_b200 import _native
+    _native.load_library()
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    from oracle import densescan_oracle
+    return densescan_oracle
+
+
+def variant(ds, fname):
+    vid = ds.VariantId.FUSED_ALGEBRAIC if fname == "alg" else ds.VariantId.FUSED
+    return ds.KernelVariant(vid)
+
+
+def gpu_stage12(ds, coords, eps, eps_sq, min_pts, fname, want_bits=True):
+    ctx = ds._native.context()
+    bits, counts, valid, _ = ctx.fused_build(coords, eps_sq, min_pts, FORMULAS[fname], 0,
+                                             want_bits=want_bits)
+    return bits, counts, valid
+
+
+def gpu_labels(ds, coords, eps, eps_sq, min_pts, fname):
+    params = ds.DbscanParams(eps=eps, eps_sq=eps_sq, min_pts=min_pts)
+    cfg = ds.PipelineConfig(variant=variant(ds, fname))
+    labeling, _ = ds.run_dbscan(ds.PointSet(coords), params, cfg)
+    return labeling.labels
+
+
+def sha(bits):
+    return hashlib.sha256(np.ascontiguousarray(bits).tobytes()).hexdigest()
+
+
+# ---- reference golden vectors ------------------------------------------------------
+def test_kat_cases(ds):
+    g = load_golden("kat.npz")
+    for name, pts, eps, eps_sq, min_pts in golden_cases(g):
+        for fname in FORMULAS:
+            bits, counts, valid = gpu_stage12(ds, pts, eps, eps_sq, min_pts, fname)
+            assert sha(bits) == str(g[f"{name}/{fname}/bits_sha"]), (name, fname)
+            assert np.array_equal(counts, g[f"{name}/{fname}/counts"]), (name, fname)
+            labels = gpu_labels(ds, pts, eps, eps_sq, min_pts, fname)
+            assert np.array_equal(labels, g[f"{name}/{fname}/labels"]), (name, fname)
+
+
+@pytest.mark.parametrize("native_2d", [True, False])
+def test_c1_full(ds, native_2d):
+    g = load_golden("c1.npz")
+    pts = ds.generate_blobs(10_000, 4, 0.5, 0.0, 1, 2).coords_aos
+    if not native_2d:
+        pts = pad3(pts)
+    for fname in FORMULAS:
+        bits, counts, _ = gpu_stage12(ds, pts, 0.3, 0.3 * 0.3, 4, fname)
+        assert np.array_equal(bits[:64], g[f"{fname}/bits_rows0_64"])
+        assert sha(bits) == str(g[f"{fname}/bits_sha"])
+        assert np.array_equal(counts, g[f"{fname}/counts"])
+        labels = gpu_labels(ds, pts, 0.3, 0.3 * 0.3, 4, fname)
+        assert np.array_equal(labels, g[f"{fname}/labels"])
+
+
+@pytest.mark.parametrize("fixture", ["lattice.npz", "random.npz"])
+def test_boundary_dense_and_random(ds, fixture):
+    g = load_golden(fixture)
+    cases = golden_cases(g) if fixture == "lattice.npz" else random_specs(g)
+    seen = 0
+    for name, pts, eps, eps_sq, min_pts in cases:
+        for fname in FORMULAS:
+            bits, counts, _ = gpu_stage12(ds, pts, eps, eps_sq, min_pts, fname)
+            assert sha(bits) == str(g[f"{name}/{fname}/bits_sha"]), (fixture, name, fname)
+            assert np.array_equal(counts, g[f"{name}/{fname}/counts"]), (name, fname)
+            labels = gpu_labels(ds, pts, eps, eps_sq, min_pts, fname)
+            assert np.array_equal(labels, g[f"{name}/{fname}/labels"]), (name, fname)
+        seen += 1
+    assert seen > 0
+
+
+def test_blob23040(ds):
+    g = load_golden("blob23040.npz")
+    pts = ds.generate_blobs(23040, 3, 0.03, 0.02, 1).coords_aos
+    for fname in FORMULAS:
+        _, counts, _ = gpu_stage12(ds, pts, 0.1, 0.01, 8, fname, want_bits=False)
+        assert np.array_equal(counts, g[f"{fname}/counts"])
+        labels = gpu_labels(ds, pts, 0.1, 0.1 * 0.1, 8, fname)
+        assert np.array_equal(labels, g[f"{fname}/labels"])
+
+
+def test_c2_full_reference_labels(ds):
+    g = load_golden("c2.npz")
+    cfg = ds.CONFIGS["C2"]
+    pts = cfg.points()
+    params = ds.validate_params(cfg.eps, cfg.min_pts)
+    labeling, _ = ds.run_dbscan(pts, params, ds.default_config())
+    assert np.array_equal(labeling.labels, g["labels"])
+    _, counts, _ = gpu_stage12(ds, pts.coords_aos, cfg.eps, params.eps_sq, cfg.min_pts, "alg",
+                               want_bits=False)
+    assert np.array_equal(counts, g["counts"])
+
+
+# ---- oracle comparisons beyond the reference's reach ---------------------------------
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 13, 16, 17, 33])
+@pytest.mark.parametrize("fname", ["alg", "dir"])
+def test_oracle_any_dimension(ds, oracle, rng, d, fname):
+    for n in (1, 2, 31, 511, 512, 513, 1500):
+        k = int(rng.integers(1, min(4, n) + 1))
+        pts = ds.generate_blobs(n, k, 0.3, 0.2, int(rng.integers(2**31)), d).coords_aos
+        pts = pts * rng.choice([1.0, 7.0]) + rng.choice([0.0, 50.0])
+        eps = float(rng.uniform(0.2, 1.2)) * np.sqrt(d / 2.0)
+        eps_sq = eps * eps
+        min_pts = int(rng.integers(1, 10))
+        bits, counts, _ = gpu_stage12(ds, pts, eps, eps_sq, min_pts, fname)
+        obits, ocounts = oracle.neighborhood(pts, eps_sq, FORMULAS[fname])
+        assert np.array_equal(bits, obits), (d, n, fname)
+        assert np.array_equal(counts, ocounts), (d, n, fname)
+        labels = gpu_labels(ds, pts, eps, eps_sq, min_pts, fname)
+        want, _ = oracle.dbscan(pts, eps_sq, min_pts, FORMULAS[fname])
+        assert np.array_equal(labels, want), (d, n, fname)
+
+
+def test_padding_is_bit_neutral(ds):
+    pts = ds.generate_blobs(3000, 5, 0.4, 0.1, 11, 2).coords_aos
+    for fname in FORMULAS:
+        a = gpu_labels(ds, pts, 0.25, 0.0625, 5, fname)
+        b = gpu_labels(ds, pad3(pts), 0.25, 0.0625, 5, fname)
+        assert np.array_equal(a, b)
+
+
+def test_overflow_range_uses_exact_compare(ds, oracle, rng):
+    # squares overflow float32: the NaN/inf semantics must follow numpy's
+    pts = rng.normal(size=(700, 2)) * 1e19
+    pts[:5] = rng.normal(size=(5, 2))
+    for fname in FORMULAS:
+        eps_sq = 1e38
+        bits, counts, _ = gpu_stage12(ds, pts, 1e19, eps_sq, 2, fname)
+        obits, ocounts = oracle.neighborhood(pts, eps_sq, FORMULAS[fname])
+        assert np.array_equal(bits, obits)
+        assert np.array_equal(counts, ocounts)
+
+
+def test_merge_from_reference_bits(ds, oracle, rng):
+    g = load_golden("kat.npz")
+    for name, pts, eps, eps_sq, min_pts in golden_cases(g):
+        key = f"{name}/alg/bits"
+        if key not in g:
+            continue
+        bits = g[key]
+        counts = g[f"{name}/alg/counts"].astype(np.int64)
+        nbr = ds.NeighborhoodMatrix(n=counts.size, bits=bits, neighbor_count=counts)
+        valid = ds.ValidVector(valid=counts >= min_pts, min_pts=min_pts)
+        assert np.array_equal(ds.merge_iterative(nbr, valid).labels, g[f"{name}/alg/labels"])
+        assert np.array_equal(ds.merge_warshall(nbr, valid).labels, g[f"{name}/alg/labels"])
+    pts = ds.generate_blobs(2000, 3, 0.1, 0.2, 3, 2)
+    params = ds.validate_params(0.05, 4)
+    nbr, valid = ds.fused_build_algebraic(pts, params,
+                                          ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC))
+    want, _ = oracle.dbscan(pts.coords_aos, params.eps_sq, 4, 1)
+    assert np.array_equal(ds.merge_iterative(nbr, valid).labels, want)
+    valid.valid[0] = not valid.valid[0]
+    with pytest.raises(ds.InconsistentInput):
+        ds.merge_iterative(nbr, valid)
+
+
+def test_determinism_and_permutation(ds, oracle, rng):
+    pts = ds.generate_blobs(20_000, 9, 0.5, 0.1, 5, 2)
+    params = ds.validate_params(0.12, 6)
+    first, _ = ds.run_dbscan(pts, params, ds.default_config())
+    for _ in range(3):
+        again, _ = ds.run_dbscan(pts, params, ds.default_config())
+        assert np.array_equal(first.labels, again.labels)
+    # permuting the input permutes the core partition; border ties follow the new
+    # index order (lowest in-range core), so compare those against the oracle
+    perm = rng.permutation(pts.n)
+    coords = pts.coords_aos[perm]
+    permuted, _ = ds.run_dbscan(ds.PointSet(coords), params, ds.default_config())
+    want, counts = oracle.dbscan(coords, params.eps_sq, 6, 1)
+    assert np.array_equal(permuted.labels, want)
+    core = counts >= 6
+    a = ds.canonicalize(ds.Labeling(np.where(core, first.labels[perm], -1))).labels
+    b = ds.canonicalize(ds.Labeling(np.where(core, permuted.labels, -1))).labels
+    assert np.array_equal(a, b)
+
+
+def test_capacity_regrow_and_error(ds):
+    # a dense blob emits many words: a small cap must raise, a generous one regrows
+    pts = ds.generate_blobs(6000, 1, 0.05, 0.0, 1, 2)
+    params = ds.validate_params(0.5, 4)
+    with pytest.raises(ds.CapacityExceeded) as exc:
+        ds.run_dbscan(pts, params, ds.PipelineConfig(
+            variant=ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC), mem_cap=2_000_000))
+    assert exc.value.cap_bytes == 2_000_000 and exc.value.required_bytes > 2_000_000
+    labeling, t = ds.run_dbscan(pts, params, ds.default_config())
+    assert labeling.cluster_count() == 1 and t.words_emitted > 0
