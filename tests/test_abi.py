@@ -1,0 +1,102 @@
+"""The C-ABI library: it loads, exports exactly what include/densescan_b200.h
+declares, fails cleanly without a GPU, and its SASS honours the no-FMA rule.
+
+CPU-only (no kernel is executed here).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "densescan_b200.h")
+LIB = os.path.join(ROOT, "paper_1506_02226_b200", "libdensescan_b200.so")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(ds_[a-z_0-9]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_1506_02226_b200", "csrc")],
+                       check=True)
+    from paper_1506_02226_b200 import _native
+    return _native.load_library()
+
+
+def test_header_declares_the_binding_set():
+    from paper_1506_02226_b200 import _native
+    assert declared_symbols() == sorted(_native.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    if shutil.which("nm"):
+        out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True,
+                             text=True, check=True).stdout
+        exported = set(re.findall(r"\sT\s(ds_\w+)", out))
+        assert set(declared_symbols()) <= exported
+
+
+def test_abi_version_and_build_info(lib):
+    assert lib.ds_abi_version() == 1
+    assert b"sm_100a" in lib.ds_build_info()
+
+
+def test_context_creation_fails_cleanly_without_gpu(lib):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    handle = ctypes.c_void_p()
+    status = lib.ds_ctx_create(0, ctypes.byref(handle))
+    assert status != 0 and not handle.value
+    assert lib.ds_last_error()
+
+
+def test_null_arguments_are_rejected(lib):
+    assert lib.ds_ctx_create(0, None) == 1  # DS_EINVAL
+    assert lib.ds_run_dbscan(None, None, 0, 0, 0.0, 0, 0, 0, None, None, None) == 1
+
+
+def test_no_cpu_fallback_when_library_missing(tmp_path):
+    from paper_1506_02226_b200 import _native
+    saved = _native._lib
+    _native._lib = None
+    try:
+        with pytest.raises(ImportError, match="no CPU fallback"):
+            _native.load_library(str(tmp_path / "missing.so"))
+    finally:
+        _native._lib = saved
+
+
+@pytest.mark.skipif(not shutil.which("cuobjdump"), reason="cuobjdump not available")
+def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
+    """Parity needs every product and sum rounded separately: the eps-tile
+    kernels must contain no FFMA/FFMA2 (ptxas would otherwise be free to fuse
+    packed mul+add, SURVEY §0 finding 4), and they must use the packed FP32
+    instructions and the TMA bulk copy the design relies on."""
+    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True,
+                          check=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)
+    tile = [f for f in funcs if f.startswith("_ZN2ds") and "eps_tile_kernel" in f.split("\n")[0]]
+    assert len(tile) >= 16
+    for body in tile:
+        name = body.split("\n")[0]
+        assert not re.search(r"\bFFMA2?\b", body), name
+    k2 = [f for f in tile if "eps_tile_kernelILi2ELi1ELb1E" in f.split("\n")[0]]
+    assert k2 and "FMUL2" in k2[0] and "FADD2" in k2[0]
+    assert "UBLKCP" in k2[0] or "UTMALDG" in k2[0]
