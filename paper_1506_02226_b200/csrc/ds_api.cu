@@ -62,8 +62,8 @@ struct ds_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
-      words, scalars, dense;
-  unsigned long long words_cap = 0;  // in words (uint4 records)
+      words, chunks, scalars, dense;
+  unsigned long long words_cap = 0;  // in words (8-byte records)
   Scalars* h_scalars = nullptr;      // pinned
 };
 
@@ -87,7 +87,7 @@ cudaError_t ensure(Buf& b, size_t bytes) {
 size_t held_bytes(const ds_ctx* c) {
   const Buf* all[] = {&c->coords64, &c->rec, &c->cnt,   &c->core,     &c->corew,   &c->parent,
                       &c->bmin,     &c->cmin, &c->root, &c->flag,     &c->partials, &c->labels,
-                      &c->counts64, &c->words, &c->scalars, &c->dense};
+                      &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -122,10 +122,13 @@ ds_status check_args(int64_t n, int32_t d, int64_t min_pts, int32_t formula) {
   return DS_OK;
 }
 
+constexpr size_t WORD_BYTES = 8;  // one adjacency record
+
 // Bytes of every device buffer the pipeline needs except the adjacency words.
 size_t base_bytes(int64_t n, int d) {
   const size_t N = (size_t)n;
   return N * rec_stride(d) * 4      // rec
+         + (size_t)n_items(n_tiles(n)) * 16  // chunk table
          + N * 4 * 6                // cnt parent bmin cmin root flag
          + N                        // core
          + ((N + 31) / 32) * 4      // corew
@@ -163,6 +166,7 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->flag, N * 4));
   DS_CK(ensure(c->partials, (size_t)scan_partials_len(n) * 4));
   DS_CK(ensure(c->scalars, sizeof(Scalars)));
+  DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));
   return DS_OK;
 }
 
@@ -186,12 +190,12 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
       set_error("device workspace exceeds the memory cap");
       return DS_ECAPACITY;
     }
-    want = std::min<unsigned long long>(want, (unsigned long long)(room / 16));
+    want = std::min<unsigned long long>(want, (unsigned long long)(room / WORD_BYTES));
   }
-  if (c->words.bytes < want * 16) DS_CK(ensure(c->words, want * 16));
-  c->words_cap = c->words.bytes / 16;
+  if (c->words.bytes < want * WORD_BYTES) DS_CK(ensure(c->words, want * WORD_BYTES));
+  c->words_cap = c->words.bytes / WORD_BYTES;
   if (mem_cap > 0) {  // a buffer kept from an earlier, larger call must not bypass the cap
-    const unsigned long long room_words = (unsigned long long)((mem_cap - (int64_t)base) / 16);
+    const unsigned long long room_words = (unsigned long long)((mem_cap - (int64_t)base) / WORD_BYTES);
     c->words_cap = std::min(c->words_cap, room_words);
   }
 
@@ -215,9 +219,11 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     a.work_ctr = &sc->work_ctr;
     a.eps32 = eps32;
     a.cnt = (int32_t*)c->cnt.p;
-    a.words = (uint4*)c->words.p;
+    a.words = (uint2*)c->words.p;
     a.words_cap = c->words_cap;
     a.words_count = &sc->words_count;
+    a.chunks = (uint4*)c->chunks.p;
+    a.chunks_cap = (unsigned long long)items;
     a.nonempty_count = &sc->nonempty_count;
     a.unsafe_flag = &sc->unsafe_flag;
     DS_CK(cudaEventRecord(c->ev[1], s));
@@ -230,17 +236,17 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     if (need <= c->words_cap) break;
     // regrow to the exact requirement (+6%) and evaluate the tiles again
     const unsigned long long grow = need + need / 16 + 1024;
-    const int64_t required = (int64_t)(base + grow * 16);
+    const int64_t required = (int64_t)(base + grow * WORD_BYTES);
     if (mem_cap > 0 && required > mem_cap) {
-      set_capacity((int64_t)(base + need * 16), mem_cap);
+      set_capacity((int64_t)(base + need * WORD_BYTES), mem_cap);
       set_error("adjacency words exceed the memory cap");
       return DS_ECAPACITY;
     }
-    if (c->words.bytes < grow * 16) {
+    if (c->words.bytes < grow * WORD_BYTES) {
       if (c->words.p) cudaFree(c->words.p);
       c->words.p = nullptr;
       c->words.bytes = 0;
-      DS_CK(ensure(c->words, grow * 16));
+      DS_CK(ensure(c->words, grow * WORD_BYTES));
     }
     c->words_cap = grow;
   }
@@ -266,7 +272,8 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(launch_core_init(w, min_pts, s));
   DS_CK(cudaEventRecord(c->ev[3], s));
-  DS_CK(launch_union_words(w, (const uint4*)c->words.p, &sc->words_count, c->words_cap, s));
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, (const uint4*)c->chunks.p,
+                            &sc->nonempty_count, s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, d_counts64, s));
   DS_CK(cudaEventRecord(c->ev[4], s));
@@ -338,7 +345,7 @@ void ds_ctx_destroy(ds_ctx* c) {
   cudaSetDevice(c->device);
   Buf* all[] = {&c->coords64, &c->rec,    &c->cnt,    &c->core,   &c->corew,    &c->parent,
                 &c->bmin,     &c->cmin,   &c->root,   &c->flag,   &c->partials, &c->labels,
-                &c->counts64, &c->words,  &c->scalars, &c->dense};
+                &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -435,8 +442,8 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
     DS_CK(ensure(c->dense, dense));
     DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
     Scalars* sc = (Scalars*)c->scalars.p;
-    DS_CK(launch_export_bits((const uint4*)c->words.p, &sc->words_count, c->words_cap,
-                             (uint32_t*)c->dense.p, stride, s));
+    DS_CK(launch_export_bits((const uint2*)c->words.p, (const uint4*)c->chunks.p,
+                             &sc->nonempty_count, (uint32_t*)c->dense.p, stride, s));
     DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
     const size_t row_bytes = (size_t)(n + 7) / 8;
     DS_CK(cudaMemcpy2DAsync(bits_out, row_bytes, c->dense.p, stride * 4, row_bytes, (size_t)n,

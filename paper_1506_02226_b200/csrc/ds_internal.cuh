@@ -6,9 +6,11 @@
 //   cnt      int32   [n]         neighbour counts incl. self (kernels.py:331)
 //   core     uint8   [n]         cnt >= min_pts            (kernels.py:335)
 //   corew    uint32  [ceil(n/32)] core flags as adjacency words (bit 31-t <-> point 32w+t)
-//   words    uint4   [cap]       {row i, column word jw, 32-bit adjacency word, 0}:
-//                                the non-zero words of the upper-triangle tiles, i.e. the
-//                                bit-packed neighbourhood matrix without its empty part
+//   words    uint2   [cap]       {32-bit adjacency word, local row << 4 | column word}: the
+//                                non-zero words of the upper-triangle tile pairs, i.e. the
+//                                bit-packed neighbourhood matrix without its empty part,
+//                                grouped in one contiguous chunk per tile pair
+//   chunks   uint4   [items]     {a, b, first word lo, count | first word hi << 16}
 //   parent   int32   [n]         union-find forest over core points (root = min index)
 //   bmin     int32   [n]         lowest in-range core of each non-core point
 //   root/cmin/flag/id int32 [n]  canonical relabel workspace
@@ -50,10 +52,12 @@ struct TileArgs {
   unsigned long long* work_ctr;
   float eps32;
   int32_t* cnt;
-  uint4* words;
+  uint2* words;                        // {32-bit word, local row << 4 | column word}
   unsigned long long words_cap;
   unsigned long long* words_count;
-  unsigned long long* nonempty_count;
+  uint4* chunks;                       // {a, b, base lo, count | base hi << 16}
+  unsigned long long chunks_cap;
+  unsigned long long* nonempty_count;  // = chunks emitted
   const uint32_t* unsafe_flag;
 };
 
@@ -80,15 +84,15 @@ struct MergeWs {
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
-cudaError_t launch_union_words(const MergeWs& w, const uint4* words, const unsigned long long* count,
-                               unsigned long long cap, cudaStream_t s);
+cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint4* chunks,
+                                const unsigned long long* nchunks, cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s);
-cudaError_t launch_export_bits(const uint4* words, const unsigned long long* count,
-                               unsigned long long cap, uint32_t* bits32, int64_t stride_words,
-                               cudaStream_t s);
+cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
+                               const unsigned long long* nchunks, uint32_t* bits32,
+                               int64_t stride_words, cudaStream_t s);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
 // ---- error plumbing (ds_api.cu) -----------------------------------------------

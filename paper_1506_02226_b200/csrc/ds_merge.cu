@@ -122,49 +122,131 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
   return r;
 }
 
-// mode 0: every core-core bit; mode 1: only the first core-core bit of each word
-// (Afforest-style sampling: cheap links that make most later checks one load);
-// borders are resolved in mode 0 only.
-template <int MODE>
-__global__ void union_words_kernel(const uint4* __restrict__ words,
-                                   const unsigned long long* __restrict__ count,
-                                   unsigned long long cap, const uint8_t* __restrict__ core,
-                                   const uint32_t* __restrict__ corew, int32_t* parent,
-                                   int32_t* bmin) {
-  unsigned long long total = *count;
-  if (total > cap) total = cap;
-  for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
-       r += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint4 rec = words[r];
-    const int i = (int)rec.x;
-    const int jw = (int)rec.y;
-    const uint32_t x = rec.z;
-    const uint32_t cw = corew[jw];
-    if (core[i]) {
-      uint32_t um = x & cw;  // core-core: same cluster (merge.py:149-159)
-      if (um) {
-        int ri = find_plain(parent, i);
-        if (MODE == 1) um &= 0x80000000u >> __clz(um);
+// ---- union over tile-pair chunks (two rounds, shared-memory local forests) ---------
+// Round 1 (diagonal chunks, one per tile): the core-core words of tile a with
+// itself are merged in a shared-memory union-find over the tile's 512 points;
+// every core point then gets parent = its local root (the smallest index of
+// its local component). Each tile is owned by exactly one CTA, so these
+// writes need no atomics.
+// Round 2 (off-diagonal chunks): the 1024 points of tiles a and b first look
+// up their current global roots; a core-core bit whose endpoints already share
+// a root costs nothing, the others are merged in shared memory, and only one
+// global link per (local component, differing global root) is issued. In dense
+// regions that is ~1 global CAS per tile pair instead of one per in-range pair.
+// Border minima are reduced per chunk in shared memory, then once per point in
+// global memory.
+struct ChunkInfo {
+  int a, b;
+  unsigned long long base;
+  int count;
+};
+
+__device__ __forceinline__ ChunkInfo decode_chunk(uint4 c) {
+  ChunkInfo ci;
+  ci.a = (int)c.x;
+  ci.b = (int)c.y;
+  ci.base = (unsigned long long)c.z | ((unsigned long long)(c.w >> 16) << 32);
+  ci.count = (int)(c.w & 0xffffu);
+  return ci;
+}
+
+__device__ __forceinline__ int find_local(int* lp, int v) {
+  int p = lp[v];
+  while (p != v) {
+    const int gp = lp[p];
+    if (gp != p) lp[v] = gp;  // halving (smem; benign race)
+    v = p;
+    p = gp;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void unite_local(int* lp, int u, int v) {
+  for (;;) {
+    u = find_local(lp, u);
+    v = find_local(lp, v);
+    if (u == v) return;
+    if (u < v) {
+      const int t = u;
+      u = v;
+      v = t;
+    }
+    if (atomicCAS(&lp[u], u, v) == u) return;  // hook the larger local root
+  }
+}
+
+template <int ROUND>
+__global__ void __launch_bounds__(128) union_chunks_kernel(
+    const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
+    const uint2* __restrict__ words, int64_t n, const uint8_t* __restrict__ core,
+    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin) {
+  __shared__ int lp[2 * TILE];
+  __shared__ int gr[2 * TILE];
+  __shared__ int lb[2 * TILE];
+  __shared__ uint32_t lcw[2 * WPR];
+  const int tid = threadIdx.x;
+  const unsigned long long total = *nchunks;
+  const int64_t nw = (n + 31) / 32;
+  for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
+    const ChunkInfo ci = decode_chunk(chunks[c]);
+    const bool diag = ci.a == ci.b;
+    if ((ROUND == 1) != diag) continue;  // uniform per CTA
+    const int nloc = diag ? TILE : 2 * TILE;
+    for (int v = tid; v < nloc; v += blockDim.x) {
+      const int64_t g = (int64_t)(v < TILE ? ci.a : ci.b) * TILE + (v & (TILE - 1));
+      lp[v] = v;
+      lb[v] = NONE;
+      int r = (int)g;
+      if (ROUND == 2 && g < n && core[g]) r = find_plain(parent, (int)g);
+      gr[v] = r;
+    }
+    if (tid < (diag ? WPR : 2 * WPR)) {
+      const int64_t gw = (int64_t)(tid < WPR ? ci.a : ci.b) * WPR + (tid & (WPR - 1));
+      lcw[tid] = gw < nw ? corew[gw] : 0u;
+    }
+    __syncthreads();
+    const int jb = diag ? 0 : TILE;  // local index of column 0 of tile b
+    for (int k = tid; k < ci.count; k += blockDim.x) {
+      const uint2 rec = words[ci.base + k];
+      const uint32_t x = rec.x;
+      const int u = (int)(rec.y >> 4);
+      const int w = (int)(rec.y & 15u);
+      const uint32_t cw = lcw[(diag ? 0 : WPR) + w];
+      const bool cu = (lcw[u >> 5] >> (31 - (u & 31))) & 1u;
+      const int vb = jb + w * 32;
+      if (cu) {
+        uint32_t um = x & cw;  // core-core (merge.py:149-159)
         while (um) {
           const int t = __clz(um);
           um &= ~(0x80000000u >> t);
-          const int j = jw * 32 + t;
-          if (parent[j] == ri) continue;  // already linked: one (usually L1) load
-          ri = link_root(parent, ri, j);
+          const int v = vb + t;
+          if (ROUND == 1 || gr[u] != gr[v]) unite_local(lp, u, v);
         }
-      }
-      if (MODE == 0) {
-        uint32_t bm = x & ~cw;  // core i in range of non-core j: border candidate
+        uint32_t bm = x & ~cw;  // core u in range of non-core v (merge.py:116-130)
+        const int gu = ci.a * TILE + u;
         while (bm) {
           const int t = __clz(bm);
           bm &= ~(0x80000000u >> t);
-          atomicMin(&bmin[jw * 32 + t], i);
+          atomicMin(&lb[vb + t], gu);
         }
+      } else {
+        const uint32_t cm = x & cw;  // non-core u: its lowest in-range core
+        if (cm) atomicMin(&lb[u], (diag ? ci.a : ci.b) * TILE + w * 32 + __clz(cm));
       }
-    } else if (MODE == 0) {
-      const uint32_t cm = x & cw;  // lowest in-range core of non-core i (merge.py:116-130)
-      if (cm) atomicMin(&bmin[i], jw * 32 + __clz(cm));
     }
+    __syncthreads();
+    for (int v = tid; v < nloc; v += blockDim.x) {
+      const int64_t g = (int64_t)(v < TILE ? ci.a : ci.b) * TILE + (v & (TILE - 1));
+      if (g >= n) continue;
+      const int r = find_local(lp, v);
+      if (ROUND == 1) {
+        if (r != v) parent[g] = (int)((int64_t)ci.a * TILE + r);  // r < v: parent[x] <= x holds
+      } else if (r != v && gr[v] != gr[r]) {
+        link_root(parent, find_plain(parent, gr[v]), gr[r]);
+      }
+      if (lb[v] != NONE) atomicMin(&bmin[g], lb[v]);
+    }
+    __syncthreads();
   }
 }
 
@@ -319,24 +401,25 @@ __global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n, in
   if (i < n) out[i] = cnt[i];
 }
 
-// words -> dense native-word rows, both orientations (the tile list only holds a <= b)
-__global__ void export_bits_kernel(const uint4* __restrict__ words,
-                                   const unsigned long long* __restrict__ count,
-                                   unsigned long long cap, uint32_t* bits32, int64_t stride_words) {
-  unsigned long long total = *count;
-  if (total > cap) total = cap;
-  for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
-       r += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint4 rec = words[r];
-    const int64_t i = rec.x;
-    const int64_t jw = rec.y;
-    uint32_t x = rec.z;
-    atomicOr(&bits32[i * stride_words + jw], x);
-    while (x) {
-      const int t = __clz(x);
-      x &= ~(0x80000000u >> t);
-      const int64_t j = jw * 32 + t;
-      atomicOr(&bits32[j * stride_words + (i >> 5)], 0x80000000u >> (i & 31));
+// chunks -> dense native-word rows, both orientations (the chunks only hold a <= b)
+__global__ void export_bits_kernel(const uint2* __restrict__ words, const uint4* __restrict__ chunks,
+                                   const unsigned long long* __restrict__ nchunks, uint32_t* bits32,
+                                   int64_t stride_words) {
+  const unsigned long long total = *nchunks;
+  for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
+    const ChunkInfo ci = decode_chunk(chunks[c]);
+    for (int k = threadIdx.x; k < ci.count; k += blockDim.x) {
+      const uint2 rec = words[ci.base + k];
+      uint32_t x = rec.x;
+      const int64_t i = (int64_t)ci.a * TILE + (rec.y >> 4);
+      const int64_t jw = (int64_t)ci.b * WPR + (rec.y & 15u);
+      atomicOr(&bits32[i * stride_words + jw], x);
+      while (x) {
+        const int t = __clz(x);
+        x &= ~(0x80000000u >> t);
+        const int64_t j = jw * 32 + t;
+        atomicOr(&bits32[j * stride_words + (i >> 5)], 0x80000000u >> (i & 31));
+      }
     }
   }
 }
@@ -361,16 +444,15 @@ cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) 
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_words(const MergeWs& w, const uint4* words,
-                               const unsigned long long* count, unsigned long long cap,
-                               cudaStream_t s) {
+cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint4* chunks,
+                                const unsigned long long* nchunks, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int t = 256;
-  union_words_kernel<1><<<sms * 8, t, 0, s>>>(words, count, cap, w.core, w.corew, w.parent, w.bmin);
-  compress_kernel<<<blocks_for(w.n, t), t, 0, s>>>(w.core, w.n, w.parent);
-  union_words_kernel<0><<<sms * 8, t, 0, s>>>(words, count, cap, w.core, w.corew, w.parent, w.bmin);
+  union_chunks_kernel<1><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
+                                                 w.parent, w.bmin);
+  union_chunks_kernel<2><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
+                                                 w.parent, w.bmin);
   return cudaGetLastError();
 }
 
@@ -403,10 +485,10 @@ cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_export_bits(const uint4* words, const unsigned long long* count,
-                               unsigned long long cap, uint32_t* bits32, int64_t stride_words,
-                               cudaStream_t s) {
-  export_bits_kernel<<<148 * 8, 256, 0, s>>>(words, count, cap, bits32, stride_words);
+cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
+                               const unsigned long long* nchunks, uint32_t* bits32,
+                               int64_t stride_words, cudaStream_t s) {
+  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, chunks, nchunks, bits32, stride_words);
   return cudaGetLastError();
 }
 

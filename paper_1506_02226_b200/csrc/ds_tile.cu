@@ -30,7 +30,9 @@
 //   * words go to shared memory; the lane-side counts are popcounts of the
 //     words, the broadcast-side counts a bit-sliced (carry-save) vertical
 //     popcount of the same words; the non-zero words are appended to HBM for
-//     stage 3 after a block-wide prefix scan.
+//     stage 3 after a block-wide prefix scan, as one contiguous "chunk" per
+//     tile pair: 8-byte records {word, row << 4 | column word} plus a chunk
+//     entry {a, b, base, count}.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -473,7 +475,13 @@ eps_tile_kernel(const TileArgs args) {
           run += t2;
         }
         base_sh = run ? atomicAdd(args.words_count, (unsigned long long)run) : 0ull;
-        if (run) atomicAdd(args.nonempty_count, 1ull);
+        if (run) {
+          // one chunk per non-empty tile pair: its words are contiguous
+          const unsigned long long ci = atomicAdd(args.nonempty_count, 1ull);
+          if (ci < args.chunks_cap)
+            args.chunks[ci] = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)base_sh,
+                                         run | ((uint32_t)(base_sh >> 32) << 16));
+        }
       }
       __syncthreads();
       unsigned long long pos = base_sh + scan_sh[tid >> 5] + (incl - nz);
@@ -486,9 +494,7 @@ eps_tile_kernel(const TileArgs args) {
             x &= diag_keep(rel);
           }
           if (x) {
-            if (pos < args.words_cap)
-              args.words[pos] = make_uint4((uint32_t)((int64_t)a * TILE + il),
-                                           (uint32_t)((int64_t)b * WPR + w), x, 0u);
+            if (pos < args.words_cap) args.words[pos] = make_uint2(x, (uint32_t)(il << 4 | w));
             ++pos;
           }
         }
