@@ -153,6 +153,7 @@ def run_b200(args):
     import torch
     import paper_1506_02226_b200 as ds
     from paper_1506_02226_b200 import _native
+    from paper_1506_02226_b200 import distributed as D
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -160,7 +161,7 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = ds.CONFIGS[args.config]
     pts = cfg.points()
@@ -169,15 +170,30 @@ def run_b200(args):
     n, d = pts.n, pts.d
     mem_cap = 150 * 1024**3
     ctx = _native.context(local)
+    dev = f"cuda:{local}"
 
-    coords_dev = torch.from_numpy(pts.coords_aos.copy()).to(f"cuda:{local}")
-    labels_dev = torch.empty(n, dtype=torch.int64, device=f"cuda:{local}")
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    coords_dev = torch.from_numpy(pts.coords_aos.copy()).to(dev)
+    labels_dev = torch.empty(n, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    backend = D.NativeShardBackend(local) if world > 1 else None
 
     def step():
-        return ctx.run_dbscan_device(coords_dev.data_ptr(), n, d, params.eps_sq, params.min_pts,
-                                     formula, mem_cap, labels_dev.data_ptr(), stream.cuda_stream)
+        """One clustering of the resident points -> (tile_ms, pairs_evaluated, stage dict)."""
+        if world > 1:
+            labeling, tm = D.run_dbscan_sharded(None, params, formula=formula, mem_cap=mem_cap,
+                                                backend=backend, coords=coords_dev)
+            labels_dev.copy_(torch.from_numpy(labeling.labels))
+            return tm.tile_ms, tm.pairs_evaluated, {
+                "stage12": tm.stage12_ms, "exchange1": tm.exchange1_ms,
+                "stage3_local": tm.stage3_local_ms, "exchange2": tm.exchange2_ms,
+                "stage3_merge": tm.stage3_merge_ms, "tile": tm.tile_ms}, 1
+        t = ctx.run_dbscan_device(coords_dev.data_ptr(), n, d, params.eps_sq, params.min_pts,
+                                  formula, mem_cap, labels_dev.data_ptr(), stream.cuda_stream)
+        extra = {"words_emitted": t.words_emitted, "tiles_nonempty": t.tiles_nonempty,
+                 "tiles_total": t.tiles_total}
+        return t.tile_ms, t.pairs_evaluated, {"fused": t.fused_ms, "merge": t.merge_ms,
+                                               "tile": t.tile_ms, **extra}, t.tile_launches
 
     for _ in range(args.warmup):
         step()
@@ -193,40 +209,54 @@ def run_b200(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    times, tile_ms, tl = [], [], []
-    with ClockSampler(local) as clk:
+    times, tile_ms, last = [], [], None
+    clk = ClockSampler(local).__enter__()  # spans the device-timed and the e2e legs
+    if True:
         for _ in range(args.steps):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            t = step()
+            last = step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-            tile_ms.append(t.tile_ms)
-            tl.append(t)
+            tile_ms.append(last[0])
     torch.cuda.synchronize()
     ms = statistics.mean(times)
     if world > 1:
-        tt = torch.tensor([ms], device=f"cuda:{local}")
+        tt = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
-    last = tl[-1]
+    pairs = last[1]
 
     # end-to-end through the public API with host buffers
     e2e_ms = []
     cfg_api = ds.PipelineConfig(variant=ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC),
                                 mem_cap=mem_cap, device=local)
+
+    def e2e_step():
+        if world > 1:
+            return D.run_dbscan_sharded(pts, params, formula=formula, mem_cap=mem_cap,
+                                        backend=backend)
+        return ds.run_dbscan(pts, params, cfg_api)
+
     for _ in range(max(1, args.warmup)):
-        ds.run_dbscan(pts, params, cfg_api)
+        e2e_step()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        labeling, st = ds.run_dbscan(pts, params, cfg_api)
+        e2e_step()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e = statistics.mean(e2e_ms)
+    clk.__exit__(None, None, None)
+    if world > 1:
+        tt = torch.tensor([e2e], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(tt.item())
 
     peaks = load_peaks()
     clocks = clk.summary()
@@ -236,42 +266,42 @@ def run_b200(args):
     fp32_peak = sms * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12  # T lane-ops/s
     ops = algorithmic_ops_per_pair(d, formula)
     tile_s = statistics.mean(tile_ms) / 1e3
-    achieved = last.pairs_evaluated * ops / tile_s / 1e12
-    decisions = n * n  # ordered pair decisions produced per step (symmetry exploited)
-    launches_per_step = 12 + 2 * (last.tile_launches - 1)
+    achieved = pairs * ops / tile_s / 1e12
+    # kernels per step: prep, 2x eps-tile (one exits at once), core flags, 2 union rounds,
+    # 7 finalize kernels; sharded runs add the forest merge and run core flags twice
+    launches_per_step = (12 + 2 * (last[3] - 1)) if world == 1 else 14
 
     line = {
         "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",
-        "value": world * n / (ms / 1e3),
+        "value": n / (ms / 1e3),
         "unit": "points/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded Gaussian blobs + uniform noise, datasets.generate_blobs)",
         "config": {"workload": f"{cfg.name}: {cfg.description}", "n": n, "d": d,
                    "eps": cfg.eps, "min_pts": cfg.min_pts, "formula": "algebraic",
                    "l2": "flushed (512 MB write) before every timed step",
-                   "parallelism": f"replica x{world}" if world > 1 else "1 GPU"},
-        "e2e": {"value": world * n / (e2e / 1e3), "unit": "points/s",
-                "h2d_bytes_per_step": n * d * 8, "d2h_bytes_per_step": n * 8,
-                "ms_per_step": e2e},
+                   "parallelism": (f"tile-pair items sharded over {world} GPUs (NCCL)"
+                                   if world > 1 else "1 GPU")},
+        "e2e": {"value": n / (e2e / 1e3), "unit": "points/s",
+                "h2d_bytes_per_step": n * d * 8 * (world if world > 1 else 1),
+                "d2h_bytes_per_step": n * 8, "ms_per_step": e2e},
         "roofline": {"bound": "fp32", "kernel": "eps_tile_kernel", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": None,
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz "
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
-                     "ops_per_pair": ops, "pairs_per_launch": last.pairs_evaluated,
+                     "ops_per_pair": ops, "pairs_per_launch": pairs,
                      "tile_ms": statistics.mean(tile_ms)},
-        "gpair_evals_per_s": last.pairs_evaluated / tile_s / 1e9,
-        "n2_decisions_per_s": decisions / tile_s / 1e9,
-        "stages_ms": {"fused": last.fused_ms, "merge": last.merge_ms, "tile": last.tile_ms},
-        "words_emitted": last.words_emitted, "tiles_nonempty": last.tiles_nonempty,
-        "tiles_total": last.tiles_total,
+        "gpair_evals_per_s": pairs / tile_s / 1e9,
+        "n2_decisions_per_s": (n * n if world == 1 else n * n / world) / tile_s / 1e9,
+        "stages_ms": last[2],
         "gpu_launches": launches_per_step * args.steps,
         "parity_vs_reference_labels": parity,
         "clocks": clocks,

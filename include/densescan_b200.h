@@ -128,6 +128,36 @@ ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
                         const uint8_t* valid, int64_t n, int64_t min_pts,
                         int64_t* labels_out, ds_timings* timings);
 
+/* ---- multi-GPU shards (row-block sharding of stage 1 over tile-pair items) ----
+ * The upper-triangle tile pairs (TILE = ds_tile_side() points per side) are
+ * numbered 0 .. ds_tile_items(n)-1 row-major. Each rank evaluates a contiguous
+ * item range; exchanges (done by the caller over NCCL, see
+ * paper_1506_02226_b200/distributed.py) are: all-reduce(SUM) of the int32
+ * counts, all-gather of the int32 parent forests, all-reduce(MIN) of the
+ * int32 border minima. Replaces the reference's fork-join over row ranges
+ * (_parallel.py:24-39) at GPU granularity. */
+int64_t ds_tile_items(int64_t n);
+int ds_tile_side(void);
+
+/* Stage 1+2 on items [item_lo, item_hi): partial neighbour counts into
+ * d_counts (int32[n], overwritten); the adjacency words stay in the context. */
+ds_status ds_shard_stage12(ds_ctx* ctx, const double* d_coords, int64_t n, int32_t d,
+                           double eps_sq, int32_t formula, int64_t item_lo, int64_t item_hi,
+                           int64_t mem_cap, int32_t* d_counts, void* stream,
+                           ds_timings* timings);
+
+/* Stage 3 on this shard's words with the all-reduced counts: the shard's
+ * union-find forest (int32[n]) and border minima (int32[n], INT32_MAX = none). */
+ds_status ds_shard_stage3_local(ds_ctx* ctx, const int32_t* d_counts, int64_t n, int64_t min_pts,
+                                int32_t* d_parent, int32_t* d_bmin, void* stream,
+                                ds_timings* timings);
+
+/* Fold nparents gathered forests (nparents x n) and the min-reduced border
+ * minima into canonical int64 labels. */
+ds_status ds_shard_stage3_merge(ds_ctx* ctx, const int32_t* d_counts, int64_t n, int64_t min_pts,
+                                const int32_t* d_parents, int32_t nparents, const int32_t* d_bmin,
+                                int64_t* d_labels, void* stream, ds_timings* timings);
+
 #ifdef __cplusplus
 }
 #endif

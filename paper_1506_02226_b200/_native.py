@@ -26,7 +26,8 @@ FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 EXPORTS = (
     "ds_abi_version", "ds_build_info", "ds_last_error", "ds_last_capacity",
     "ds_ctx_create", "ds_ctx_destroy", "ds_run_dbscan", "ds_run_dbscan_device",
-    "ds_fused_build", "ds_merge_bits",
+    "ds_fused_build", "ds_merge_bits", "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
+    "ds_shard_stage3_local", "ds_shard_stage3_merge",
 )
 
 
@@ -99,6 +100,19 @@ def load_library(path: str = LIB_PATH):
         lib.ds_merge_bits.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
                                       ctypes.POINTER(Timings)]
         lib.ds_merge_bits.restype = ctypes.c_int
+        lib.ds_tile_items.argtypes = [ctypes.c_int64]
+        lib.ds_tile_items.restype = ctypes.c_int64
+        lib.ds_tile_side.restype = ctypes.c_int
+        lib.ds_shard_stage12.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                         ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int64, vp, vp, ctypes.POINTER(Timings)]
+        lib.ds_shard_stage12.restype = ctypes.c_int
+        lib.ds_shard_stage3_local.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp,
+                                              ctypes.POINTER(Timings)]
+        lib.ds_shard_stage3_local.restype = ctypes.c_int
+        lib.ds_shard_stage3_merge.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
+                                              ctypes.c_int32, vp, vp, vp, ctypes.POINTER(Timings)]
+        lib.ds_shard_stage3_merge.restype = ctypes.c_int
         if lib.ds_abi_version() != 1:
             raise ImportError(f"{path}: unexpected ABI version {lib.ds_abi_version()}")
         _lib = lib
@@ -170,6 +184,37 @@ class Context:
                                            int(d), float(eps_sq), int(min_pts), int(formula),
                                            int(mem_cap), ctypes.c_void_p(labels_ptr),
                                            ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
+        raise_for(st, self.lib)
+        return t
+
+    # -- multi-GPU shard stages (device pointers; see distributed.py) -----------
+    def shard_stage12(self, coords_ptr, n, d, eps_sq, formula, item_lo, item_hi, mem_cap,
+                      counts_ptr, stream_ptr=0):
+        t = Timings()
+        st = self.lib.ds_shard_stage12(self.handle, ctypes.c_void_p(coords_ptr), int(n), int(d),
+                                       float(eps_sq), int(formula), int(item_lo), int(item_hi),
+                                       int(mem_cap), ctypes.c_void_p(counts_ptr),
+                                       ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
+        raise_for(st, self.lib)
+        return t
+
+    def shard_stage3_local(self, counts_ptr, n, min_pts, parent_ptr, bmin_ptr, stream_ptr=0):
+        t = Timings()
+        st = self.lib.ds_shard_stage3_local(self.handle, ctypes.c_void_p(counts_ptr), int(n),
+                                            int(min_pts), ctypes.c_void_p(parent_ptr),
+                                            ctypes.c_void_p(bmin_ptr),
+                                            ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
+        raise_for(st, self.lib)
+        return t
+
+    def shard_stage3_merge(self, counts_ptr, n, min_pts, parents_ptr, nparents, bmin_ptr,
+                           labels_ptr, stream_ptr=0):
+        t = Timings()
+        st = self.lib.ds_shard_stage3_merge(self.handle, ctypes.c_void_p(counts_ptr), int(n),
+                                            int(min_pts), ctypes.c_void_p(parents_ptr),
+                                            int(nparents), ctypes.c_void_p(bmin_ptr),
+                                            ctypes.c_void_p(labels_ptr),
+                                            ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
         raise_for(st, self.lib)
         return t
 

@@ -174,11 +174,17 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
 // counts and scalars are valid on `s` (the stream has been synchronised once to
 // read the word count).
 ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq, int formula,
-                  int64_t mem_cap, cudaStream_t s, ds_timings* t) {
+                  int64_t mem_cap, cudaStream_t s, ds_timings* t, int64_t item_lo = 0,
+                  int64_t item_hi = -1, int32_t* cnt_out = nullptr) {
   ds_status st = alloc_common(c, n, d);
   if (st != DS_OK) return st;
   const int64_t T = n_tiles(n);
-  const int64_t items = n_items(T);
+  const int64_t all_items = n_items(T);
+  if (item_hi < 0 || item_hi > all_items) item_hi = all_items;
+  if (item_lo < 0) item_lo = 0;
+  if (item_lo > item_hi) item_lo = item_hi;
+  const int64_t items = item_hi - item_lo;
+  int32_t* cnt = cnt_out ? cnt_out : (int32_t*)c->cnt.p;
   const size_t base = base_bytes(n, d);
 
   // first guess for the adjacency words: keep what earlier calls needed
@@ -207,18 +213,18 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
 
   int launches = 0;
   for (;;) {
-    DS_CK(cudaMemsetAsync(c->cnt.p, 0, (size_t)n * 4, s));
+    DS_CK(cudaMemsetAsync(cnt, 0, (size_t)n * 4, s));
     DS_CK(cudaMemsetAsync(&sc->work_ctr, 0, 3 * sizeof(unsigned long long), s));
     TileArgs a;
     a.rec = (const float*)c->rec.p;
     a.n = n;
     a.T = (int32_t)T;
     a.d = d;
-    a.item_lo = 0;
-    a.item_hi = items;
+    a.item_lo = item_lo;
+    a.item_hi = item_hi;
     a.work_ctr = &sc->work_ctr;
     a.eps32 = eps32;
-    a.cnt = (int32_t*)c->cnt.p;
+    a.cnt = cnt;
     a.words = (uint2*)c->words.p;
     a.words_cap = c->words_cap;
     a.words_count = &sc->words_count;
@@ -460,6 +466,108 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
   local.device_bytes = (int64_t)held_bytes(c);
   local.total_ms = now_ms() - t0;
   if (t) *t = local;
+  return DS_OK;
+}
+
+int64_t ds_tile_items(int64_t n) { return n < 1 ? 0 : n_items(n_tiles(n)); }
+
+int ds_tile_side(void) { return TILE; }
+
+ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t d, double eps_sq,
+                           int32_t formula, int64_t item_lo, int64_t item_hi, int64_t mem_cap,
+                           int32_t* d_counts, void* stream, ds_timings* t) {
+  if (!c || !d_coords || !d_counts) {
+    set_error("ctx, d_coords and d_counts must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, 1, formula);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  ds_timings local{};
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CK(cudaEventRecord(c->ev[0], s));
+  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, item_lo, item_hi, d_counts);
+  if (st != DS_OK) return st;
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(cudaEventSynchronize(c->ev[3]));
+  float f = 0, k = 0;
+  DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
+  DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+  local.fused_ms = f;
+  local.tile_ms = k;
+  local.device_bytes = (int64_t)held_bytes(c);
+  local.total_ms = now_ms() - t0;
+  if (t) *t = local;
+  return DS_OK;
+}
+
+ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, int64_t min_pts,
+                                int32_t* d_parent, int32_t* d_bmin, void* stream, ds_timings* t) {
+  if (!c || !d_counts || !d_parent || !d_bmin) {
+    set_error("ctx, d_counts, d_parent and d_bmin must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  if (!c->cnt.p || c->cnt.bytes < (size_t)n * 4 || !c->chunks.p) {
+    set_error("ds_shard_stage3_local needs a preceding ds_shard_stage12 on this context");
+    return DS_EINVAL;
+  }
+  DS_CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(cudaMemcpyAsync(c->cnt.p, d_counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  MergeWs w = merge_ws(c, n);
+  Scalars* sc = (Scalars*)c->scalars.p;
+  DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, (const uint4*)c->chunks.p,
+                            &sc->nonempty_count, s));
+  DS_CK(cudaMemcpyAsync(d_parent, c->parent.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  DS_CK(cudaMemcpyAsync(d_bmin, c->bmin.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  DS_CK(cudaEventSynchronize(c->ev[4]));
+  if (t) {
+    float m = 0;
+    DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
+    t->merge_ms = m;
+  }
+  return DS_OK;
+}
+
+ds_status ds_shard_stage3_merge(ds_ctx* c, const int32_t* d_counts, int64_t n, int64_t min_pts,
+                                const int32_t* d_parents, int32_t nparents, const int32_t* d_bmin,
+                                int64_t* d_labels, void* stream, ds_timings* t) {
+  if (!c || !d_counts || !d_parents || nparents < 1 || !d_bmin || !d_labels) {
+    set_error("ctx, d_counts, d_parents (nparents >= 1), d_bmin and d_labels are required");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  st = alloc_common(c, n, 1);
+  if (st != DS_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  Scalars* sc = (Scalars*)c->scalars.p;
+  DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
+  DS_CK(cudaMemcpyAsync(c->cnt.p, d_counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  MergeWs w = merge_ws(c, n);
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(cudaMemcpyAsync(c->bmin.p, d_bmin, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  DS_CK(launch_merge_forests(w, d_parents, nparents, s));
+  DS_CK(launch_finalize(w, d_labels, s));
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  if (t) {
+    float m = 0;
+    DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
+    t->merge_ms = m;
+    t->core_count = (int64_t)c->h_scalars->ncore;
+    t->cluster_count = c->h_scalars->nclusters;
+  }
   return DS_OK;
 }
 

@@ -88,6 +88,7 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint
                                 const unsigned long long* nchunks, cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
+cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s);
 cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,

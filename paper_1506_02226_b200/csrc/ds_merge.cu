@@ -431,6 +431,20 @@ __global__ void bswap_kernel(uint32_t* bits32, int64_t total) {
     bits32[k] = __byte_perm(bits32[k], 0, 0x0123);
 }
 
+// Multi-GPU: fold the R per-shard forests into one. parents is R x n; every
+// parent pointer of a shard is a connectivity fact of that shard's edges, so
+// linking i with parents[r][i] for all r yields the union of all shards' edges.
+__global__ void merge_forests_kernel(const int32_t* __restrict__ parents, int R, int64_t n,
+                                     const uint8_t* __restrict__ core, int32_t* parent) {
+  const int64_t total = (int64_t)R * n;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k % n;
+    const int p = parents[k];
+    if (p != (int)i && core[i]) link_root(parent, find_plain(parent, (int)i), p);
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -477,6 +491,15 @@ cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
   scan_top_kernel<<<1, SCAN_T, 0, s>>>(w.partials, np, w.nclusters);
   scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
   label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, labels);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R,
+                                 cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  merge_forests_kernel<<<sms * 8, 256, 0, s>>>(parents, R, w.n, w.core, w.parent);
   return cudaGetLastError();
 }
 

@@ -216,3 +216,42 @@ def test_capacity_regrow_and_error(ds):
     assert exc.value.cap_bytes == 2_000_000 and exc.value.required_bytes > 2_000_000
     labeling, t = ds.run_dbscan(pts, params, ds.default_config())
     assert labeling.cluster_count() == 1 and t.words_emitted > 0
+
+
+@pytest.mark.parametrize("shards", [2, 3, 5])
+def test_shard_stages_fold_to_reference_labels(ds, shards):
+    """The real device shard stages, run as `shards` virtual ranks on one GPU
+    (one context each); the exchanges are done with torch ops exactly as the
+    NCCL collectives would (sum, gather, min)."""
+    import torch
+    from paper_1506_02226_b200 import _native, distributed as D
+
+    g = load_golden("c1.npz")
+    pts = ds.generate_blobs(10_000, 4, 0.5, 0.0, 1, 2).coords_aos
+    coords = torch.from_numpy(pts.copy()).cuda()
+    n, d = pts.shape
+    total = D.tile_items(n)
+    ctxs = [_native.Context(0) for _ in range(shards)]
+    counts = []
+    for r, ctx in enumerate(ctxs):
+        lo, hi = D.shard_range(total, shards, r)
+        c = torch.empty(n, dtype=torch.int32, device="cuda")
+        ctx.shard_stage12(coords.data_ptr(), n, d, 0.09, 1, lo, hi, 0, c.data_ptr())
+        counts.append(c)
+    total_counts = torch.stack(counts).sum(0).to(torch.int32)
+    assert np.array_equal(total_counts.cpu().numpy(), g["alg/counts"])
+    parents, bmins = [], []
+    for ctx in ctxs:
+        p = torch.empty(n, dtype=torch.int32, device="cuda")
+        b = torch.empty(n, dtype=torch.int32, device="cuda")
+        ctx.shard_stage3_local(total_counts.data_ptr(), n, 4, p.data_ptr(), b.data_ptr())
+        parents.append(p)
+        bmins.append(b)
+    par = torch.stack(parents).contiguous()
+    bmin = torch.stack(bmins).min(0).values.to(torch.int32).contiguous()
+    labels = torch.empty(n, dtype=torch.int64, device="cuda")
+    ctxs[0].shard_stage3_merge(total_counts.data_ptr(), n, 4, par.data_ptr(), shards,
+                               bmin.data_ptr(), labels.data_ptr())
+    assert np.array_equal(labels.cpu().numpy(), g["alg/labels"])
+    for ctx in ctxs:
+        ctx.close()
