@@ -86,6 +86,14 @@ void ds_last_capacity(int64_t* required_bytes, int64_t* cap_bytes);
 ds_status ds_ctx_create(int device, ds_ctx** out);
 void ds_ctx_destroy(ds_ctx* ctx);
 
+/* Context options.
+ * DS_OPT_TILE_CULL (default 1): skip tile pairs whose bounding boxes prove every
+ * pair out of range, with a float32 rounding-error margin;
+ * results are bit-identical with 0 (the paper's dense schedule). */
+enum { DS_OPT_TILE_CULL = 1 };
+ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
+int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
+
 /*
  * run_dbscan (pipeline.py:70-92): host float64 coords in, host int64
  * canonical labels out. mem_cap bounds the device workspace in bytes
@@ -131,7 +139,7 @@ ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
 /* ---- multi-GPU shards (row-block sharding of stage 1 over tile-pair items) ----
  * The upper-triangle tile pairs (TILE = ds_tile_side() points per side) are
  * numbered 0 .. ds_tile_items(n)-1 row-major. Each rank evaluates a contiguous
- * item range; exchanges (done by the caller over NCCL, see
+ * share of them; exchanges (done by the caller over NCCL, see
  * paper_1506_02226_b200/distributed.py) are: all-reduce(SUM) of the int32
  * counts, all-gather of the int32 parent forests, all-reduce(MIN) of the
  * int32 border minima. Replaces the reference's fork-join over row ranges
@@ -139,10 +147,12 @@ ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
 int64_t ds_tile_items(int64_t n);
 int ds_tile_side(void);
 
-/* Stage 1+2 on items [item_lo, item_hi): partial neighbour counts into
- * d_counts (int32[n], overwritten); the adjacency words stay in the context. */
+/* Stage 1+2 on rank's contiguous share of the tile-pair items (of the culled
+ * list when DS_OPT_TILE_CULL is on, of the dense triangle otherwise): partial
+ * neighbour counts into d_counts (int32[n], overwritten); the adjacency words
+ * stay in the context for ds_shard_stage3_local. */
 ds_status ds_shard_stage12(ds_ctx* ctx, const double* d_coords, int64_t n, int32_t d,
-                           double eps_sq, int32_t formula, int64_t item_lo, int64_t item_hi,
+                           double eps_sq, int32_t formula, int32_t rank, int32_t world,
                            int64_t mem_cap, int32_t* d_counts, void* stream,
                            ds_timings* timings);
 

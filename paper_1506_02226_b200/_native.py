@@ -20,12 +20,14 @@ LIB_NAME = "libdensescan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
+DS_OPT_TILE_CULL = 1
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
 EXPORTS = (
     "ds_abi_version", "ds_build_info", "ds_last_error", "ds_last_capacity",
-    "ds_ctx_create", "ds_ctx_destroy", "ds_run_dbscan", "ds_run_dbscan_device",
+    "ds_ctx_create", "ds_ctx_destroy", "ds_ctx_set_option", "ds_ctx_get_option",
+    "ds_run_dbscan", "ds_run_dbscan_device",
     "ds_fused_build", "ds_merge_bits", "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
     "ds_shard_stage3_local", "ds_shard_stage3_merge",
 )
@@ -85,6 +87,10 @@ def load_library(path: str = LIB_PATH):
         lib.ds_ctx_create.restype = ctypes.c_int
         lib.ds_ctx_destroy.argtypes = [vp]
         lib.ds_ctx_destroy.restype = None
+        lib.ds_ctx_set_option.argtypes = [vp, ctypes.c_int32, ctypes.c_int64]
+        lib.ds_ctx_set_option.restype = ctypes.c_int
+        lib.ds_ctx_get_option.argtypes = [vp, ctypes.c_int32]
+        lib.ds_ctx_get_option.restype = ctypes.c_int64
         lib.ds_run_dbscan.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
                                       ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp, vp,
                                       ctypes.POINTER(Timings)]
@@ -104,7 +110,7 @@ def load_library(path: str = LIB_PATH):
         lib.ds_tile_items.restype = ctypes.c_int64
         lib.ds_tile_side.restype = ctypes.c_int
         lib.ds_shard_stage12.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
-                                         ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int64, vp, vp, ctypes.POINTER(Timings)]
         lib.ds_shard_stage12.restype = ctypes.c_int
         lib.ds_shard_stage3_local.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp,
@@ -161,6 +167,14 @@ class Context:
         except Exception:
             pass
 
+    def set_tile_cull(self, on: bool) -> None:
+        """Bounding-box culling of provably empty tile pairs (default on; exact)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_TILE_CULL, 1 if on else 0),
+                  self.lib)
+
+    def tile_cull(self) -> bool:
+        return self.lib.ds_ctx_get_option(self.handle, DS_OPT_TILE_CULL) == 1
+
     # -- entry points --------------------------------------------------------
     def run_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
                    mem_cap: int, want_counts: bool = False):
@@ -188,11 +202,11 @@ class Context:
         return t
 
     # -- multi-GPU shard stages (device pointers; see distributed.py) -----------
-    def shard_stage12(self, coords_ptr, n, d, eps_sq, formula, item_lo, item_hi, mem_cap,
+    def shard_stage12(self, coords_ptr, n, d, eps_sq, formula, rank, world, mem_cap,
                       counts_ptr, stream_ptr=0):
         t = Timings()
         st = self.lib.ds_shard_stage12(self.handle, ctypes.c_void_p(coords_ptr), int(n), int(d),
-                                       float(eps_sq), int(formula), int(item_lo), int(item_hi),
+                                       float(eps_sq), int(formula), int(rank), int(world),
                                        int(mem_cap), ctypes.c_void_p(counts_ptr),
                                        ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
         raise_for(st, self.lib)

@@ -49,7 +49,9 @@ struct Scalars {
   unsigned long long work_ctr;
   unsigned long long words_count;
   unsigned long long nonempty_count;
+  unsigned long long kept;  // tile pairs surviving the culling test
   unsigned long long ncore;
+  int32_t kept32;
   uint32_t unsafe_flag;
   int32_t nclusters;
 };
@@ -62,7 +64,8 @@ struct ds_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
-      words, chunks, scalars, dense;
+      words, chunks, scalars, dense, tbox, items, iflags, ipartials;
+  int cull = 1;  // DS_OPT_TILE_CULL
   unsigned long long words_cap = 0;  // in words (8-byte records)
   Scalars* h_scalars = nullptr;      // pinned
 };
@@ -87,7 +90,8 @@ cudaError_t ensure(Buf& b, size_t bytes) {
 size_t held_bytes(const ds_ctx* c) {
   const Buf* all[] = {&c->coords64, &c->rec, &c->cnt,   &c->core,     &c->corew,   &c->parent,
                       &c->bmin,     &c->cmin, &c->root, &c->flag,     &c->partials, &c->labels,
-                      &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense};
+                      &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
+                      &c->tbox,     &c->items,  &c->iflags, &c->ipartials};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -128,7 +132,8 @@ constexpr size_t WORD_BYTES = 8;  // one adjacency record
 size_t base_bytes(int64_t n, int d) {
   const size_t N = (size_t)n;
   return N * rec_stride(d) * 4      // rec
-         + (size_t)n_items(n_tiles(n)) * 16  // chunk table
+         + (size_t)n_items(n_tiles(n)) * (16 + 4 + 4)  // chunk table + item list + flags
+         + (size_t)n_tiles(n) * (2 * padded_dim(d) + 1) * 4  // tile boxes
          + N * 4 * 6                // cnt parent bmin cmin root flag
          + N                        // core
          + ((N + 31) / 32) * 4      // corew
@@ -174,16 +179,22 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
 // counts and scalars are valid on `s` (the stream has been synchronised once to
 // read the word count).
 ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq, int formula,
-                  int64_t mem_cap, cudaStream_t s, ds_timings* t, int64_t item_lo = 0,
-                  int64_t item_hi = -1, int32_t* cnt_out = nullptr) {
+                  int64_t mem_cap, cudaStream_t s, ds_timings* t, int rank = 0, int world = 1,
+                  int32_t* cnt_out = nullptr) {
   ds_status st = alloc_common(c, n, d);
   if (st != DS_OK) return st;
   const int64_t T = n_tiles(n);
   const int64_t all_items = n_items(T);
-  if (item_hi < 0 || item_hi > all_items) item_hi = all_items;
-  if (item_lo < 0) item_lo = 0;
-  if (item_lo > item_hi) item_lo = item_hi;
-  const int64_t items = item_hi - item_lo;
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("shard: rank must be in [0, world)");
+    return DS_EINVAL;
+  }
+  const bool cull = c->cull != 0 && T > 1;
+  // dense schedule: contiguous equal slice of the triangle; culled schedule: the
+  // slice of the device-side kept list is taken inside the kernel
+  const int64_t item_lo = all_items * rank / world;
+  const int64_t item_hi = all_items * (rank + 1) / world;
+  const int64_t items = cull ? all_items : item_hi - item_lo;
   int32_t* cnt = cnt_out ? cnt_out : (int32_t*)c->cnt.p;
   const size_t base = base_bytes(n, d);
 
@@ -210,6 +221,18 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
 
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
   DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, s));
+  if (cull) {
+    const int dp = padded_dim(d);
+    DS_CK(ensure(c->tbox, (size_t)T * (2 * dp + 1) * 4));
+    DS_CK(ensure(c->items, (size_t)all_items * 4));
+    DS_CK(ensure(c->iflags, (size_t)all_items * 4));
+    DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(all_items) * 4));
+    float* lo = (float*)c->tbox.p;
+    DS_CK(launch_cull((const float*)c->rec.p, n, d, eps32, formula, &sc->unsafe_flag, lo,
+                      lo + (size_t)T * dp, lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p,
+                      (int32_t*)c->ipartials.p, &sc->kept32, (uint32_t*)c->items.p, &sc->kept,
+                      s));
+  }
 
   int launches = 0;
   for (;;) {
@@ -222,6 +245,10 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     a.d = d;
     a.item_lo = item_lo;
     a.item_hi = item_hi;
+    a.item_list = cull ? (const uint32_t*)c->items.p : nullptr;
+    a.item_count = &sc->kept;
+    a.shard_rank = rank;
+    a.shard_world = world;
     a.work_ctr = &sc->work_ctr;
     a.eps32 = eps32;
     a.cnt = cnt;
@@ -258,12 +285,17 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
   }
   if (t) {
     t->tile_launches = launches;
-    t->tiles_total = items;
+    int64_t evaluated = item_hi - item_lo;
+    if (cull) {
+      const int64_t kept = (int64_t)c->h_scalars->kept;
+      evaluated = kept * (rank + 1) / world - kept * rank / world;
+    }
+    t->tiles_total = evaluated;
     t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;
     t->words_emitted = (int64_t)c->h_scalars->words_count;
     t->unsafe_range = c->h_scalars->unsafe_flag ? 1 : 0;
-    // every item evaluates the full 512 x 512 pair block (ragged edges masked)
-    t->pairs_evaluated = items * (int64_t)TILE * TILE;
+    // every evaluated item is a full 512 x 512 pair block (ragged edges masked)
+    t->pairs_evaluated = evaluated * (int64_t)TILE * TILE;
   }
   return DS_OK;
 }
@@ -351,7 +383,8 @@ void ds_ctx_destroy(ds_ctx* c) {
   cudaSetDevice(c->device);
   Buf* all[] = {&c->coords64, &c->rec,    &c->cnt,    &c->core,   &c->corew,    &c->parent,
                 &c->bmin,     &c->cmin,   &c->root,   &c->flag,   &c->partials, &c->labels,
-                &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense};
+                &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
+                &c->tbox,     &c->items,  &c->iflags, &c->ipartials};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -469,12 +502,30 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
   return DS_OK;
 }
 
+ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
+  if (!c) {
+    set_error("ctx: NULL");
+    return DS_EINVAL;
+  }
+  if (option == DS_OPT_TILE_CULL) {
+    c->cull = value ? 1 : 0;
+    return DS_OK;
+  }
+  set_error("option: unknown option id");
+  return DS_EINVAL;
+}
+
+int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
+  if (c && option == DS_OPT_TILE_CULL) return c->cull;
+  return -1;
+}
+
 int64_t ds_tile_items(int64_t n) { return n < 1 ? 0 : n_items(n_tiles(n)); }
 
 int ds_tile_side(void) { return TILE; }
 
 ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t d, double eps_sq,
-                           int32_t formula, int64_t item_lo, int64_t item_hi, int64_t mem_cap,
+                           int32_t formula, int32_t rank, int32_t world, int64_t mem_cap,
                            int32_t* d_counts, void* stream, ds_timings* t) {
   if (!c || !d_coords || !d_counts) {
     set_error("ctx, d_coords and d_counts must be non-NULL");
@@ -487,7 +538,7 @@ ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t
   ds_timings local{};
   cudaStream_t s = (cudaStream_t)stream;
   DS_CK(cudaEventRecord(c->ev[0], s));
-  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, item_lo, item_hi, d_counts);
+  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, rank, world, d_counts);
   if (st != DS_OK) return st;
   DS_CK(cudaEventRecord(c->ev[3], s));
   DS_CK(cudaEventSynchronize(c->ev[3]));

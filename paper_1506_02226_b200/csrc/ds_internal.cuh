@@ -59,12 +59,23 @@ struct TileArgs {
   unsigned long long chunks_cap;
   unsigned long long* nonempty_count;  // = chunks emitted
   const uint32_t* unsafe_flag;
+  const uint32_t* item_list;           // culled items (a << 16 | b), or nullptr: dense triangle
+  const unsigned long long* item_count; // length of item_list (device)
+  int32_t shard_rank, shard_world;     // slice of item_list this launch evaluates
 };
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
                         cudaStream_t s);
 cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream_t s);
+// tile bounding boxes + list of tile pairs that are not provably empty
+cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
+                        const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
+                        int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
+                        unsigned long long* count, cudaStream_t s);
+// exclusive prefix sum of int32 data in place (3 kernels); *total = sum
+cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
+                                  cudaStream_t s);
 size_t tile_smem_bytes(int d);
 
 // ---- launchers (ds_merge.cu) --------------------------------------------------

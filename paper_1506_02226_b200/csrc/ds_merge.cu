@@ -503,6 +503,15 @@ cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R
   return cudaGetLastError();
 }
 
+cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
+                                  cudaStream_t s) {
+  const int64_t np = scan_partials_len(n);
+  scan_partials_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(data, n, partials);
+  scan_top_kernel<<<1, SCAN_T, 0, s>>>(partials, np, total);
+  scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(data, n, partials);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s) {
   counts_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(cnt, n, out);
   return cudaGetLastError();

@@ -98,6 +98,19 @@ __device__ __forceinline__ uint32_t diag_keep(int rel) {
   return rel <= 0 ? 0xffffffffu : (rel > 31 ? 0u : ((1u << (32 - rel)) - 1u));
 }
 
+// Item q -> tile pair: through the culled item list when one is given, else the
+// dense upper-triangle enumeration.
+__device__ __forceinline__ void item_tiles(const TileArgs& args, int64_t q, int64_t T, int& a,
+                                           int& b) {
+  if (args.item_list) {
+    const uint32_t ab = args.item_list[q];
+    a = (int)(ab >> 16);
+    b = (int)(ab & 0xffffu);
+  } else {
+    decode_item(q, T, a, b);
+  }
+}
+
 __device__ __forceinline__ uint32_t valid_mask(int m) {
   // bit (31 - t) <-> column t of the word; the first m columns are valid
   return m >= 32 ? 0xffffffffu : (m <= 0 ? 0u : (0xffffffffu << (32 - m)));
@@ -301,32 +314,45 @@ eps_tile_kernel(const TileArgs args) {
 
   auto issue = [&](long long q, int buf) {  // thread 0 only
     int a, b;
-    decode_item(q, T, a, b);
+    item_tiles(args, q, T, a, b);
     const int64_t nb = min((int64_t)TILE, n - (int64_t)b * TILE);
     const uint32_t bytes = (uint32_t)(nb * S * 4);
     mbar_expect_tx(&mbar[buf], bytes);
     bulk_g2s(bc + (size_t)buf * TILE * S, args.rec + (size_t)b * TILE * S, bytes, &mbar[buf]);
   };
 
+  __shared__ long long range_sh[2];
   if (tid == 0) {
-    const long long q0 = args.item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
+    long long lo = args.item_lo, hi = args.item_hi;
+    if (args.item_list) {  // culled list: this shard's slice of the device-side count
+      const long long total = (long long)*args.item_count;
+      lo = total * args.shard_rank / args.shard_world;
+      hi = total * (args.shard_rank + 1) / args.shard_world;
+    }
+    range_sh[0] = lo;
+    range_sh[1] = hi;
+  }
+  __syncthreads();
+  const long long item_lo = range_sh[0], item_hi = range_sh[1];
+  if (tid == 0) {
+    const long long q0 = item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
     item_sh[0] = q0;
-    if (q0 < args.item_hi) issue(q0, 0);
+    if (q0 < item_hi) issue(q0, 0);
   }
   __syncthreads();
 
   long long q = item_sh[0];
   uint32_t phase = 0;  // bit b = parity of buffer b's next completion
   int it = 0;
-  while (q < args.item_hi) {
+  while (q < item_hi) {
     const int cur = (G::NBUF == 2) ? (it & 1) : 0;
     if (tid == 0) {
-      const long long qn = args.item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
+      const long long qn = item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
       item_sh[(it + 1) & 1] = qn;
-      if (G::NBUF == 2 && qn < args.item_hi) issue(qn, cur ^ 1);
+      if (G::NBUF == 2 && qn < item_hi) issue(qn, cur ^ 1);
     }
     int a, b;
-    decode_item(q, T, a, b);
+    item_tiles(args, q, T, a, b);
     const int na = (int)min((int64_t)TILE, n - (int64_t)a * TILE);
     const int nb = (int)min((int64_t)TILE, n - (int64_t)b * TILE);
 
@@ -502,7 +528,7 @@ eps_tile_kernel(const TileArgs args) {
     }
     __syncthreads();
     const long long qn = item_sh[(it + 1) & 1];
-    if (G::NBUF == 1 && tid == 0 && qn < args.item_hi) issue(qn, 0);
+    if (G::NBUF == 1 && tid == 0 && qn < item_hi) issue(qn, 0);
     q = qn;
     ++it;
   }
@@ -529,6 +555,112 @@ __global__ void prep_kernel(const double* __restrict__ coords, int64_t n, int d,
   if (bad) atomicOr(unsafe_flag, 1u);
 }
 
+// ---- tile culling ------------------------------------------------------------------
+// Per tile: coordinate bounding box (float32, exact) and max squared norm.
+__global__ void tile_bounds_kernel(const float* __restrict__ rec, int64_t n, int dpad, int S,
+                                   float* __restrict__ lo, float* __restrict__ hi,
+                                   float* __restrict__ maxnorm) {
+  const int tile = blockIdx.x;
+  const int64_t base = (int64_t)tile * TILE;
+  const int cnt = (int)min((int64_t)TILE, n - base);
+  __shared__ float red[32];
+  for (int k = 0; k <= dpad; ++k) {  // k == dpad: the norm column
+    float mn = INFINITY, mx = -INFINITY;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const float v = rec[(base + i) * S + k];
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    for (int off = 16; off; off >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) red[warp] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) mn = fminf(mn, red[w]);
+      red[0] = mn;
+    }
+    __syncthreads();
+    mn = red[0];
+    __syncthreads();
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) mx = fmaxf(mx, red[w]);
+      if (k < dpad) {
+        lo[(int64_t)tile * dpad + k] = mn;
+        hi[(int64_t)tile * dpad + k] = mx;
+      } else {
+        maxnorm[tile] = mx;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Keep tile pair (a, b), a <= b, unless every pair in it is provably out of range
+// in the formula's float32 arithmetic. L = squared gap between the boxes (exact
+// reals, evaluated in double). DIRECT: every op is monotone in |dx| and the terms
+// are >= 0, so d2_computed >= L (1 - u)^(3d); ALGEBRAIC: |d2_computed - D| <=
+// (2d+3) u (T + P) (1 + O(u)) by the standard summation bound, D >= L. Both
+// slacks are taken 4x larger; a tile pair is culled only if even the slackened
+// lower bound exceeds eps32. Inputs that need the overflow-safe compare are never
+// culled (the flag is checked here, on the device).
+__device__ __forceinline__ bool keep_item(const float* __restrict__ lo, const float* __restrict__ hi,
+                                          const float* __restrict__ maxnorm, int dpad, int a, int b,
+                                          float eps32, int formula, bool unsafe) {
+  if (unsafe || a == b) return true;
+  const double u = 1.0 / 16777216.0;
+  double L = 0.0;
+  for (int k = 0; k < dpad; ++k) {
+    const double g1 = (double)lo[(int64_t)b * dpad + k] - (double)hi[(int64_t)a * dpad + k];
+    const double g2 = (double)lo[(int64_t)a * dpad + k] - (double)hi[(int64_t)b * dpad + k];
+    const double g = fmax(0.0, fmax(g1, g2));
+    L += g * g;
+  }
+  double bound = L * (1.0 - 4.0 * 3.0 * dpad * u) * (1.0 - 1e-12);
+  if (formula == DS_FORMULA_ALGEBRAIC)
+    bound -= 4.0 * (2.0 * dpad + 3.0) * u * ((double)maxnorm[a] + (double)maxnorm[b]) * 1.001;
+  return !(bound > (double)eps32);  // NaN bounds keep the pair
+}
+
+// pass 1: keep flag per item (int32, scanned in place afterwards)
+__global__ void cull_flags_kernel(const float* __restrict__ lo, const float* __restrict__ hi,
+                                  const float* __restrict__ maxnorm, int dpad, int64_t T,
+                                  float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
+                                  int32_t* __restrict__ flags) {
+  const int64_t total = T * (T + 1) / 2;
+  const bool unsafe = *unsafe_flag != 0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int a, b;
+    decode_item(q, T, a, b);
+    flags[q] = keep_item(lo, hi, maxnorm, dpad, a, b, eps32, formula, unsafe) ? 1 : 0;
+  }
+}
+
+// pass 3: stable scatter by the exclusive scan, so the kept list is in item order
+// and identical on every rank (ranks slice it by position)
+__global__ void cull_scatter_kernel(const float* __restrict__ lo, const float* __restrict__ hi,
+                                    const float* __restrict__ maxnorm, int dpad, int64_t T,
+                                    float eps32, int formula,
+                                    const uint32_t* __restrict__ unsafe_flag,
+                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ total_kept,
+                                    uint32_t* __restrict__ list, unsigned long long* count) {
+  const int64_t total = T * (T + 1) / 2;
+  const bool unsafe = *unsafe_flag != 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)*total_kept;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int a, b;
+    decode_item(q, T, a, b);
+    if (keep_item(lo, hi, maxnorm, dpad, a, b, eps32, formula, unsafe))
+      list[pos[q]] = ((uint32_t)a << 16) | (uint32_t)b;
+  }
+}
+
 int pad_dim(int d) {
   if (d <= 4) return d;
   if (d <= 8) return 8;
@@ -552,7 +684,7 @@ cudaError_t launch_one(const TileArgs& a, int sm_count, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
-  const int64_t items = a.item_hi - a.item_lo;
+  const int64_t items = a.item_list ? (int64_t)1 << 40 : a.item_hi - a.item_lo;
   int64_t grid = (int64_t)sm_count * per_sm;
   if (grid > items) grid = items;
   if (grid < 1) grid = 1;
@@ -600,6 +732,26 @@ cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
   prep_kernel<<<(unsigned)blocks, threads, 0, s>>>(coords, n, d, dp, S, rec, unsafe_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
+                        const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
+                        int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
+                        unsigned long long* count, cudaStream_t s) {
+  const int dp = pad_dim(d);
+  const int S = ((dp + 1) + 3) / 4 * 4;
+  const int64_t T = (n + TILE - 1) / TILE;
+  tile_bounds_kernel<<<(unsigned)T, 256, 0, s>>>(rec, n, dp, S, lo, hi, maxnorm);
+  const int64_t total = T * (T + 1) / 2;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  cull_flags_kernel<<<(unsigned)blocks, 256, 0, s>>>(lo, hi, maxnorm, dp, T, eps32, formula,
+                                                     unsafe_flag, flags);
+  cudaError_t e = launch_exclusive_scan(flags, total, partials, total_kept, s);
+  if (e != cudaSuccess) return e;
+  cull_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(lo, hi, maxnorm, dp, T, eps32, formula,
+                                                       unsafe_flag, flags, total_kept, list, count);
   return cudaGetLastError();
 }
 

@@ -7,8 +7,10 @@ NCCL for the exchanges):
 
   * every rank holds all n points (float64, <= 32 MB at every config);
   * the upper-triangle tile pairs (items, TILE = 512 points per side,
-    numbered row-major by ds_tile_items) are split into contiguous equal
-    ranges, one per rank — items cost the same, so ranks are balanced;
+    numbered row-major by ds_tile_items) — after bounding-box culling, the
+    list of tile pairs that can hold an in-range pair, built identically on
+    every rank — are split into contiguous equal ranges, one per rank; items
+    cost the same, so ranks are balanced;
   * stage 1+2 on the rank's items gives partial neighbour counts and the
     rank's adjacency words (ds_shard_stage12);
   * exchange 1: all_reduce(SUM) of the int32 counts -> identical core flags;
@@ -86,11 +88,11 @@ class NativeShardBackend:
         return self.torch.from_numpy(np.ascontiguousarray(coords, dtype=np.float64).copy()).to(
             self.device)
 
-    def stage12(self, coords, eps_sq, formula, lo, hi, mem_cap):
+    def stage12(self, coords, eps_sq, formula, rank, world, mem_cap):
         n, d = coords.shape
         counts = self.torch.empty(n, dtype=self.torch.int32, device=self.device)
-        t = self.ctx.shard_stage12(coords.data_ptr(), n, d, eps_sq, formula, lo, hi, mem_cap,
-                                   counts.data_ptr(), self.stream())
+        t = self.ctx.shard_stage12(coords.data_ptr(), n, d, eps_sq, formula, rank, world,
+                                   mem_cap, counts.data_ptr(), self.stream())
         return counts, t
 
     def stage3_local(self, counts, min_pts):
@@ -144,12 +146,11 @@ def run_dbscan_sharded(points, params: DbscanParams, formula: int = _native.FORM
     if coords is None:
         coords = backend.to_device(points.coords_aos if isinstance(points, PointSet) else points)
     n = coords.shape[0]
-    lo, hi = shard_range(tile_items(n), world, rank)
-    tm.items = (lo, hi)
+    tm.items = shard_range(tile_items(n), world, rank)  # dense share (culled: same fraction)
     cap = resolve_mem_cap(mem_cap)
 
     t = time.perf_counter()
-    counts, st = backend.stage12(coords, params.eps_sq, formula, lo, hi, cap)
+    counts, st = backend.stage12(coords, params.eps_sq, formula, rank, world, cap)
     tm.tile_ms = getattr(st, "tile_ms", 0.0)
     tm.pairs_evaluated = getattr(st, "pairs_evaluated", 0)
     sync()

@@ -36,6 +36,9 @@ class PipelineConfig:
 
     `threads` is validated as in the reference but the device ignores it.
     `device` picks the CUDA ordinal (None: $DENSESCAN_DEVICE or 0).
+    `prune` skips tile pairs whose bounding boxes prove every pair out of range
+    (with a float32 error margin; results are bit-identical either way);
+    prune=False runs the paper's dense all-pairs schedule.
     """
 
     variant: KernelVariant
@@ -43,6 +46,7 @@ class PipelineConfig:
     threads: int = 1
     mem_cap: int | None = None
     device: int | None = None
+    prune: bool = True
 
     def __post_init__(self):
         if isinstance(self.threads, bool) or not (
@@ -116,6 +120,7 @@ def run_dbscan(points: PointSet, params: DbscanParams, config: PipelineConfig):
         # the reference allocates the 4 n^2 float32 matrix for these rungs (kernels.py:156)
         ensure_capacity(4 * points.n * points.n, mem_cap)
     ctx = _native.context(config.device)
+    ctx.set_tile_cull(config.prune)
     labels, _, t = ctx.run_dbscan(points.coords_aos, params.eps_sq, params.min_pts,
                                   variant.formula, mem_cap)
     total = (time.perf_counter() - t0) * 1e3

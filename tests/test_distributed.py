@@ -34,9 +34,10 @@ class CpuShardBackend:
     def to_device(self, coords):
         return torch.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
 
-    def stage12(self, coords, eps_sq, formula, lo, hi, mem_cap):
+    def stage12(self, coords, eps_sq, formula, rank, world, mem_cap):
         c = coords.numpy()
         n = c.shape[0]
+        lo, hi = D.shard_range(D.tile_items(n), world, rank)
         p32 = oracle.narrow(c)
         norms = oracle.sq_norms(p32)
         thr = oracle.thr32(eps_sq)

@@ -218,8 +218,9 @@ def test_capacity_regrow_and_error(ds):
     assert labeling.cluster_count() == 1 and t.words_emitted > 0
 
 
+@pytest.mark.parametrize("cull", [True, False])
 @pytest.mark.parametrize("shards", [2, 3, 5])
-def test_shard_stages_fold_to_reference_labels(ds, shards):
+def test_shard_stages_fold_to_reference_labels(ds, shards, cull):
     """The real device shard stages, run as `shards` virtual ranks on one GPU
     (one context each); the exchanges are done with torch ops exactly as the
     NCCL collectives would (sum, gather, min)."""
@@ -234,9 +235,9 @@ def test_shard_stages_fold_to_reference_labels(ds, shards):
     ctxs = [_native.Context(0) for _ in range(shards)]
     counts = []
     for r, ctx in enumerate(ctxs):
-        lo, hi = D.shard_range(total, shards, r)
+        ctx.set_tile_cull(cull)  # every rank builds the same (ordered) item list
         c = torch.empty(n, dtype=torch.int32, device="cuda")
-        ctx.shard_stage12(coords.data_ptr(), n, d, 0.09, 1, lo, hi, 0, c.data_ptr())
+        ctx.shard_stage12(coords.data_ptr(), n, d, 0.09, 1, r, shards, 0, c.data_ptr())
         counts.append(c)
     total_counts = torch.stack(counts).sum(0).to(torch.int32)
     assert np.array_equal(total_counts.cpu().numpy(), g["alg/counts"])
@@ -255,3 +256,49 @@ def test_shard_stages_fold_to_reference_labels(ds, shards):
     assert np.array_equal(labels.cpu().numpy(), g["alg/labels"])
     for ctx in ctxs:
         ctx.close()
+
+
+def _labels_counts(ds, coords, eps_sq, min_pts, formula, prune):
+    ctx = ds._native.context()
+    ctx.set_tile_cull(prune)
+    try:
+        labels, counts, t = ctx.run_dbscan(coords, eps_sq, min_pts, formula, 0, want_counts=True)
+    finally:
+        ctx.set_tile_cull(True)
+    return labels, counts, t
+
+
+def test_tile_culling_is_exact(ds, oracle, rng):
+    """Culled and dense schedules give identical counts and labels, including
+    tile pairs right at the eps boundary and far-from-origin data where the
+    algebraic rounding error exceeds eps^2."""
+    cases = []
+    # blobs exactly eps apart across tile boundaries (direct: exact lattice arithmetic)
+    a = np.stack(np.meshgrid(np.arange(23.0), np.arange(23.0)), -1).reshape(-1, 2)[:512]
+    cases.append((np.concatenate([a, a + [30.0, 0.0], a + [52.0, 0.0]]), 64.0, 3))
+    # same far from the origin, in the algebraic cancellation regime
+    cases.append((np.concatenate([a, a + [22.5, 0.0]]) * 0.02 + 1000.0, 0.0004, 3))
+    cases.append((rng.normal(size=(3000, 2)) * 0.05 + [[700.0, -300.0]], 0.0009, 4))
+    # blob-ordered data where most tile pairs are culled
+    cases.append((ds.generate_blobs(12_000, 9, 0.3, 0.05, 3, 2).coords_aos, 0.01, 5))
+    cases.append((ds.generate_blobs(6_000, 5, 0.2, 0.0, 8, 16).coords_aos * 3.0, 0.5, 5))
+    for coords, eps_sq, mp in cases:
+        for f in (0, 1):
+            lc, cc, tc = _labels_counts(ds, coords, eps_sq, mp, f, True)
+            ld, cd, td = _labels_counts(ds, coords, eps_sq, mp, f, False)
+            assert np.array_equal(cc, cd) and np.array_equal(lc, ld)
+            want, wc = oracle.dbscan(coords, eps_sq, mp, f)
+            assert np.array_equal(cc, wc) and np.array_equal(lc, want)
+            assert tc.pairs_evaluated <= td.pairs_evaluated
+
+
+def test_culling_skips_work_on_c2(ds):
+    cfg = ds.CONFIGS["C2"]
+    pts = cfg.points()
+    params = ds.validate_params(cfg.eps, cfg.min_pts)
+    _, t_cull = ds.run_dbscan(pts, params, ds.default_config())
+    dense_cfg = ds.default_config()
+    dense_cfg.prune = False
+    lab_dense, t_dense = ds.run_dbscan(pts, params, dense_cfg)
+    assert np.array_equal(lab_dense.labels, load_golden("c2.npz")["labels"])
+    assert t_cull.pairs_evaluated < 0.5 * t_dense.pairs_evaluated
