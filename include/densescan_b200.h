@@ -89,8 +89,11 @@ void ds_ctx_destroy(ds_ctx* ctx);
 /* Context options.
  * DS_OPT_TILE_CULL (default 1): skip tile pairs whose bounding boxes prove every
  * pair out of range, with a float32 rounding-error margin;
- * results are bit-identical with 0 (the paper's dense schedule). */
-enum { DS_OPT_TILE_CULL = 1 };
+ * results are bit-identical with 0 (the paper's dense schedule).
+ * DS_OPT_SPATIAL_SORT (default 1): visit points in Morton order of their
+ * coordinates so tiles are compact (more tile pairs culled); index-dependent
+ * rules still use original indices, results are bit-identical with 0. */
+enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2 };
 ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
 int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
 
@@ -156,8 +159,9 @@ ds_status ds_shard_stage12(ds_ctx* ctx, const double* d_coords, int64_t n, int32
                            int64_t mem_cap, int32_t* d_counts, void* stream,
                            ds_timings* timings);
 
-/* Stage 3 on this shard's words with the all-reduced counts: the shard's
- * union-find forest (int32[n]) and border minima (int32[n], INT32_MAX = none). */
+/* Stage 3 on this shard's words with the all-reduced counts (original order):
+ * the shard's union-find forest and border minima (int32[n] each, in the
+ * context's internal point order, identical on every rank; INT32_MAX = none). */
 ds_status ds_shard_stage3_local(ds_ctx* ctx, const int32_t* d_counts, int64_t n, int64_t min_pts,
                                 int32_t* d_parent, int32_t* d_bmin, void* stream,
                                 ds_timings* timings);

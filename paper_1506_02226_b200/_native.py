@@ -20,7 +20,7 @@ LIB_NAME = "libdensescan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
-DS_OPT_TILE_CULL = 1
+DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT = 1, 2
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
@@ -174,6 +174,15 @@ class Context:
 
     def tile_cull(self) -> bool:
         return self.lib.ds_ctx_get_option(self.handle, DS_OPT_TILE_CULL) == 1
+
+    def set_spatial_sort(self, on: bool) -> None:
+        """Visit points in Morton order (compact tiles; exact, default on)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_SPATIAL_SORT, 1 if on else 0),
+                  self.lib)
+
+    def configure(self, prune: bool = True, spatial_order: bool = True) -> None:
+        self.set_tile_cull(prune)
+        self.set_spatial_sort(spatial_order)
 
     # -- entry points --------------------------------------------------------
     def run_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,

@@ -64,8 +64,11 @@ struct ds_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
-      words, chunks, scalars, dense, tbox, items, iflags, ipartials;
-  int cull = 1;  // DS_OPT_TILE_CULL
+      words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
+      keys_alt, kidx, sort_temp, bbox;
+  int cull = 1;          // DS_OPT_TILE_CULL
+  int sort = 1;          // DS_OPT_SPATIAL_SORT
+  bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
   Scalars* h_scalars = nullptr;      // pinned
 };
@@ -91,7 +94,9 @@ size_t held_bytes(const ds_ctx* c) {
   const Buf* all[] = {&c->coords64, &c->rec, &c->cnt,   &c->core,     &c->corew,   &c->parent,
                       &c->bmin,     &c->cmin, &c->root, &c->flag,     &c->partials, &c->labels,
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
-                      &c->tbox,     &c->items,  &c->iflags, &c->ipartials};
+                      &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
+                      &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
+                      &c->sort_temp, &c->bbox};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -134,6 +139,7 @@ size_t base_bytes(int64_t n, int d) {
   return N * rec_stride(d) * 4      // rec
          + (size_t)n_items(n_tiles(n)) * (16 + 4 + 4)  // chunk table + item list + flags
          + (size_t)n_tiles(n) * (2 * padded_dim(d) + 1) * 4  // tile boxes
+         + N * rec_stride(d) * 4 + N * (4 + 4 + 8 + 8 + 4)  // spatial order
          + N * 4 * 6                // cnt parent bmin cmin root flag
          + N                        // core
          + ((N + 31) / 32) * 4      // corew
@@ -155,6 +161,10 @@ MergeWs merge_ws(ds_ctx* c, int64_t n) {
   w.partials = (int32_t*)c->partials.p;
   w.nclusters = &sc->nclusters;
   w.ncore = &sc->ncore;
+  if (c->sorted) {
+    w.perm = (const int32_t*)c->perm.p;
+    w.inv = (const int32_t*)c->inv.p;
+  }
   return w;
 }
 
@@ -221,6 +231,26 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
 
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
   DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, s));
+  const float* rec = (const float*)c->rec.p;
+  c->sorted = false;
+  if (c->sort && T > 1) {  // Morton order: compact tiles (ds_sort.cu)
+    const size_t N = (size_t)n;
+    DS_CK(ensure(c->rec_sorted, N * rec_stride(d) * 4));
+    DS_CK(ensure(c->perm, N * 4));
+    DS_CK(ensure(c->inv, N * 4));
+    DS_CK(ensure(c->keys, N * 8));
+    DS_CK(ensure(c->keys_alt, N * 8));
+    DS_CK(ensure(c->kidx, N * 4));
+    DS_CK(ensure(c->bbox, 64));
+    const size_t tb = sort_temp_bytes(n);
+    DS_CK(ensure(c->sort_temp, tb));
+    DS_CK(launch_spatial_sort(rec, n, d, (float*)c->rec_sorted.p, (int32_t*)c->perm.p,
+                              (int32_t*)c->inv.p, (unsigned long long*)c->keys.p,
+                              (unsigned long long*)c->keys_alt.p, (int32_t*)c->kidx.p,
+                              c->sort_temp.p, c->sort_temp.bytes, (unsigned int*)c->bbox.p, s));
+    rec = (const float*)c->rec_sorted.p;
+    c->sorted = true;
+  }
   if (cull) {
     const int dp = padded_dim(d);
     DS_CK(ensure(c->tbox, (size_t)T * (2 * dp + 1) * 4));
@@ -228,7 +258,7 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     DS_CK(ensure(c->iflags, (size_t)all_items * 4));
     DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(all_items) * 4));
     float* lo = (float*)c->tbox.p;
-    DS_CK(launch_cull((const float*)c->rec.p, n, d, eps32, formula, &sc->unsafe_flag, lo,
+    DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo,
                       lo + (size_t)T * dp, lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p,
                       (int32_t*)c->ipartials.p, &sc->kept32, (uint32_t*)c->items.p, &sc->kept,
                       s));
@@ -239,7 +269,7 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     DS_CK(cudaMemsetAsync(cnt, 0, (size_t)n * 4, s));
     DS_CK(cudaMemsetAsync(&sc->work_ctr, 0, 3 * sizeof(unsigned long long), s));
     TileArgs a;
-    a.rec = (const float*)c->rec.p;
+    a.rec = rec;
     a.n = n;
     a.T = (int32_t)T;
     a.d = d;
@@ -313,7 +343,8 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
   DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(launch_finalize(w, d_labels, s));
-  if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, d_counts64, s));
+  if (d_counts64)
+    DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
   DS_CK(cudaEventRecord(c->ev[4], s));
   DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   DS_CK(cudaStreamSynchronize(s));
@@ -384,7 +415,9 @@ void ds_ctx_destroy(ds_ctx* c) {
   Buf* all[] = {&c->coords64, &c->rec,    &c->cnt,    &c->core,   &c->corew,    &c->parent,
                 &c->bmin,     &c->cmin,   &c->root,   &c->flag,   &c->partials, &c->labels,
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
-                &c->tbox,     &c->items,  &c->iflags, &c->ipartials};
+                &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
+                &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
+                &c->sort_temp, &c->bbox};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -472,7 +505,8 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
   DS_CK(cudaEventRecord(c->ev[0], s));
   st = stage12(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, &local);
   if (st != DS_OK) return st;
-  DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, (int64_t*)c->counts64.p, s));
+  const int32_t* perm = c->sorted ? (const int32_t*)c->perm.p : nullptr;
+  DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, perm, (int64_t*)c->counts64.p, s));
   DS_CK(cudaEventRecord(c->ev[3], s));
   DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
   if (bits_out) {
@@ -482,7 +516,7 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
     DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
     Scalars* sc = (Scalars*)c->scalars.p;
     DS_CK(launch_export_bits((const uint2*)c->words.p, (const uint4*)c->chunks.p,
-                             &sc->nonempty_count, (uint32_t*)c->dense.p, stride, s));
+                             &sc->nonempty_count, perm, (uint32_t*)c->dense.p, stride, s));
     DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
     const size_t row_bytes = (size_t)(n + 7) / 8;
     DS_CK(cudaMemcpy2DAsync(bits_out, row_bytes, c->dense.p, stride * 4, row_bytes, (size_t)n,
@@ -511,12 +545,17 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
     c->cull = value ? 1 : 0;
     return DS_OK;
   }
+  if (option == DS_OPT_SPATIAL_SORT) {
+    c->sort = value ? 1 : 0;
+    return DS_OK;
+  }
   set_error("option: unknown option id");
   return DS_EINVAL;
 }
 
 int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   if (c && option == DS_OPT_TILE_CULL) return c->cull;
+  if (c && option == DS_OPT_SPATIAL_SORT) return c->sort;
   return -1;
 }
 
@@ -538,8 +577,11 @@ ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t
   ds_timings local{};
   cudaStream_t s = (cudaStream_t)stream;
   DS_CK(cudaEventRecord(c->ev[0], s));
-  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, rank, world, d_counts);
+  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, rank, world);
   if (st != DS_OK) return st;
+  // partial counts leave in original point order (the internal order is spatial)
+  DS_CK(launch_permute_i32((const int32_t*)c->cnt.p, n,
+                           c->sorted ? (const int32_t*)c->perm.p : nullptr, 1, d_counts, s));
   DS_CK(cudaEventRecord(c->ev[3], s));
   DS_CK(cudaEventSynchronize(c->ev[3]));
   float f = 0, k = 0;
@@ -568,7 +610,8 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   DS_CK(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
   DS_CK(cudaEventRecord(c->ev[3], s));
-  DS_CK(cudaMemcpyAsync(c->cnt.p, d_counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  DS_CK(launch_permute_i32(d_counts, n, c->sorted ? (const int32_t*)c->perm.p : nullptr, 0,
+                           (int32_t*)c->cnt.p, s));
   MergeWs w = merge_ws(c, n);
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
@@ -603,7 +646,8 @@ ds_status ds_shard_stage3_merge(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   DS_CK(cudaEventRecord(c->ev[3], s));
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
-  DS_CK(cudaMemcpyAsync(c->cnt.p, d_counts, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  DS_CK(launch_permute_i32(d_counts, n, c->sorted ? (const int32_t*)c->perm.p : nullptr, 0,
+                           (int32_t*)c->cnt.p, s));
   MergeWs w = merge_ws(c, n);
   DS_CK(launch_core_init(w, min_pts, s));
   DS_CK(cudaMemcpyAsync(c->bmin.p, d_bmin, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
@@ -643,6 +687,7 @@ ds_status ds_merge_bits(ds_ctx* c, const uint8_t* bits, const int64_t* counts, c
   cudaStream_t s = c->stream;
   st = alloc_common(c, n, 1);
   if (st != DS_OK) return st;
+  c->sorted = false;  // the reference-layout matrix is in original order
   std::vector<int32_t> cnt32((size_t)n);
   for (int64_t i = 0; i < n; ++i) cnt32[i] = (int32_t)std::min<int64_t>(counts[i], 0x7fffffff);
   const int64_t stride = (n + 31) / 32;

@@ -92,6 +92,8 @@ struct MergeWs {
   int32_t* partials;      // scan block partials
   int32_t* nclusters;     // device scalar
   unsigned long long* ncore;
+  const int32_t* perm = nullptr;  // sorted -> original index (nullptr: identity)
+  const int32_t* inv = nullptr;   // original -> sorted index
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
@@ -101,10 +103,19 @@ cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
-cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s);
+cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
+                              cudaStream_t s);
 cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
-                               const unsigned long long* nchunks, uint32_t* bits32,
-                               int64_t stride_words, cudaStream_t s);
+                               const unsigned long long* nchunks, const int32_t* perm,
+                               uint32_t* bits32, int64_t stride_words, cudaStream_t s);
+cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* perm, int to_original,
+                               int32_t* dst, cudaStream_t s);
+// ---- spatial order (ds_sort.cu) -----------------------------------------------
+size_t sort_temp_bytes(int64_t n);
+cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
+                                int32_t* perm, int32_t* inv, unsigned long long* keys,
+                                unsigned long long* keys_alt, int32_t* idx, void* temp,
+                                size_t temp_bytes, unsigned int* bbox, cudaStream_t s);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
 // ---- error plumbing (ds_api.cu) -----------------------------------------------

@@ -179,7 +179,8 @@ template <int ROUND>
 __global__ void __launch_bounds__(128) union_chunks_kernel(
     const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
     const uint2* __restrict__ words, int64_t n, const uint8_t* __restrict__ core,
-    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin) {
+    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
+    const int32_t* __restrict__ perm) {
   __shared__ int lp[2 * TILE];
   __shared__ int gr[2 * TILE];
   __shared__ int lb[2 * TILE];
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(128) union_chunks_kernel(
           if (ROUND == 1 || gr[u] != gr[v]) unite_local(lp, u, v);
         }
         uint32_t bm = x & ~cw;  // core u in range of non-core v (merge.py:116-130)
-        const int gu = ci.a * TILE + u;
+        const int gu = perm ? perm[ci.a * TILE + u] : ci.a * TILE + u;  // original index
         while (bm) {
           const int t = __clz(bm);
           bm &= ~(0x80000000u >> t);
@@ -231,7 +232,21 @@ __global__ void __launch_bounds__(128) union_chunks_kernel(
         }
       } else {
         const uint32_t cm = x & cw;  // non-core u: its lowest in-range core
-        if (cm) atomicMin(&lb[u], (diag ? ci.a : ci.b) * TILE + w * 32 + __clz(cm));
+        if (cm) {
+          const int jb0 = (diag ? ci.a : ci.b) * TILE + w * 32;
+          if (perm) {  // lowest ORIGINAL index among the in-range cores of the word
+            int best = NONE;
+            uint32_t mm = cm;
+            while (mm) {
+              const int t = __clz(mm);
+              mm &= ~(0x80000000u >> t);
+              best = min(best, perm[jb0 + t]);
+            }
+            atomicMin(&lb[u], best);
+          } else {
+            atomicMin(&lb[u], jb0 + __clz(cm));
+          }
+        }
       }
     }
     __syncthreads();
@@ -289,8 +304,11 @@ __global__ void compress_kernel(const uint8_t* __restrict__ core, int64_t n, int
   if (i < n && core[i]) parent[i] = find_root_ro(parent, (int)i);
 }
 
+// Runs over sorted indices s; bmin holds ORIGINAL indices of cores, cmin collects
+// the lowest ORIGINAL member index of each root (borders included).
 __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __restrict__ parent,
                              const int32_t* __restrict__ bmin, int64_t n,
+                             const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
                              int32_t* __restrict__ root, int32_t* cmin) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -299,18 +317,20 @@ __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __
     r = parent[i];
   } else {
     const int b = bmin[i];
-    if (b != NONE) r = parent[b];
+    if (b != NONE) r = parent[inv ? inv[b] : b];
   }
   root[i] = r;
-  if (r >= 0) atomicMin(&cmin[r], (int)i);  // first appearance of the cluster
+  if (r >= 0) atomicMin(&cmin[r], perm ? perm[i] : (int)i);  // first appearance
 }
 
+// flag[o] = 1 iff original index o is the first appearance of its cluster
 __global__ void flags_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
-                             int64_t n, int32_t* __restrict__ flag) {
+                             int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int r = root[i];
-  flag[i] = (r >= 0 && cmin[r] == (int)i) ? 1 : 0;
+  const int o = perm ? perm[i] : (int)i;
+  flag[o] = (r >= 0 && cmin[r] == o) ? 1 : 0;
 }
 
 // block-wide exclusive scan of one int per thread; also returns the block total
@@ -389,21 +409,25 @@ __global__ void scan_apply_kernel(int32_t* flag, int64_t n, const int32_t* __res
 }
 
 __global__ void label_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
-                             const int32_t* __restrict__ id, int64_t n, int64_t* __restrict__ labels) {
+                             const int32_t* __restrict__ id, int64_t n,
+                             const int32_t* __restrict__ perm, int64_t* __restrict__ labels) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int r = root[i];
-  labels[i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
+  labels[perm ? perm[i] : i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
 }
 
-__global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ out) {
+__global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n,
+                                  const int32_t* __restrict__ perm, int64_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = cnt[i];
+  if (i < n) out[perm ? perm[i] : i] = cnt[i];
 }
 
-// chunks -> dense native-word rows, both orientations (the chunks only hold a <= b)
+// chunks -> dense native-word rows in ORIGINAL index order, both orientations
+// (the chunks only hold a <= b)
 __global__ void export_bits_kernel(const uint2* __restrict__ words, const uint4* __restrict__ chunks,
-                                   const unsigned long long* __restrict__ nchunks, uint32_t* bits32,
+                                   const unsigned long long* __restrict__ nchunks,
+                                   const int32_t* __restrict__ perm, uint32_t* bits32,
                                    int64_t stride_words) {
   const unsigned long long total = *nchunks;
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
@@ -411,13 +435,15 @@ __global__ void export_bits_kernel(const uint2* __restrict__ words, const uint4*
     for (int k = threadIdx.x; k < ci.count; k += blockDim.x) {
       const uint2 rec = words[ci.base + k];
       uint32_t x = rec.x;
-      const int64_t i = (int64_t)ci.a * TILE + (rec.y >> 4);
+      const int64_t is = (int64_t)ci.a * TILE + (rec.y >> 4);
+      const int64_t i = perm ? perm[is] : is;
       const int64_t jw = (int64_t)ci.b * WPR + (rec.y & 15u);
-      atomicOr(&bits32[i * stride_words + jw], x);
       while (x) {
         const int t = __clz(x);
         x &= ~(0x80000000u >> t);
-        const int64_t j = jw * 32 + t;
+        const int64_t js = jw * 32 + t;
+        const int64_t j = perm ? perm[js] : js;
+        atomicOr(&bits32[i * stride_words + (j >> 5)], 0x80000000u >> (j & 31));
         atomicOr(&bits32[j * stride_words + (i >> 5)], 0x80000000u >> (i & 31));
       }
     }
@@ -464,9 +490,9 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   union_chunks_kernel<1><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
-                                                 w.parent, w.bmin);
+                                                 w.parent, w.bmin, w.perm);
   union_chunks_kernel<2><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
-                                                 w.parent, w.bmin);
+                                                 w.parent, w.bmin, w.perm);
   return cudaGetLastError();
 }
 
@@ -484,13 +510,13 @@ cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
   const int t = 256;
   const unsigned b = blocks_for(w.n, t);
   compress_kernel<<<b, t, 0, s>>>(w.core, w.n, w.parent);
-  roots_kernel<<<b, t, 0, s>>>(w.core, w.parent, w.bmin, w.n, w.root, w.cmin);
-  flags_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.n, w.flag);
+  roots_kernel<<<b, t, 0, s>>>(w.core, w.parent, w.bmin, w.n, w.perm, w.inv, w.root, w.cmin);
+  flags_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.n, w.perm, w.flag);
   const int64_t np = scan_partials_len(w.n);
   scan_partials_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
   scan_top_kernel<<<1, SCAN_T, 0, s>>>(w.partials, np, w.nclusters);
   scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
-  label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, labels);
+  label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, w.perm, labels);
   return cudaGetLastError();
 }
 
@@ -503,6 +529,23 @@ cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R
   return cudaGetLastError();
 }
 
+// counts between sorted order (device workspace) and original order (shard ABI)
+__global__ void permute_i32_kernel(const int32_t* __restrict__ src, int64_t n,
+                                   const int32_t* __restrict__ perm, int to_original,
+                                   int32_t* __restrict__ dst) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t o = perm ? perm[s] : s;
+  if (to_original) dst[o] = src[s];
+  else dst[s] = src[o];
+}
+
+cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* perm, int to_original,
+                               int32_t* dst, cudaStream_t s) {
+  permute_i32_kernel<<<blocks_for(n, 256), 256, 0, s>>>(src, n, perm, to_original, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
                                   cudaStream_t s) {
   const int64_t np = scan_partials_len(n);
@@ -512,15 +555,16 @@ cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, int64_t* out, cudaStream_t s) {
-  counts_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(cnt, n, out);
+cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
+                              cudaStream_t s) {
+  counts_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(cnt, n, perm, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
-                               const unsigned long long* nchunks, uint32_t* bits32,
-                               int64_t stride_words, cudaStream_t s) {
-  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, chunks, nchunks, bits32, stride_words);
+                               const unsigned long long* nchunks, const int32_t* perm,
+                               uint32_t* bits32, int64_t stride_words, cudaStream_t s) {
+  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, chunks, nchunks, perm, bits32, stride_words);
   return cudaGetLastError();
 }
 

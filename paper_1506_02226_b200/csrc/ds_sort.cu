@@ -1,0 +1,123 @@
+// Spatial ordering of the points before tiling.
+//
+// The eps-tile kernel evaluates 512 x 512 tile pairs, and bounding-box culling
+// (ds_tile.cu, keep_item) skips the pairs of tiles that are provably apart. Both
+// work best when a tile is a compact region: the points are therefore visited in
+// Morton (Z-curve) order of their quantised coordinates. Sorting only changes
+// which pairs share a tile, never a pair's arithmetic, so bits and counts are
+// unchanged; every index-dependent rule (the lowest-indexed-core border rule,
+// merge.py:116-130, and first-appearance numbering, core.py:116-132) is applied
+// to ORIGINAL indices through perm / inv (ds_merge.cu).
+//
+// Keys: up to 4 leading dimensions, 64 / k bits each (2-D: 32 bits per dim),
+// over the global bounding box. The sort is CUB's stable LSD radix sort on
+// (key, original index), so the permutation is deterministic and identical on
+// every rank.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/cub.cuh>
+
+#include "ds_internal.cuh"
+
+namespace ds {
+namespace {
+
+__global__ void bbox_kernel(const float* __restrict__ rec, int64_t n, int S, int kd,
+                            unsigned int* __restrict__ lo_bits, unsigned int* __restrict__ hi_bits) {
+  // order-preserving float -> uint mapping for atomicMin/Max
+  for (int k = 0; k < kd; ++k) {
+    float mn = INFINITY, mx = -INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const float v = rec[i * S + k];
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    for (int off = 16; off; off >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      auto ord = [](float f) {
+        const unsigned int u = __float_as_uint(f);
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      };
+      atomicMin(&lo_bits[k], ord(mn));
+      atomicMax(&hi_bits[k], ord(mx));
+    }
+  }
+}
+
+__device__ __forceinline__ float unord(unsigned int u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, int kd,
+                              const unsigned int* __restrict__ lo_bits,
+                              const unsigned int* __restrict__ hi_bits,
+                              unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int bits = 64 / kd > 32 ? 32 : 64 / kd;
+  const double levels = (double)((1ull << bits) - 1);
+  uint32_t q[4] = {0, 0, 0, 0};
+  for (int k = 0; k < kd; ++k) {
+    const double lo = unord(lo_bits[k]), hi = unord(hi_bits[k]);
+    const double span = hi - lo;
+    double t = span > 0 ? ((double)rec[i * S + k] - lo) / span * levels : 0.0;
+    t = t < 0 ? 0 : (t > levels ? levels : t);  // NaN -> 0 via the comparisons below
+    q[k] = (t == t) ? (uint32_t)t : 0u;
+  }
+  unsigned long long key = 0;
+  for (int b = bits - 1; b >= 0; --b)
+    for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
+  keys[i] = key;
+  idx[i] = (int32_t)i;
+}
+
+__global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
+                               const int32_t* __restrict__ perm, float* __restrict__ out,
+                               int32_t* __restrict__ inv) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t o = perm[s];
+  const float4* src = reinterpret_cast<const float4*>(rec + o * S);
+  float4* dst = reinterpret_cast<float4*>(out + s * S);
+  for (int v = 0; v < S / 4; ++v) dst[v] = src[v];
+  inv[o] = (int32_t)s;
+}
+
+}  // namespace
+
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)n);
+  return bytes;
+}
+
+cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
+                                int32_t* perm, int32_t* inv, unsigned long long* keys,
+                                unsigned long long* keys_alt, int32_t* idx, void* temp,
+                                size_t temp_bytes, unsigned int* bbox, cudaStream_t s) {
+  const int dp = padded_dim(d);
+  const int S = rec_stride(d);
+  const int kd = d < 4 ? d : 4;
+  cudaError_t e = cudaMemsetAsync(bbox, 0xff, 4 * sizeof(unsigned int), s);  // lo = max
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(bbox + 4, 0, 4 * sizeof(unsigned int), s);             // hi = min
+  if (e != cudaSuccess) return e;
+  (void)dp;
+  bbox_kernel<<<148 * 4, 256, 0, s>>>(rec, n, S, kd, bbox, bbox + 4);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, bbox, bbox + 4, keys, idx);
+  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, idx, perm, (int)n, 0, 64,
+                                      s);
+  if (e != cudaSuccess) return e;
+  permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted, inv);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

@@ -133,7 +133,7 @@ def _fused(points: PointSet, params: DbscanParams, formula: int, mem_cap, device
     # the exported matrix is n x ceil(n/8) host bytes, guarded like kernels.py:318
     ensure_capacity(n * row_bytes(n), mem_cap)
     ctx = _native.context(device)
-    ctx.set_tile_cull(True)
+    ctx.configure(True, True)
     bits, counts, valid, t = ctx.fused_build(points.coords_aos, params.eps_sq, params.min_pts,
                                              formula, 0)
     return (NeighborhoodMatrix(n=n, bits=bits, neighbor_count=counts),

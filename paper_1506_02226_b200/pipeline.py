@@ -37,8 +37,9 @@ class PipelineConfig:
     `threads` is validated as in the reference but the device ignores it.
     `device` picks the CUDA ordinal (None: $DENSESCAN_DEVICE or 0).
     `prune` skips tile pairs whose bounding boxes prove every pair out of range
-    (with a float32 error margin; results are bit-identical either way);
-    prune=False runs the paper's dense all-pairs schedule.
+    (with a float32 error margin) and `spatial_order` visits the points in
+    Morton order so tiles are compact; results are bit-identical either way,
+    and prune=False, spatial_order=False is the paper's dense all-pairs schedule.
     """
 
     variant: KernelVariant
@@ -47,6 +48,7 @@ class PipelineConfig:
     mem_cap: int | None = None
     device: int | None = None
     prune: bool = True
+    spatial_order: bool = True
 
     def __post_init__(self):
         if isinstance(self.threads, bool) or not (
@@ -120,7 +122,7 @@ def run_dbscan(points: PointSet, params: DbscanParams, config: PipelineConfig):
         # the reference allocates the 4 n^2 float32 matrix for these rungs (kernels.py:156)
         ensure_capacity(4 * points.n * points.n, mem_cap)
     ctx = _native.context(config.device)
-    ctx.set_tile_cull(config.prune)
+    ctx.configure(config.prune, config.spatial_order)
     labels, _, t = ctx.run_dbscan(points.coords_aos, params.eps_sq, params.min_pts,
                                   variant.formula, mem_cap)
     total = (time.perf_counter() - t0) * 1e3

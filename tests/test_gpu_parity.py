@@ -258,13 +258,13 @@ def test_shard_stages_fold_to_reference_labels(ds, shards, cull):
         ctx.close()
 
 
-def _labels_counts(ds, coords, eps_sq, min_pts, formula, prune):
+def _labels_counts(ds, coords, eps_sq, min_pts, formula, prune, order=True):
     ctx = ds._native.context()
-    ctx.set_tile_cull(prune)
+    ctx.configure(prune, order)
     try:
         labels, counts, t = ctx.run_dbscan(coords, eps_sq, min_pts, formula, 0, want_counts=True)
     finally:
-        ctx.set_tile_cull(True)
+        ctx.configure(True, True)
     return labels, counts, t
 
 
@@ -285,7 +285,7 @@ def test_tile_culling_is_exact(ds, oracle, rng):
     for coords, eps_sq, mp in cases:
         for f in (0, 1):
             lc, cc, tc = _labels_counts(ds, coords, eps_sq, mp, f, True)
-            ld, cd, td = _labels_counts(ds, coords, eps_sq, mp, f, False)
+            ld, cd, td = _labels_counts(ds, coords, eps_sq, mp, f, False, False)
             assert np.array_equal(cc, cd) and np.array_equal(lc, ld)
             want, wc = oracle.dbscan(coords, eps_sq, mp, f)
             assert np.array_equal(cc, wc) and np.array_equal(lc, want)
@@ -302,3 +302,24 @@ def test_culling_skips_work_on_c2(ds):
     lab_dense, t_dense = ds.run_dbscan(pts, params, dense_cfg)
     assert np.array_equal(lab_dense.labels, load_golden("c2.npz")["labels"])
     assert t_cull.pairs_evaluated < 0.5 * t_dense.pairs_evaluated
+
+
+@pytest.mark.parametrize("prune,order", [(True, True), (True, False), (False, True),
+                                         (False, False)])
+def test_schedules_shuffled_input(ds, oracle, rng, prune, order):
+    """Random input order (worst case for tiles) and border points shared by
+    several clusters: the lowest-ORIGINAL-index core rule must survive the
+    spatial permutation."""
+    base = ds.generate_blobs(4000, 6, 0.25, 0.15, 17, 2).coords_aos
+    coords = base[rng.permutation(base.shape[0])]
+    # bridges of sparse points between blobs create multi-cluster border points
+    bridge = np.stack([np.linspace(0, 5.0, 60), np.zeros(60)], 1)
+    coords = np.concatenate([coords, bridge])[rng.permutation(coords.shape[0] + 60)]
+    for f in (0, 1):
+        labels, counts, _ = _labels_counts(ds, coords, 0.03, 6, f, prune, order)
+        want, wc = oracle.dbscan(coords, 0.03, 6, f)
+        assert np.array_equal(counts, wc) and np.array_equal(labels, want)
+        nbr, valid = ds.fused_build_algebraic(ds.PointSet(coords), ds.validate_params(
+            np.sqrt(0.03), 6), ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC))
+        obits, _ = oracle.neighborhood(coords, np.sqrt(0.03) ** 2, 1)
+        assert np.array_equal(nbr.bits, obits)
