@@ -122,19 +122,22 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
   return r;
 }
 
-// ---- union over tile-pair chunks (two rounds, shared-memory local forests) ---------
-// Round 1 (diagonal chunks, one per tile): the core-core words of tile a with
-// itself are merged in a shared-memory union-find over the tile's 512 points;
-// every core point then gets parent = its local root (the smallest index of
-// its local component). Each tile is owned by exactly one CTA, so these
-// writes need no atomics.
-// Round 2 (off-diagonal chunks): the 1024 points of tiles a and b first look
-// up their current global roots; a core-core bit whose endpoints already share
-// a root costs nothing, the others are merged in shared memory, and only one
-// global link per (local component, differing global root) is issued. In dense
-// regions that is ~1 global CAS per tile pair instead of one per in-range pair.
-// Border minima are reduced per chunk in shared memory, then once per point in
-// global memory.
+// ---- union over tile-pair chunks (two rounds) --------------------------------------
+// Round 1, one CTA per diagonal chunk (tile a with itself, words hold j >= i):
+//   * every in-range core pair (u < v) proposes u as v's minimum neighbour
+//     (shared-memory atomicMin, no CAS);
+//   * pointer jumping on that min-neighbour forest (9 halvings cover 512 nodes);
+//   * the few pairs whose endpoints still have different roots are merged with a
+//     shared-memory union-find (CAS on the larger root);
+//   * every core point gets parent = its local root (the smallest index of its
+//     local component) — each tile is owned by one CTA, so no global atomics.
+// Round 2, one CTA per off-diagonal chunk (tiles a < b): each point's current
+// ancestor is one coalesced load; the dominant ancestor of each tile (the
+// round-1 giant component in dense regions) is found with a shared histogram.
+// A core-core bit whose tile-b end hangs under tile b's dominant ancestor is
+// covered by one global link per chunk; the other bits link their two
+// ancestors directly (rare). Border minima (lowest ORIGINAL core index,
+// merge.py:116-130) are reduced per chunk in shared memory, then once per point.
 struct ChunkInfo {
   int a, b;
   unsigned long long base;
@@ -175,91 +178,314 @@ __device__ __forceinline__ void unite_local(int* lp, int u, int v) {
   }
 }
 
-template <int ROUND>
-__global__ void __launch_bounds__(128) union_chunks_kernel(
+__device__ __forceinline__ int orig_of(const int32_t* perm, int g) { return perm ? perm[g] : g; }
+
+// lowest ORIGINAL index among the core points flagged in `bits` of word column jb0
+__device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t bits) {
+  if (!perm) return jb0 + __clz(bits);
+  int best = NONE;
+  while (bits) {
+    const int t = __clz(bits);
+    bits &= ~(0x80000000u >> t);
+    best = min(best, perm[jb0 + t]);
+  }
+  return best;
+}
+
+// Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
+__global__ void __launch_bounds__(512) union_diag_kernel(
     const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
-    const uint2* __restrict__ words, int64_t n, const uint8_t* __restrict__ core,
-    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
-    const int32_t* __restrict__ perm) {
-  __shared__ int lp[2 * TILE];
-  __shared__ int gr[2 * TILE];
-  __shared__ int lb[2 * TILE];
+    const uint2* __restrict__ words, int64_t n, const uint32_t* __restrict__ corew,
+    int32_t* parent, int32_t* bmin, const int32_t* __restrict__ perm) {
+  constexpr int THREADS = 512;
+  constexpr int RB = TILE / (THREADS / WPR);  // rows per block: 16
+  extern __shared__ uint32_t dsm[];
+  uint32_t* R = dsm;                         // [WPR][TILE] core-masked adjacency words
+  uint32_t* M = R + WPR * TILE;              // [THREADS / WPR][WPR] row-block column masks
+  int* lp = reinterpret_cast<int*>(M + THREADS);
+  int* lb = lp + TILE;
+  int* hist = lb + TILE;
+  __shared__ uint32_t lcw[WPR];
+  __shared__ uint32_t adj[32];
+  __shared__ int wroots[WPR], wpre[WPR], slot_root[32];
+  __shared__ int ntrees_sh;
+  const int tid = threadIdx.x;
+  const int w = tid % WPR, cblk = tid / WPR;
+  const unsigned long long total = *nchunks;
+  const int64_t nw = (n + 31) / 32;
+  for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
+    const ChunkInfo ci = decode_chunk(chunks[c]);
+    if (ci.a != ci.b) continue;  // uniform per CTA
+    const int base = ci.a * TILE;
+    if (tid < WPR) {
+      const int64_t gw = (int64_t)ci.a * WPR + tid;
+      lcw[tid] = gw < nw ? corew[gw] : 0u;
+    }
+    for (int k = tid; k < WPR * TILE; k += THREADS) R[k] = 0u;
+    for (int v = tid; v < TILE; v += THREADS) {
+      lp[v] = v;
+      lb[v] = NONE;
+      hist[v] = 0;
+    }
+    __syncthreads();
+    // scatter the chunk into the dense matrix (core rows, core columns only);
+    // non-core rows give their own border candidate directly
+    for (int k = tid; k < ci.count; k += THREADS) {
+      const uint2 rec = words[ci.base + k];
+      const int u = (int)(rec.y >> 4);
+      const int ww = (int)(rec.y & 15u);
+      const uint32_t cw = lcw[ww];
+      if ((lcw[u >> 5] >> (31 - (u & 31))) & 1u) {
+        R[ww * TILE + u] = rec.x & cw;
+        uint32_t bm = rec.x & ~cw;  // core u in range of non-core v (merge.py:116-130)
+        if (bm) {
+          const int gu = orig_of(perm, base + u);
+          while (bm) {
+            const int t = __clz(bm);
+            bm &= ~(0x80000000u >> t);
+            atomicMin(&lb[ww * 32 + t], gu);
+          }
+        }
+      } else {
+        const uint32_t cm = rec.x & cw;
+        if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
+      }
+    }
+    __syncthreads();
+    // minimum neighbour of every core column = first row (ascending) holding it:
+    // OR per row block, exclusive prefix OR over blocks, then a second scan writes
+    // each column exactly once
+    uint32_t acc = 0;
+    for (int r = 0; r < RB; ++r) acc |= R[w * TILE + cblk * RB + r];
+    M[cblk * WPR + w] = acc;
+    __syncthreads();
+    uint32_t seen = 0;
+    for (int q = 0; q < cblk; ++q) seen |= M[q * WPR + w];
+    for (int r = 0; r < RB; ++r) {
+      const int u = cblk * RB + r;
+      const uint32_t x = R[w * TILE + u];
+      uint32_t fresh = x & ~seen;
+      seen |= x;
+      while (fresh) {
+        const int t = __clz(fresh);
+        fresh &= ~(0x80000000u >> t);
+        lp[w * 32 + t] = u;  // u <= column: parent pointers decrease
+      }
+    }
+    __syncthreads();
+    // pointer jumping over the min-neighbour forest (9 halvings cover 512 nodes)
+#pragma unroll 1
+    for (int r = 0; r < 9; ++r) {
+      const int nv = lp[lp[tid]];
+      __syncthreads();
+      lp[tid] = nv;
+      __syncthreads();
+    }
+    // merge the min-neighbour trees. Roots get slots in index order; with <= 32
+    // trees every word ANDs its row's complement mask against the tree masks to
+    // find crossing trees, and a 32 x 32 boolean closure (one warp) merges them —
+    // no per-bit work. More trees (sparse tiles, few bits) use a shared-memory
+    // union-find over the crossing bits.
+    const bool is_core = (lcw[tid >> 5] >> (31 - (tid & 31))) & 1u;
+    const bool is_root = is_core && lp[tid] == tid;
+    const uint32_t rball = __ballot_sync(0xffffffffu, is_root);
+    if ((tid & 31) == 0) wroots[tid >> 5] = __popc(rball);
+    for (int k = tid; k < 32 * WPR; k += THREADS) M[k] = 0u;  // M becomes T[32][WPR]
+    if (tid < 32) adj[tid] = 0u;
+    __syncthreads();
+    if (tid < 32) {  // exclusive prefix of roots per warp -> slots in index order
+      const int cnt = tid < WPR ? wroots[tid] : 0;
+      int incl = cnt;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (tid >= off) incl += y;
+      }
+      if (tid < WPR) wpre[tid] = incl - cnt;
+      if (tid == 31) ntrees_sh = incl;
+    }
+    __syncthreads();
+    const int ntrees = ntrees_sh;
+    if (is_root) {
+      const int k = wpre[tid >> 5] + __popc(rball & ((1u << (tid & 31)) - 1u));
+      hist[tid] = k;                     // root node -> slot
+      if (k < 32) slot_root[k] = tid;    // slot -> root node
+    }
+    __syncthreads();
+    if (ntrees <= 32) {
+      if (is_core) atomicOr(&M[hist[lp[tid]] * WPR + (tid >> 5)], 0x80000000u >> (tid & 31));
+      __syncthreads();
+      for (int r = 0; r < RB; ++r) {
+        const int u = cblk * RB + r;
+        const uint32_t um = R[w * TILE + u];
+        if (!um) continue;
+        const int k = hist[lp[u]];
+        const uint32_t cross = um & ~M[k * WPR + w];
+        if (!cross) continue;
+        uint32_t bits = 0;
+        for (int j = 0; j < ntrees; ++j)
+          if (cross & M[j * WPR + w]) bits |= 1u << j;
+        atomicOr(&adj[k], bits);
+      }
+      __syncthreads();
+      if (tid < 32) {  // symmetric transitive closure of the tree graph (one warp)
+        uint32_t row = adj[tid] | (1u << tid);
+        uint32_t col = 0;
+        for (int j = 0; j < 32; ++j)
+          if ((__shfl_sync(0xffffffffu, row, j) >> tid) & 1u) col |= 1u << j;
+        row |= col;
+        for (int p = 0; p < 32; ++p) {
+          const uint32_t rp = __shfl_sync(0xffffffffu, row, p);
+          if ((row >> p) & 1u) row |= rp;
+        }
+        adj[tid] = row;
+      }
+      __syncthreads();
+      if (is_core) {  // lowest slot of the merged component = its smallest root
+        const int kmin = __ffs(adj[hist[lp[tid]]]) - 1;
+        lp[tid] = slot_root[kmin];
+      }
+    } else {
+      for (int r = 0; r < RB; ++r) {
+        const int u = cblk * RB + r;
+        uint32_t um = R[w * TILE + u];
+        const int ru = lp[u];
+        while (um) {
+          const int t = __clz(um);
+          um &= ~(0x80000000u >> t);
+          const int v = w * 32 + t;
+          if (lp[v] != ru) unite_local(lp, u, v);
+        }
+      }
+    }
+    __syncthreads();
+    {
+      const int v = tid;
+      const int64_t g = (int64_t)base + v;
+      if (g < n) {
+        const int r = find_local(lp, v);
+        if (r != v) parent[g] = base + r;  // r < v: parent[x] <= x holds
+        if (lb[v] != NONE) atomicMin(&bmin[g], lb[v]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) union_pair_kernel(
+    const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
+    const uint2* __restrict__ words, int64_t n, const uint32_t* __restrict__ corew,
+    int32_t* parent, int32_t* bmin, const int32_t* __restrict__ perm) {
+  __shared__ int la[2 * TILE];    // current ancestor of each point (-1: not core)
+  __shared__ int lb[2 * TILE];    // border minima (original indices)
+  __shared__ int hist[2 * TILE];  // ancestors that are local indices of the own tile
   __shared__ uint32_t lcw[2 * WPR];
+  __shared__ uint32_t mb[WPR];    // tile-b points under tile b's dominant ancestor
+  __shared__ int dom[2];
+  __shared__ int link_ab;
   const int tid = threadIdx.x;
   const unsigned long long total = *nchunks;
   const int64_t nw = (n + 31) / 32;
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
     const ChunkInfo ci = decode_chunk(chunks[c]);
-    const bool diag = ci.a == ci.b;
-    if ((ROUND == 1) != diag) continue;  // uniform per CTA
-    const int nloc = diag ? TILE : 2 * TILE;
-    for (int v = tid; v < nloc; v += blockDim.x) {
-      const int64_t g = (int64_t)(v < TILE ? ci.a : ci.b) * TILE + (v & (TILE - 1));
-      lp[v] = v;
-      lb[v] = NONE;
-      int r = (int)g;
-      if (ROUND == 2 && g < n && core[g]) r = find_plain(parent, (int)g);
-      gr[v] = r;
-    }
-    if (tid < (diag ? WPR : 2 * WPR)) {
+    if (ci.a == ci.b) continue;  // uniform per CTA
+    if (tid < 2 * WPR) {
       const int64_t gw = (int64_t)(tid < WPR ? ci.a : ci.b) * WPR + (tid & (WPR - 1));
       lcw[tid] = gw < nw ? corew[gw] : 0u;
     }
+    for (int v = tid; v < 2 * TILE; v += THREADS) {
+      hist[v] = 0;
+      lb[v] = NONE;
+    }
+    if (tid == 0) link_ab = 0;
     __syncthreads();
-    const int jb = diag ? 0 : TILE;  // local index of column 0 of tile b
-    for (int k = tid; k < ci.count; k += blockDim.x) {
+    for (int v = tid; v < 2 * TILE; v += THREADS) {
+      const int tb = v < TILE ? ci.a : ci.b;
+      const int64_t g = (int64_t)tb * TILE + (v & (TILE - 1));
+      const bool cv = g < n && ((lcw[v >> 5] >> (31 - (v & 31))) & 1u);
+      int anc = -1;
+      if (cv) {
+        anc = parent[g];
+        const int rel = anc - tb * TILE;
+        if (rel >= 0 && rel < TILE) atomicAdd(&hist[(v & TILE) + rel], 1);
+      }
+      la[v] = anc;
+    }
+    __syncthreads();
+    // dominant ancestor per tile: argmax of the histogram (one warp per tile)
+    if (tid < 64) {
+      const int half = tid >> 5, lane = tid & 31;
+      int best = -1, bestc = 0;
+      for (int r = lane; r < TILE; r += 32) {
+        const int h = hist[half * TILE + r];
+        if (h > bestc) {
+          bestc = h;
+          best = r;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        const int oc = __shfl_xor_sync(0xffffffffu, bestc, off);
+        const int ob = __shfl_xor_sync(0xffffffffu, best, off);
+        if (oc > bestc || (oc == bestc && ob >= 0 && (best < 0 || ob < best))) {
+          bestc = oc;
+          best = ob;
+        }
+      }
+      if (lane == 0) dom[half] = best < 0 ? -1 : (half ? ci.b : ci.a) * TILE + best;
+    }
+    __syncthreads();
+    const int gb = dom[1];
+    for (int ww = tid; ww < WPR; ww += THREADS) {
+      uint32_t m = 0;
+      for (int t = 0; t < 32; ++t)
+        if (gb >= 0 && la[TILE + ww * 32 + t] == gb) m |= 0x80000000u >> t;
+      mb[ww] = m;
+    }
+    __syncthreads();
+    const int ga = dom[0];
+    for (int k = tid; k < ci.count; k += THREADS) {
       const uint2 rec = words[ci.base + k];
       const uint32_t x = rec.x;
       const int u = (int)(rec.y >> 4);
       const int w = (int)(rec.y & 15u);
-      const uint32_t cw = lcw[(diag ? 0 : WPR) + w];
-      const bool cu = (lcw[u >> 5] >> (31 - (u & 31))) & 1u;
-      const int vb = jb + w * 32;
-      if (cu) {
-        uint32_t um = x & cw;  // core-core (merge.py:149-159)
-        while (um) {
-          const int t = __clz(um);
-          um &= ~(0x80000000u >> t);
-          const int v = vb + t;
-          if (ROUND == 1 || gr[u] != gr[v]) unite_local(lp, u, v);
+      const uint32_t cw = lcw[WPR + w];
+      const int vb = TILE + w * 32;
+      if (la[u] >= 0) {
+        const int au = la[u];
+        const uint32_t um = x & cw;
+        const uint32_t hit = um & mb[w];
+        if (hit) {
+          if (au == ga) link_ab = 1;  // benign race: every writer stores 1
+          else if (au != gb) link_root(parent, find_plain(parent, au), gb);
         }
-        uint32_t bm = x & ~cw;  // core u in range of non-core v (merge.py:116-130)
-        const int gu = perm ? perm[ci.a * TILE + u] : ci.a * TILE + u;  // original index
-        while (bm) {
-          const int t = __clz(bm);
-          bm &= ~(0x80000000u >> t);
-          atomicMin(&lb[vb + t], gu);
+        uint32_t rest = um & ~mb[w];
+        while (rest) {
+          const int t = __clz(rest);
+          rest &= ~(0x80000000u >> t);
+          const int av = la[vb + t];
+          if (av != au) link_root(parent, find_plain(parent, au), av);
         }
-      } else {
-        const uint32_t cm = x & cw;  // non-core u: its lowest in-range core
-        if (cm) {
-          const int jb0 = (diag ? ci.a : ci.b) * TILE + w * 32;
-          if (perm) {  // lowest ORIGINAL index among the in-range cores of the word
-            int best = NONE;
-            uint32_t mm = cm;
-            while (mm) {
-              const int t = __clz(mm);
-              mm &= ~(0x80000000u >> t);
-              best = min(best, perm[jb0 + t]);
-            }
-            atomicMin(&lb[u], best);
-          } else {
-            atomicMin(&lb[u], jb0 + __clz(cm));
+        uint32_t bm = x & ~cw;
+        if (bm) {
+          const int gu = orig_of(perm, ci.a * TILE + u);
+          while (bm) {
+            const int t = __clz(bm);
+            bm &= ~(0x80000000u >> t);
+            atomicMin(&lb[vb + t], gu);
           }
         }
+      } else {
+        const uint32_t cm = x & cw;
+        if (cm) atomicMin(&lb[u], min_orig(perm, ci.b * TILE + w * 32, cm));
       }
     }
     __syncthreads();
-    for (int v = tid; v < nloc; v += blockDim.x) {
+    if (tid == 0 && link_ab && ga >= 0 && gb >= 0 && ga != gb)
+      link_root(parent, find_plain(parent, ga), gb);
+    for (int v = tid; v < 2 * TILE; v += THREADS) {
+      if (lb[v] == NONE) continue;
       const int64_t g = (int64_t)(v < TILE ? ci.a : ci.b) * TILE + (v & (TILE - 1));
-      if (g >= n) continue;
-      const int r = find_local(lp, v);
-      if (ROUND == 1) {
-        if (r != v) parent[g] = (int)((int64_t)ci.a * TILE + r);  // r < v: parent[x] <= x holds
-      } else if (r != v && gr[v] != gr[r]) {
-        link_root(parent, find_plain(parent, gr[v]), gr[r]);
-      }
-      if (lb[v] != NONE) atomicMin(&bmin[g], lb[v]);
+      atomicMin(&bmin[g], lb[v]);
     }
     __syncthreads();
   }
@@ -489,10 +715,18 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  union_chunks_kernel<1><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
-                                                 w.parent, w.bmin, w.perm);
-  union_chunks_kernel<2><<<sms * 16, 128, 0, s>>>(chunks, nchunks, words, w.n, w.core, w.corew,
-                                                 w.parent, w.bmin, w.perm);
+  // round 1: one chunk per tile (few, dense) -> wide CTAs; round 2: many chunks
+  const size_t diag_smem = (size_t)(WPR * TILE + 512) * 4 + (size_t)3 * TILE * 4;
+  static bool diag_cfg = false;
+  if (!diag_cfg) {
+    cudaFuncSetAttribute(union_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)diag_smem);
+    diag_cfg = true;
+  }
+  union_diag_kernel<<<sms * 2, 512, diag_smem, s>>>(chunks, nchunks, words, w.n, w.corew,
+                                                    w.parent, w.bmin, w.perm);
+  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(chunks, nchunks, words, w.n, w.corew, w.parent,
+                                                 w.bmin, w.perm);
   return cudaGetLastError();
 }
 

@@ -9,8 +9,9 @@
 // merge.py:116-130, and first-appearance numbering, core.py:116-132) is applied
 // to ORIGINAL indices through perm / inv (ds_merge.cu).
 //
-// Keys: up to 4 leading dimensions, 64 / k bits each (2-D: 32 bits per dim),
-// over the global bounding box. The sort is CUB's stable LSD radix sort on
+// Keys: up to 4 leading dimensions quantised to a 2^(24/k)-per-dimension grid
+// over the global bounding box (24-bit keys: three radix passes; 4096 cells per
+// dimension in 2-D is far finer than a 512-point tile). The sort is CUB's stable LSD radix sort on
 // (key, original index), so the permutation is deterministic and identical on
 // every rank.
 #include <cuda_runtime.h>
@@ -23,9 +24,21 @@
 namespace ds {
 namespace {
 
+constexpr int KEY_BITS = 24;
+
+__device__ __forceinline__ unsigned int ord_bits(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving float -> uint
+}
+
 __global__ void bbox_kernel(const float* __restrict__ rec, int64_t n, int S, int kd,
                             unsigned int* __restrict__ lo_bits, unsigned int* __restrict__ hi_bits) {
-  // order-preserving float -> uint mapping for atomicMin/Max
+  __shared__ unsigned int smin[4], smax[4];
+  if (threadIdx.x < 4) {
+    smin[threadIdx.x] = 0xffffffffu;
+    smax[threadIdx.x] = 0u;
+  }
+  __syncthreads();
   for (int k = 0; k < kd; ++k) {
     float mn = INFINITY, mx = -INFINITY;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -39,13 +52,14 @@ __global__ void bbox_kernel(const float* __restrict__ rec, int64_t n, int S, int
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     }
     if ((threadIdx.x & 31) == 0) {
-      auto ord = [](float f) {
-        const unsigned int u = __float_as_uint(f);
-        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-      };
-      atomicMin(&lo_bits[k], ord(mn));
-      atomicMax(&hi_bits[k], ord(mx));
+      atomicMin(&smin[k], ord_bits(mn));
+      atomicMax(&smax[k], ord_bits(mx));
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < kd) {
+    atomicMin(&lo_bits[threadIdx.x], smin[threadIdx.x]);
+    atomicMax(&hi_bits[threadIdx.x], smax[threadIdx.x]);
   }
 }
 
@@ -59,7 +73,7 @@ __global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, i
                               unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int bits = 64 / kd > 32 ? 32 : 64 / kd;
+  const int bits = KEY_BITS / kd;
   const double levels = (double)((1ull << bits) - 1);
   uint32_t q[4] = {0, 0, 0, 0};
   for (int k = 0; k < kd; ++k) {
@@ -110,11 +124,11 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   e = cudaMemsetAsync(bbox + 4, 0, 4 * sizeof(unsigned int), s);             // hi = min
   if (e != cudaSuccess) return e;
   (void)dp;
-  bbox_kernel<<<148 * 4, 256, 0, s>>>(rec, n, S, kd, bbox, bbox + 4);
+  bbox_kernel<<<148, 512, 0, s>>>(rec, n, S, kd, bbox, bbox + 4);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, bbox, bbox + 4, keys, idx);
-  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, idx, perm, (int)n, 0, 64,
-                                      s);
+  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, idx, perm, (int)n, 0,
+                                      KEY_BITS, s);
   if (e != cudaSuccess) return e;
   permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted, inv);
   return cudaGetLastError();
