@@ -231,15 +231,15 @@ def run_b200(args):
     pairs = last[1]
 
     # end-to-end through the public API with host buffers
-    e2e_ms = []
+    e2e_ms, e2e_parts = [], []
     cfg_api = ds.PipelineConfig(variant=ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC),
                                 mem_cap=mem_cap, device=local)
 
     def e2e_step():
         if world > 1:
             return D.run_dbscan_sharded(pts, params, formula=formula, mem_cap=mem_cap,
-                                        backend=backend)
-        return ds.run_dbscan(pts, params, cfg_api)
+                                        backend=backend)[1]
+        return ds.run_dbscan(pts, params, cfg_api)[1]
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -249,8 +249,9 @@ def run_b200(args):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        e2e_step()
+        st = e2e_step()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_parts.append(st)
     e2e = statistics.mean(e2e_ms)
     clk.__exit__(None, None, None)
     if world > 1:
@@ -291,7 +292,10 @@ def run_b200(args):
                                    if world > 1 else "1 GPU")},
         "e2e": {"value": n / (e2e / 1e3), "unit": "points/s",
                 "h2d_bytes_per_step": n * d * 8 * (world if world > 1 else 1),
-                "d2h_bytes_per_step": n * 8, "ms_per_step": e2e},
+                "d2h_bytes_per_step": n * 8, "ms_per_step": e2e,
+                "parts_ms": ({k: statistics.mean(getattr(p, k) or 0.0 for p in e2e_parts)
+                              for k in ("h2d_ms", "fused_ms", "merge_ms", "d2h_ms", "total_ms")}
+                             if world == 1 else None)},
         "roofline": {"bound": "fp32", "kernel": "eps_tile_kernel", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": None,

@@ -82,6 +82,14 @@ const char* ds_build_info(void);
 const char* ds_last_error(void);
 void ds_last_capacity(int64_t* required_bytes, int64_t* cap_bytes);
 
+/* Page-lock (and release) a caller-owned host range so the copies of
+ * ds_run_dbscan / ds_fused_build run at DMA speed. Frozen inputs (the
+ * reference PointSet arrays are read-only after construction, core.py:59-64)
+ * are registered once per lifetime. Registering an already registered range
+ * succeeds. */
+ds_status ds_host_register(const void* ptr, size_t bytes);
+ds_status ds_host_unregister(const void* ptr);
+
 /* Context on one CUDA device (ordinal). */
 ds_status ds_ctx_create(int device, ds_ctx** out);
 void ds_ctx_destroy(ds_ctx* ctx);

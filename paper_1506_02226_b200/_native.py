@@ -27,6 +27,7 @@ FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 EXPORTS = (
     "ds_abi_version", "ds_build_info", "ds_last_error", "ds_last_capacity",
     "ds_ctx_create", "ds_ctx_destroy", "ds_ctx_set_option", "ds_ctx_get_option",
+    "ds_host_register", "ds_host_unregister",
     "ds_run_dbscan", "ds_run_dbscan_device",
     "ds_fused_build", "ds_merge_bits", "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
     "ds_shard_stage3_local", "ds_shard_stage3_merge",
@@ -87,6 +88,10 @@ def load_library(path: str = LIB_PATH):
         lib.ds_ctx_create.restype = ctypes.c_int
         lib.ds_ctx_destroy.argtypes = [vp]
         lib.ds_ctx_destroy.restype = None
+        lib.ds_host_register.argtypes = [vp, ctypes.c_size_t]
+        lib.ds_host_register.restype = ctypes.c_int
+        lib.ds_host_unregister.argtypes = [vp]
+        lib.ds_host_unregister.restype = ctypes.c_int
         lib.ds_ctx_set_option.argtypes = [vp, ctypes.c_int32, ctypes.c_int64]
         lib.ds_ctx_set_option.restype = ctypes.c_int
         lib.ds_ctx_get_option.argtypes = [vp, ctypes.c_int32]
@@ -189,7 +194,7 @@ class Context:
                    mem_cap: int, want_counts: bool = False):
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         n, d = coords.shape
-        labels = np.empty(n, dtype=np.int64)
+        labels = pinned_empty(n)
         counts = np.empty(n, dtype=np.int64) if want_counts else None
         t = Timings()
         st = self.lib.ds_run_dbscan(self.handle, coords.ctypes.data, n, d, float(eps_sq),
@@ -270,6 +275,37 @@ class Context:
                                     ctypes.byref(t))
         raise_for(st, self.lib)
         return labels, t
+
+
+def pin_frozen(arr: np.ndarray, owner) -> bool:
+    """Page-lock the (read-only) buffer of `arr` for the lifetime of `owner`.
+
+    Used for PointSet coordinates, which are frozen after construction: every
+    call still copies them to the device, but at DMA speed. Failure only means
+    pageable (slower) copies.
+    """
+    import weakref
+    if getattr(owner, "_ds_pinned", False) or arr.nbytes == 0:
+        return getattr(owner, "_ds_pinned", False)
+    lib = load_library()
+    if lib.ds_host_register(ctypes.c_void_p(arr.ctypes.data), arr.nbytes) != DS_OK:
+        return False
+    owner._ds_pinned = True
+    weakref.finalize(owner, lib.ds_host_unregister, ctypes.c_void_p(arr.ctypes.data))
+    return True
+
+
+def pinned_empty(n: int, dtype=np.int64) -> np.ndarray:
+    """Page-locked host array from torch's caching host allocator when available
+    (device->host copies into it run at DMA speed); plain numpy otherwise."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+            return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+    except Exception:
+        pass
+    return np.empty(n, dtype=dtype)
 
 
 _ctx_local = threading.local()

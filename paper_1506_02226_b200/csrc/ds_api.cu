@@ -185,35 +185,44 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   return DS_OK;
 }
 
-// Stage 1+2: prep + eps-tile kernel (+ capacity regrow). On return the words,
-// counts and scalars are valid on `s` (the stream has been synchronised once to
-// read the word count).
-ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq, int formula,
-                  int64_t mem_cap, cudaStream_t s, ds_timings* t, int rank = 0, int world = 1,
-                  int32_t* cnt_out = nullptr) {
+struct Plan {
+  int64_t T = 0, all_items = 0, item_lo = 0, item_hi = 0;
+  bool cull = false;
+  size_t base = 0;
+  int rank = 0, world = 1;
+};
+
+// Stage 1+2 enqueue (prep, spatial order, culling, eps-tile kernel). Nothing here
+// waits for the device: the adjacency-word buffer is sized from what earlier calls
+// needed, and an overflow (detected by check_words after the caller's single sync)
+// triggers one re-run with the exact size.
+ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
+                          int formula, int64_t mem_cap, cudaStream_t s, Plan& pl, int rank = 0,
+                          int world = 1) {
   ds_status st = alloc_common(c, n, d);
   if (st != DS_OK) return st;
-  const int64_t T = n_tiles(n);
-  const int64_t all_items = n_items(T);
   if (world < 1 || rank < 0 || rank >= world) {
     set_error("shard: rank must be in [0, world)");
     return DS_EINVAL;
   }
-  const bool cull = c->cull != 0 && T > 1;
+  pl.T = n_tiles(n);
+  pl.all_items = n_items(pl.T);
+  pl.cull = c->cull != 0 && pl.T > 1;
+  pl.rank = rank;
+  pl.world = world;
   // dense schedule: contiguous equal slice of the triangle; culled schedule: the
   // slice of the device-side kept list is taken inside the kernel
-  const int64_t item_lo = all_items * rank / world;
-  const int64_t item_hi = all_items * (rank + 1) / world;
-  const int64_t items = cull ? all_items : item_hi - item_lo;
-  int32_t* cnt = cnt_out ? cnt_out : (int32_t*)c->cnt.p;
-  const size_t base = base_bytes(n, d);
+  pl.item_lo = pl.all_items * rank / world;
+  pl.item_hi = pl.all_items * (rank + 1) / world;
+  pl.base = base_bytes(n, d);
+  const int64_t T = pl.T;
 
-  // first guess for the adjacency words: keep what earlier calls needed
-  unsigned long long want = std::max<unsigned long long>(c->words_cap, (unsigned long long)n * 8 + (1ull << 20));
+  unsigned long long want =
+      std::max<unsigned long long>(c->words_cap, (unsigned long long)n * 8 + (1ull << 20));
   if (mem_cap > 0) {
-    const int64_t room = mem_cap - (int64_t)base;
+    const int64_t room = mem_cap - (int64_t)pl.base;
     if (room < 16 * 1024) {
-      set_capacity((int64_t)base + 16 * 1024, mem_cap);
+      set_capacity((int64_t)pl.base + 16 * 1024, mem_cap);
       set_error("device workspace exceeds the memory cap");
       return DS_ECAPACITY;
     }
@@ -222,7 +231,8 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
   if (c->words.bytes < want * WORD_BYTES) DS_CK(ensure(c->words, want * WORD_BYTES));
   c->words_cap = c->words.bytes / WORD_BYTES;
   if (mem_cap > 0) {  // a buffer kept from an earlier, larger call must not bypass the cap
-    const unsigned long long room_words = (unsigned long long)((mem_cap - (int64_t)base) / WORD_BYTES);
+    const unsigned long long room_words =
+        (unsigned long long)((mem_cap - (int64_t)pl.base) / WORD_BYTES);
     c->words_cap = std::min(c->words_cap, room_words);
   }
 
@@ -230,6 +240,7 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
   const float eps32 = (float)eps_sq;  // float32(float64 eps^2), RN (kernels.py:355/385)
 
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
+  DS_CK(cudaMemsetAsync(c->cnt.p, 0, (size_t)n * 4, s));
   DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, s));
   const float* rec = (const float*)c->rec.p;
   c->sorted = false;
@@ -242,8 +253,7 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     DS_CK(ensure(c->keys_alt, N * 8));
     DS_CK(ensure(c->kidx, N * 4));
     DS_CK(ensure(c->bbox, 64));
-    const size_t tb = sort_temp_bytes(n);
-    DS_CK(ensure(c->sort_temp, tb));
+    DS_CK(ensure(c->sort_temp, sort_temp_bytes(n)));
     DS_CK(launch_spatial_sort(rec, n, d, (float*)c->rec_sorted.p, (int32_t*)c->perm.p,
                               (int32_t*)c->inv.p, (unsigned long long*)c->keys.p,
                               (unsigned long long*)c->keys_alt.p, (int32_t*)c->kidx.p,
@@ -251,111 +261,130 @@ ds_status stage12(ds_ctx* c, const double* d_coords, int64_t n, int d, double ep
     rec = (const float*)c->rec_sorted.p;
     c->sorted = true;
   }
-  if (cull) {
+  if (pl.cull) {
     const int dp = padded_dim(d);
     DS_CK(ensure(c->tbox, (size_t)T * (2 * dp + 1) * 4));
-    DS_CK(ensure(c->items, (size_t)all_items * 4));
-    DS_CK(ensure(c->iflags, (size_t)all_items * 4));
-    DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(all_items) * 4));
+    DS_CK(ensure(c->items, (size_t)pl.all_items * 4));
+    DS_CK(ensure(c->iflags, (size_t)pl.all_items * 4));
+    DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(pl.all_items) * 4));
     float* lo = (float*)c->tbox.p;
-    DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo,
-                      lo + (size_t)T * dp, lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p,
-                      (int32_t*)c->ipartials.p, &sc->kept32, (uint32_t*)c->items.p, &sc->kept,
-                      s));
+    DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo, lo + (size_t)T * dp,
+                      lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p,
+                      &sc->kept32, (uint32_t*)c->items.p, &sc->kept, s));
   }
-
-  int launches = 0;
-  for (;;) {
-    DS_CK(cudaMemsetAsync(cnt, 0, (size_t)n * 4, s));
-    DS_CK(cudaMemsetAsync(&sc->work_ctr, 0, 3 * sizeof(unsigned long long), s));
-    TileArgs a;
-    a.rec = rec;
-    a.n = n;
-    a.T = (int32_t)T;
-    a.d = d;
-    a.item_lo = item_lo;
-    a.item_hi = item_hi;
-    a.item_list = cull ? (const uint32_t*)c->items.p : nullptr;
-    a.item_count = &sc->kept;
-    a.shard_rank = rank;
-    a.shard_world = world;
-    a.work_ctr = &sc->work_ctr;
-    a.eps32 = eps32;
-    a.cnt = cnt;
-    a.words = (uint2*)c->words.p;
-    a.words_cap = c->words_cap;
-    a.words_count = &sc->words_count;
-    a.chunks = (uint4*)c->chunks.p;
-    a.chunks_cap = (unsigned long long)items;
-    a.nonempty_count = &sc->nonempty_count;
-    a.unsafe_flag = &sc->unsafe_flag;
-    DS_CK(cudaEventRecord(c->ev[1], s));
-    DS_CK(launch_tile(a, formula, c->sm_count, s));
-    DS_CK(cudaEventRecord(c->ev[2], s));
-    ++launches;
-    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-    DS_CK(cudaStreamSynchronize(s));
-    const unsigned long long need = c->h_scalars->words_count;
-    if (need <= c->words_cap) break;
-    // regrow to the exact requirement (+6%) and evaluate the tiles again
-    const unsigned long long grow = need + need / 16 + 1024;
-    const int64_t required = (int64_t)(base + grow * WORD_BYTES);
-    if (mem_cap > 0 && required > mem_cap) {
-      set_capacity((int64_t)(base + need * WORD_BYTES), mem_cap);
-      set_error("adjacency words exceed the memory cap");
-      return DS_ECAPACITY;
-    }
-    if (c->words.bytes < grow * WORD_BYTES) {
-      if (c->words.p) cudaFree(c->words.p);
-      c->words.p = nullptr;
-      c->words.bytes = 0;
-      DS_CK(ensure(c->words, grow * WORD_BYTES));
-    }
-    c->words_cap = grow;
-  }
-  if (t) {
-    t->tile_launches = launches;
-    int64_t evaluated = item_hi - item_lo;
-    if (cull) {
-      const int64_t kept = (int64_t)c->h_scalars->kept;
-      evaluated = kept * (rank + 1) / world - kept * rank / world;
-    }
-    t->tiles_total = evaluated;
-    t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;
-    t->words_emitted = (int64_t)c->h_scalars->words_count;
-    t->unsafe_range = c->h_scalars->unsafe_flag ? 1 : 0;
-    // every evaluated item is a full 512 x 512 pair block (ragged edges masked)
-    t->pairs_evaluated = evaluated * (int64_t)TILE * TILE;
-  }
+  TileArgs a;
+  a.rec = rec;
+  a.n = n;
+  a.T = (int32_t)T;
+  a.d = d;
+  a.item_lo = pl.item_lo;
+  a.item_hi = pl.item_hi;
+  a.item_list = pl.cull ? (const uint32_t*)c->items.p : nullptr;
+  a.item_count = &sc->kept;
+  a.shard_rank = rank;
+  a.shard_world = world;
+  a.work_ctr = &sc->work_ctr;
+  a.eps32 = eps32;
+  a.cnt = (int32_t*)c->cnt.p;
+  a.words = (uint2*)c->words.p;
+  a.words_cap = c->words_cap;
+  a.words_count = &sc->words_count;
+  a.chunks = (uint4*)c->chunks.p;
+  a.chunks_cap = (unsigned long long)pl.all_items;
+  a.nonempty_count = &sc->nonempty_count;
+  a.unsafe_flag = &sc->unsafe_flag;
+  DS_CK(cudaEventRecord(c->ev[1], s));
+  DS_CK(launch_tile(a, formula, c->sm_count, s));
+  DS_CK(cudaEventRecord(c->ev[2], s));
   return DS_OK;
 }
 
+// After the caller's sync (h_scalars copied): did the words overflow? If so grow the
+// buffer to the exact need (+6%) and ask for a re-run.
+ds_status check_words(ds_ctx* c, const Plan& pl, int64_t mem_cap, bool* retry) {
+  *retry = false;
+  const unsigned long long need = c->h_scalars->words_count;
+  if (need <= c->words_cap) return DS_OK;
+  const unsigned long long grow = need + need / 16 + 1024;
+  const int64_t required = (int64_t)(pl.base + grow * WORD_BYTES);
+  if (mem_cap > 0 && required > mem_cap) {
+    set_capacity((int64_t)(pl.base + need * WORD_BYTES), mem_cap);
+    set_error("adjacency words exceed the memory cap");
+    return DS_ECAPACITY;
+  }
+  if (c->words.bytes < grow * WORD_BYTES) {
+    if (c->words.p) cudaFree(c->words.p);
+    c->words.p = nullptr;
+    c->words.bytes = 0;
+    DS_CK(ensure(c->words, grow * WORD_BYTES));
+  }
+  c->words_cap = grow;
+  *retry = true;
+  return DS_OK;
+}
+
+void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* t) {
+  if (!t) return;
+  t->tile_launches = launches;
+  int64_t evaluated = pl.item_hi - pl.item_lo;
+  if (pl.cull) {
+    const int64_t kept = (int64_t)c->h_scalars->kept;
+    evaluated = kept * (pl.rank + 1) / pl.world - kept * pl.rank / pl.world;
+  }
+  t->tiles_total = evaluated;
+  t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;
+  t->words_emitted = (int64_t)c->h_scalars->words_count;
+  t->unsafe_range = c->h_scalars->unsafe_flag ? 1 : 0;
+  // every evaluated item is a full 512 x 512 pair block (ragged edges masked)
+  t->pairs_evaluated = evaluated * (int64_t)TILE * TILE;
+}
+
+// The whole pipeline, enqueued without host round trips; the optional host
+// copies of labels / counts are enqueued before the single final sync.
 ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                    int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
-                   int64_t* d_counts64, cudaStream_t s, ds_timings* t) {
-  DS_CK(cudaEventRecord(c->ev[0], s));
-  ds_status st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, t);
-  if (st != DS_OK) return st;
-  MergeWs w = merge_ws(c, n);
-  Scalars* sc = (Scalars*)c->scalars.p;
-  DS_CK(launch_core_init(w, min_pts, s));
-  DS_CK(cudaEventRecord(c->ev[3], s));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, (const uint4*)c->chunks.p,
-                            &sc->nonempty_count, s));
-  DS_CK(launch_finalize(w, d_labels, s));
-  if (d_counts64)
-    DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
-  DS_CK(cudaEventRecord(c->ev[4], s));
-  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-  DS_CK(cudaStreamSynchronize(s));
+                   int64_t* d_counts64, cudaStream_t s, ds_timings* t, int64_t* h_labels = nullptr,
+                   int64_t* h_counts = nullptr) {
+  Plan pl;
+  for (int attempt = 1;; ++attempt) {
+    DS_CK(cudaEventRecord(c->ev[0], s));
+    ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl);
+    if (st != DS_OK) return st;
+    MergeWs w = merge_ws(c, n);
+    Scalars* sc = (Scalars*)c->scalars.p;
+    DS_CK(launch_core_init(w, min_pts, s));
+    DS_CK(cudaEventRecord(c->ev[3], s));
+    DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+                              &sc->nonempty_count, s));
+    DS_CK(launch_finalize(w, d_labels, s));
+    if (d_counts64)
+      DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
+    DS_CK(cudaEventRecord(c->ev[4], s));
+    if (h_labels)
+      DS_CK(cudaMemcpyAsync(h_labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    if (h_counts && d_counts64)
+      DS_CK(cudaMemcpyAsync(h_counts, d_counts64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    DS_CK(cudaEventRecord(c->ev[7], s));
+    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                          s));
+    DS_CK(cudaStreamSynchronize(s));
+    bool retry = false;
+    st = check_words(c, pl, mem_cap, &retry);
+    if (st != DS_OK) return st;
+    if (retry && attempt < 3) continue;
+    stage12_timings(c, pl, attempt, t);
+    break;
+  }
   if (t) {
-    float f = 0, m = 0, k = 0;
+    float f = 0, m = 0, k = 0, o = 0;
     DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
     DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
     DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    DS_CK(cudaEventElapsedTime(&o, c->ev[4], c->ev[7]));
     t->fused_ms = f;
     t->merge_ms = m;
     t->tile_ms = k;
+    t->d2h_ms = o;
     t->core_count = (int64_t)c->h_scalars->ncore;
     t->cluster_count = c->h_scalars->nclusters;
     t->device_bytes = (int64_t)held_bytes(c);
@@ -465,21 +494,13 @@ ds_status ds_run_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, d
   cudaStream_t s = c->stream;
   DS_CK(cudaEventRecord(c->ev[5], s));
   DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
-  DS_CK(cudaEventRecord(c->ev[6], s));
   st = pipeline(c, (const double*)c->coords64.p, n, d, eps_sq, min_pts, formula, mem_cap,
-                (int64_t*)c->labels.p, counts_out ? (int64_t*)c->counts64.p : nullptr, s, &local);
+                (int64_t*)c->labels.p, counts_out ? (int64_t*)c->counts64.p : nullptr, s, &local,
+                labels_out, counts_out);
   if (st != DS_OK) return st;
-  DS_CK(cudaEventRecord(c->ev[6], s));
-  DS_CK(cudaMemcpyAsync(labels_out, c->labels.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-  if (counts_out)
-    DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-  DS_CK(cudaEventRecord(c->ev[7], s));
-  DS_CK(cudaStreamSynchronize(s));
-  float h2d = 0, d2h = 0;
+  float h2d = 0;
   DS_CK(cudaEventElapsedTime(&h2d, c->ev[5], c->ev[0]));
-  DS_CK(cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]));
   local.h2d_ms = h2d;
-  local.d2h_ms = d2h;
   local.total_ms = now_ms() - t0;
   if (t) *t = local;
   return DS_OK;
@@ -502,27 +523,38 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
   DS_CK(ensure(c->coords64, in_bytes));
   DS_CK(ensure(c->counts64, (size_t)n * 8));
   DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
-  DS_CK(cudaEventRecord(c->ev[0], s));
-  st = stage12(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, &local);
-  if (st != DS_OK) return st;
-  const int32_t* perm = c->sorted ? (const int32_t*)c->perm.p : nullptr;
-  DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, perm, (int64_t*)c->counts64.p, s));
-  DS_CK(cudaEventRecord(c->ev[3], s));
-  DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-  if (bits_out) {
-    const int64_t stride = (n + 31) / 32;  // words per row
-    const size_t dense = (size_t)n * stride * 4;
-    DS_CK(ensure(c->dense, dense));
-    DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
-    Scalars* sc = (Scalars*)c->scalars.p;
-    DS_CK(launch_export_bits((const uint2*)c->words.p, (const uint4*)c->chunks.p,
-                             &sc->nonempty_count, perm, (uint32_t*)c->dense.p, stride, s));
-    DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
-    const size_t row_bytes = (size_t)(n + 7) / 8;
-    DS_CK(cudaMemcpy2DAsync(bits_out, row_bytes, c->dense.p, stride * 4, row_bytes, (size_t)n,
-                            cudaMemcpyDeviceToHost, s));
+  Plan pl;
+  for (int attempt = 1;; ++attempt) {
+    DS_CK(cudaEventRecord(c->ev[0], s));
+    st = stage12_enqueue(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, pl);
+    if (st != DS_OK) return st;
+    const int32_t* perm = c->sorted ? (const int32_t*)c->perm.p : nullptr;
+    DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, perm, (int64_t*)c->counts64.p, s));
+    DS_CK(cudaEventRecord(c->ev[3], s));
+    DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    if (bits_out) {
+      const int64_t stride = (n + 31) / 32;  // words per row
+      const size_t dense = (size_t)n * stride * 4;
+      DS_CK(ensure(c->dense, dense));
+      DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
+      Scalars* sc = (Scalars*)c->scalars.p;
+      DS_CK(launch_export_bits((const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+                               &sc->nonempty_count, perm, (uint32_t*)c->dense.p, stride, s));
+      DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
+      const size_t row_bytes = (size_t)(n + 7) / 8;
+      DS_CK(cudaMemcpy2DAsync(bits_out, row_bytes, c->dense.p, stride * 4, row_bytes, (size_t)n,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                          s));
+    DS_CK(cudaStreamSynchronize(s));
+    bool retry = false;
+    st = check_words(c, pl, mem_cap, &retry);
+    if (st != DS_OK) return st;
+    if (retry && attempt < 3) continue;
+    stage12_timings(c, pl, attempt, &local);
+    break;
   }
-  DS_CK(cudaStreamSynchronize(s));
   if (valid_out)
     for (int64_t i = 0; i < n; ++i) valid_out[i] = counts_out[i] >= min_pts ? 1 : 0;
   float f = 0, k = 0;
@@ -559,6 +591,26 @@ int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   return -1;
 }
 
+ds_status ds_host_register(const void* ptr, size_t bytes) {
+  if (!ptr || !bytes) {
+    set_error("ptr/bytes: empty range");
+    return DS_EINVAL;
+  }
+  cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return DS_OK;
+  }
+  DS_CK(e);
+  return DS_OK;
+}
+
+ds_status ds_host_unregister(const void* ptr) {
+  cudaError_t e = cudaHostUnregister(const_cast<void*>(ptr));
+  if (e != cudaSuccess) cudaGetLastError();  // not registered / already gone: nothing to do
+  return DS_OK;
+}
+
 int64_t ds_tile_items(int64_t n) { return n < 1 ? 0 : n_items(n_tiles(n)); }
 
 int ds_tile_side(void) { return TILE; }
@@ -576,14 +628,25 @@ ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t
   const double t0 = now_ms();
   ds_timings local{};
   cudaStream_t s = (cudaStream_t)stream;
-  DS_CK(cudaEventRecord(c->ev[0], s));
-  st = stage12(c, d_coords, n, d, eps_sq, formula, mem_cap, s, &local, rank, world);
-  if (st != DS_OK) return st;
-  // partial counts leave in original point order (the internal order is spatial)
-  DS_CK(launch_permute_i32((const int32_t*)c->cnt.p, n,
-                           c->sorted ? (const int32_t*)c->perm.p : nullptr, 1, d_counts, s));
-  DS_CK(cudaEventRecord(c->ev[3], s));
-  DS_CK(cudaEventSynchronize(c->ev[3]));
+  Plan pl;
+  for (int attempt = 1;; ++attempt) {
+    DS_CK(cudaEventRecord(c->ev[0], s));
+    st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl, rank, world);
+    if (st != DS_OK) return st;
+    // partial counts leave in original point order (the internal order is spatial)
+    DS_CK(launch_permute_i32((const int32_t*)c->cnt.p, n,
+                             c->sorted ? (const int32_t*)c->perm.p : nullptr, 1, d_counts, s));
+    DS_CK(cudaEventRecord(c->ev[3], s));
+    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                          s));
+    DS_CK(cudaStreamSynchronize(s));
+    bool retry = false;
+    st = check_words(c, pl, mem_cap, &retry);
+    if (st != DS_OK) return st;
+    if (retry && attempt < 3) continue;
+    stage12_timings(c, pl, attempt, &local);
+    break;
+  }
   float f = 0, k = 0;
   DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
   DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
@@ -616,7 +679,7 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
   DS_CK(launch_core_init(w, min_pts, s));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, (const uint4*)c->chunks.p,
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(cudaMemcpyAsync(d_parent, c->parent.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   DS_CK(cudaMemcpyAsync(d_bmin, c->bmin.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));

@@ -97,15 +97,16 @@ struct MergeWs {
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
-cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint4* chunks,
-                                const unsigned long long* nchunks, cudaStream_t s);
+cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
+                                const uint4* chunks, const unsigned long long* nchunks,
+                                cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
                               cudaStream_t s);
-cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
+cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint4* chunks,
                                const unsigned long long* nchunks, const int32_t* perm,
                                uint32_t* bits32, int64_t stride_words, cudaStream_t s);
 cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* perm, int to_original,

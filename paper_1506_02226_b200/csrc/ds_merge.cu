@@ -195,8 +195,9 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
 __global__ void __launch_bounds__(512) union_diag_kernel(
     const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
-    const uint2* __restrict__ words, int64_t n, const uint32_t* __restrict__ corew,
-    int32_t* parent, int32_t* bmin, const int32_t* __restrict__ perm) {
+    const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
+    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
+    const int32_t* __restrict__ perm) {
   constexpr int THREADS = 512;
   constexpr int RB = TILE / (THREADS / WPR);  // rows per block: 16
   extern __shared__ uint32_t dsm[];
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
     const ChunkInfo ci = decode_chunk(chunks[c]);
     if (ci.a != ci.b) continue;  // uniform per CTA
+    if (ci.base + ci.count > words_cap) continue;  // overflowed run: the host re-runs
     const int base = ci.a * TILE;
     if (tid < WPR) {
       const int64_t gw = (int64_t)ci.a * WPR + tid;
@@ -374,8 +376,9 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) union_pair_kernel(
     const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
-    const uint2* __restrict__ words, int64_t n, const uint32_t* __restrict__ corew,
-    int32_t* parent, int32_t* bmin, const int32_t* __restrict__ perm) {
+    const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
+    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
+    const int32_t* __restrict__ perm) {
   __shared__ int la[2 * TILE];    // current ancestor of each point (-1: not core)
   __shared__ int lb[2 * TILE];    // border minima (original indices)
   __shared__ int hist[2 * TILE];  // ancestors that are local indices of the own tile
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(THREADS) union_pair_kernel(
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
     const ChunkInfo ci = decode_chunk(chunks[c]);
     if (ci.a == ci.b) continue;  // uniform per CTA
+    if (ci.base + ci.count > words_cap) continue;  // overflowed run: the host re-runs
     if (tid < 2 * WPR) {
       const int64_t gw = (int64_t)(tid < WPR ? ci.a : ci.b) * WPR + (tid & (WPR - 1));
       lcw[tid] = gw < nw ? corew[gw] : 0u;
@@ -651,13 +655,15 @@ __global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n,
 
 // chunks -> dense native-word rows in ORIGINAL index order, both orientations
 // (the chunks only hold a <= b)
-__global__ void export_bits_kernel(const uint2* __restrict__ words, const uint4* __restrict__ chunks,
+__global__ void export_bits_kernel(const uint2* __restrict__ words, unsigned long long words_cap,
+                                   const uint4* __restrict__ chunks,
                                    const unsigned long long* __restrict__ nchunks,
                                    const int32_t* __restrict__ perm, uint32_t* bits32,
                                    int64_t stride_words) {
   const unsigned long long total = *nchunks;
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
     const ChunkInfo ci = decode_chunk(chunks[c]);
+    if (ci.base + ci.count > words_cap) continue;
     for (int k = threadIdx.x; k < ci.count; k += blockDim.x) {
       const uint2 rec = words[ci.base + k];
       uint32_t x = rec.x;
@@ -710,8 +716,9 @@ cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) 
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint4* chunks,
-                                const unsigned long long* nchunks, cudaStream_t s) {
+cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
+                                const uint4* chunks, const unsigned long long* nchunks,
+                                cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -723,10 +730,10 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, const uint
                          (int)diag_smem);
     diag_cfg = true;
   }
-  union_diag_kernel<<<sms * 2, 512, diag_smem, s>>>(chunks, nchunks, words, w.n, w.corew,
-                                                    w.parent, w.bmin, w.perm);
-  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(chunks, nchunks, words, w.n, w.corew, w.parent,
-                                                 w.bmin, w.perm);
+  union_diag_kernel<<<sms * 2, 512, diag_smem, s>>>(chunks, nchunks, words, words_cap, w.n,
+                                                    w.corew, w.parent, w.bmin, w.perm);
+  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(chunks, nchunks, words, words_cap, w.n, w.corew,
+                                                 w.parent, w.bmin, w.perm);
   return cudaGetLastError();
 }
 
@@ -795,10 +802,11 @@ cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm
   return cudaGetLastError();
 }
 
-cudaError_t launch_export_bits(const uint2* words, const uint4* chunks,
+cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint4* chunks,
                                const unsigned long long* nchunks, const int32_t* perm,
                                uint32_t* bits32, int64_t stride_words, cudaStream_t s) {
-  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, chunks, nchunks, perm, bits32, stride_words);
+  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, words_cap, chunks, nchunks, perm, bits32,
+                                             stride_words);
   return cudaGetLastError();
 }
 

@@ -123,6 +123,7 @@ def run_dbscan(points: PointSet, params: DbscanParams, config: PipelineConfig):
         ensure_capacity(4 * points.n * points.n, mem_cap)
     ctx = _native.context(config.device)
     ctx.configure(config.prune, config.spatial_order)
+    _native.pin_frozen(points.coords_aos, points)
     labels, _, t = ctx.run_dbscan(points.coords_aos, params.eps_sq, params.min_pts,
                                   variant.formula, mem_cap)
     total = (time.perf_counter() - t0) * 1e3
