@@ -102,6 +102,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def tile_traffic(config: str):
+    """DRAM bytes per launch of the eps-tile kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_tile_traffic.json")) as fh:
+            t = json.load(fh)[config]
+        return t["dram_read_bytes"] + t["dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def algorithmic_ops_per_pair(d: int, formula: int) -> int:
     # SURVEY §8(d): ALGEBRAIC 2d+1, DIRECT 3d-1 separately rounded FP32 ops per pair
     return 2 * d + 1 if formula == 1 else 3 * d - 1
@@ -298,7 +308,8 @@ def run_b200(args):
                              if world == 1 else None)},
         "roofline": {"bound": "fp32", "kernel": "eps_tile_kernel", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "traffic": None,
+                     "frac": achieved / fp32_peak, "traffic": tile_traffic(args.config),
+                     "traffic_source": "dram__bytes_read+write per launch, profiles/r01_tile_traffic.json",
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz "
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
                      "ops_per_pair": ops, "pairs_per_launch": pairs,
