@@ -51,6 +51,7 @@ struct Scalars {
   unsigned long long nonempty_count;
   unsigned long long kept;  // tile pairs surviving the culling test
   unsigned long long ncore;
+  unsigned long long pairs_done;
   int32_t kept32;
   uint32_t unsafe_flag;
   int32_t nclusters;
@@ -65,7 +66,7 @@ struct ds_ctx {
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, bbox;
+      keys_alt, kidx, sort_temp, bbox, blk;
   int cull = 1;          // DS_OPT_TILE_CULL
   int sort = 1;          // DS_OPT_SPATIAL_SORT
   bool sorted = false;   // perm / inv describe the last stage 1+2
@@ -96,7 +97,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                      &c->sort_temp, &c->bbox};
+                      &c->sort_temp, &c->bbox, &c->blk};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -140,6 +141,7 @@ size_t base_bytes(int64_t n, int d) {
          + (size_t)n_items(n_tiles(n)) * (16 + 4 + 4)  // chunk table + item list + flags
          + (size_t)n_tiles(n) * (2 * padded_dim(d) + 1) * 4  // tile boxes
          + N * rec_stride(d) * 4 + N * (4 + 4 + 8 + 8 + 4)  // spatial order
+         + ((N + 31) / 32) * (2 * padded_dim(d) + 1) * 4      // 32-point block boxes
          + N * 4 * 6                // cnt parent bmin cmin root flag
          + N                        // core
          + ((N + 31) / 32) * 4      // corew
@@ -272,6 +274,11 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
                       lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p,
                       &sc->kept32, (uint32_t*)c->items.p, &sc->kept, s));
   }
+  const bool block_skip = pl.cull && padded_dim(d) <= 4;
+  if (block_skip) {
+    DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * padded_dim(d) + 1) * 4));
+    DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
+  }
   TileArgs a;
   a.rec = rec;
   a.n = n;
@@ -293,6 +300,8 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.chunks_cap = (unsigned long long)pl.all_items;
   a.nonempty_count = &sc->nonempty_count;
   a.unsafe_flag = &sc->unsafe_flag;
+  a.blk = block_skip ? (const float*)c->blk.p : nullptr;
+  a.pairs_done = &sc->pairs_done;
   DS_CK(cudaEventRecord(c->ev[1], s));
   DS_CK(launch_tile(a, formula, c->sm_count, s));
   DS_CK(cudaEventRecord(c->ev[2], s));
@@ -335,8 +344,8 @@ void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* 
   t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;
   t->words_emitted = (int64_t)c->h_scalars->words_count;
   t->unsafe_range = c->h_scalars->unsafe_flag ? 1 : 0;
-  // every evaluated item is a full 512 x 512 pair block (ragged edges masked)
-  t->pairs_evaluated = evaluated * (int64_t)TILE * TILE;
+  // pairs the tile kernel actually evaluated (skipped 32-column groups excluded)
+  t->pairs_evaluated = (int64_t)c->h_scalars->pairs_done;
 }
 
 // The whole pipeline, enqueued without host round trips; the optional host
@@ -446,7 +455,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                &c->sort_temp, &c->bbox};
+                &c->sort_temp, &c->bbox, &c->blk};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)

@@ -62,12 +62,16 @@ struct TileArgs {
   const uint32_t* item_list;           // culled items (a << 16 | b), or nullptr: dense triangle
   const unsigned long long* item_count; // length of item_list (device)
   int32_t shard_rank, shard_world;     // slice of item_list this launch evaluates
+  const float* blk;                    // 32-point block boxes (nullptr: no sub-tile culling)
+  unsigned long long* pairs_done;      // ordered pairs evaluated (32 x 32*KP per word group)
 };
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
                         cudaStream_t s);
 cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream_t s);
+// 32-point block boxes [block][lo(dpad), hi(dpad), maxnorm] for sub-tile culling
+cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s);
 // tile bounding boxes + list of tile pairs that are not provably empty
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,

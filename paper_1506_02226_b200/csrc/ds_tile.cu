@@ -298,6 +298,9 @@ eps_tile_kernel(const TileArgs args) {
   __shared__ long long item_sh[2];
   __shared__ unsigned int scan_sh[NTH / 32 + 1];
   __shared__ unsigned long long base_sh;
+  __shared__ uint8_t unit_active[(NTH / 32) * WPR];
+  __shared__ uint16_t unit_list[(NTH / 32) * WPR];
+  __shared__ int unit_count;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -356,50 +359,108 @@ eps_tile_kernel(const TileArgs args) {
     const int na = (int)min((int64_t)TILE, n - (int64_t)a * TILE);
     const int nb = (int)min((int64_t)TILE, n - (int64_t)b * TILE);
 
-    // ---- lane side: KP points per thread, in registers ------------------------
-    Lanes<D, KP> L;
-    bool lvalid[KP];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-      const int il = tid + NTH * k;
-      lvalid[k] = il < na;
-      const int64_t i = (int64_t)a * TILE + (lvalid[k] ? il : 0);
-      const float4* r4 = reinterpret_cast<const float4*>(args.rec + (size_t)i * S);
-      float tmp[S];
-#pragma unroll
-      for (int v = 0; v < S / 4; ++v) {
-        const float4 x = __ldg(r4 + v);
-        tmp[4 * v + 0] = x.x;
-        tmp[4 * v + 1] = x.y;
-        tmp[4 * v + 2] = x.z;
-        tmp[4 * v + 3] = x.w;
-      }
-      float c[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q)
-        c[q] = (F == DS_FORMULA_ALGEBRAIC) ? __fadd_rn(tmp[q], tmp[q]) : -tmp[q];
-#pragma unroll
-      for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
-      L.v1[k] = c[D - 1];
-      L.t[k] = tmp[D];
-    }
-
+    // ---- work units: (lane block of 32*KP points) x (32-column group) ------------
+    // LB = NTH/32 lane blocks x WPR column groups. A unit is inactive when its
+    // columns are past the ragged end or (SAFE, d <= 4, culling on) the union box
+    // of the lane block and the 32-point column block are provably out of range
+    // (the bound of keep_item, evaluated in float with a 1e-5 relative and a 4x
+    // rounding-error margin). Active units are split evenly across the warps, so
+    // a warp whose own points are far from tile b still does its share.
+    constexpr int LB = NTH / 32;
+    constexpr int NU = LB * WPR;
+    constexpr bool kBlockSkip = SAFE && D <= 4;
+    const bool block_skip = kBlockSkip && args.blk != nullptr;
     mbar_wait(&mbar[cur], (phase >> cur) & 1u);
     phase ^= (1u << cur);
     const float* bcb = bc + (size_t)cur * TILE * S;
-
-    // ---- all pairs of the tile: 16 words of 32 columns per lane point ---------
-    uint32_t lcnt[KP];
+    for (int u = tid; u < NU; u += NTH) {
+      const int lb = u / WPR, jw = u % WPR;
+      bool active = jw * 32 < nb && lb * 32 * KP < na;
+      if (kBlockSkip && block_skip && active) {
+        constexpr int BS = 2 * D + 1;
+        const float* cb = args.blk + (size_t)(b * (TILE / 32) + jw) * BS;
+        const float* lbb = args.blk + (size_t)(a * (TILE / 32) + lb * KP) * BS;
+        float L = 0.f, wn = 0.f;
 #pragma unroll
-    for (int k = 0; k < KP; ++k) lcnt[k] = 0;
-    uint32_t any = 0;
-    for (int jw = 0; jw < WPR; ++jw) {
-      const int m = nb - jw * 32;
-      if (m <= 0) {
+        for (int q = 0; q < D; ++q) {
+          float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < KP; ++k) bits[jw * BSTRIDE + tid + NTH * k] = 0u;
-        continue;
+          for (int k = 0; k < KP; ++k) {
+            lo = fminf(lo, __ldg(lbb + k * BS + q));
+            hi = fmaxf(hi, __ldg(lbb + k * BS + D + q));
+          }
+          const float g = fmaxf(0.f, fmaxf(__ldg(cb + q) - hi, lo - __ldg(cb + D + q)));
+          L += g * g;
+        }
+#pragma unroll
+        for (int k = 0; k < KP; ++k) wn = fmaxf(wn, __ldg(lbb + k * BS + 2 * D));
+        float bound = L * (1.0f - 1e-5f);
+        if (F == DS_FORMULA_ALGEBRAIC)
+          bound -= 4.0f * (2.0f * D + 3.0f) * 5.97e-8f * (wn + __ldg(cb + 2 * D)) * 1.01f;
+        active = !(bound > eps32);  // NaN keeps the unit
       }
+      unit_active[u] = active ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid < 32 && NU > 0) {
+      // compact the active units in (lane block, column group) order
+      int cnt_total = 0;
+      for (int u0 = 0; u0 < NU; u0 += 32) {
+        const bool act = (u0 + tid < NU) && unit_active[u0 + tid];
+        const uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (act) unit_list[cnt_total + __popc(bal & ((1u << tid) - 1u))] = (uint16_t)(u0 + tid);
+        cnt_total += __popc(bal);
+      }
+      if (tid == 0) unit_count = cnt_total;
+    }
+    __syncthreads();
+    const int nact = unit_count;
+    const int warp = tid >> 5;
+    // zero the rows of inactive units (their words are 0)
+    for (int u = warp; u < NU; u += LB) {
+      if (unit_active[u]) continue;
+      const int lb = u / WPR, jw = u % WPR;
+#pragma unroll
+      for (int k = 0; k < KP; ++k) bits[jw * BSTRIDE + k * NTH + lb * 32 + lane] = 0u;
+    }
+
+    uint32_t any = 0;
+    uint32_t groups = 0;
+    int cur_lb = -1;
+    Lanes<D, KP> L;
+    bool lvalid[KP];
+    const int u_lo = nact * warp / LB, u_hi = nact * (warp + 1) / LB;
+    for (int ui = u_lo; ui < u_hi; ++ui) {
+      const int u = unit_list[ui];
+      const int lb = u / WPR, jw = u % WPR;
+      if (lb != cur_lb) {  // (re)load the lane block's points into registers
+        cur_lb = lb;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int il = (lb * 32 + lane) * KP + k;  // 32*KP consecutive points per block
+          lvalid[k] = il < na;
+          const int64_t i = (int64_t)a * TILE + (lvalid[k] ? il : 0);
+          const float4* r4 = reinterpret_cast<const float4*>(args.rec + (size_t)i * S);
+          float tmp[S];
+#pragma unroll
+          for (int v = 0; v < S / 4; ++v) {
+            const float4 x = __ldg(r4 + v);
+            tmp[4 * v + 0] = x.x;
+            tmp[4 * v + 1] = x.y;
+            tmp[4 * v + 2] = x.z;
+            tmp[4 * v + 3] = x.w;
+          }
+          float c[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+            c[q] = (F == DS_FORMULA_ALGEBRAIC) ? __fadd_rn(tmp[q], tmp[q]) : -tmp[q];
+#pragma unroll
+          for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
+          L.v1[k] = c[D - 1];
+          L.t[k] = tmp[D];
+        }
+      }
+      ++groups;
       uint32_t acc[KP];
 #pragma unroll
       for (int k = 0; k < KP; ++k) acc[k] = 0;
@@ -419,43 +480,68 @@ eps_tile_kernel(const TileArgs args) {
         eval_d2<D, F, KP>(L, xj, xj[D], d2);
         pack_bits<KP, SAFE>(d2, eps32, jj, acc);
       }
-      const uint32_t vm = valid_mask(m);
+      const uint32_t vm = valid_mask(nb - jw * 32);
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         const uint32_t w = lvalid[k] ? ((k < KC ? acc[k] : ~acc[k]) & vm) : 0u;
-        bits[jw * BSTRIDE + tid + NTH * k] = w;
-        lcnt[k] += __popc(w);
+        bits[jw * BSTRIDE + k * NTH + lb * 32 + lane] = w;
         any |= w;
       }
     }
 
     // ---- epilogue --------------------------------------------------------------
+    if (lane == 0 && groups)  // pairs actually evaluated: groups x 32 columns x 32*KP lane points
+      atomicAdd(args.pairs_done, (unsigned long long)groups * 32ull * 32ull * KP);
     const int any_all = __syncthreads_or(any != 0);
+    if (any_all) {  // lane-side counts: popcount of each row's active words (slot k*NTH + tid)
 #pragma unroll
-    for (int k = 0; k < KP; ++k)
-      if (lcnt[k]) atomicAdd(&args.cnt[(int64_t)a * TILE + tid + NTH * k], (int)lcnt[k]);
+      for (int k = 0; k < KP; ++k) {
+        uint32_t cnt_k = 0;
+#pragma unroll
+        for (int jw = 0; jw < WPR; ++jw)
+          if (unit_active[warp * WPR + jw]) cnt_k += __popc(bits[jw * BSTRIDE + k * NTH + tid]);
+        if (cnt_k) atomicAdd(&args.cnt[(int64_t)a * TILE + tid * KP + k], (int)cnt_k);
+      }
+    }
 
     if (any_all) {
       const int w = tid / G::CHUNKS;   // word column handled by this thread
-      const int c = tid % G::CHUNKS;   // row chunk: rows c, c + CHUNKS, ...
+      const int c = tid % G::CHUNKS;   // row chunk: slots c, c + CHUNKS, ...
       const uint32_t* col = bits + w * BSTRIDE + c;
+      // slots c + CHUNKS*r for r in [r0, r0 + SEG) all belong to one lane block, so
+      // an inactive (lane block, w) unit skips SEG rows at once
+      constexpr int SEG = 32 / G::CHUNKS;
 
-      if (a != b) {
-        // broadcast-side counts: vertical popcount of word column w over all lane rows
-        uint32_t s[10];
+      // pass 1: staged-side counts (vertical popcount of word column w) and the
+      // number of words to append (upper triangle only on the diagonal tile)
+      uint32_t s[10];
 #pragma unroll
-        for (int l = 0; l < 10; ++l) s[l] = 0;
-        for (int r = 0; r < G::ROWS; ++r) {
-          uint32_t carry = col[r * G::CHUNKS];
-          if (carry) {
+      for (int l = 0; l < 10; ++l) s[l] = 0;
+      uint32_t nz = 0;
+      for (int r0 = 0; r0 < G::ROWS; r0 += SEG) {
+        const int lb0 = ((c + r0 * G::CHUNKS) % NTH) / 32;
+        if (!unit_active[lb0 * WPR + w]) continue;
+#pragma unroll
+        for (int r = r0; r < r0 + SEG; ++r) {
+          uint32_t x = col[r * G::CHUNKS];
+          if (!x) continue;
+          if (a != b) {
+            uint32_t carry = x;
 #pragma unroll
             for (int l = 0; l < G::SL0; ++l) {
               const uint32_t t2 = s[l] & carry;
               s[l] ^= carry;
               carry = t2;
             }
+          } else {
+            const int p = c + r * G::CHUNKS;  // smem slot -> point (slot k*NTH + t holds t*KP + k)
+            const int il = (p % NTH) * KP + p / NTH;
+            x &= diag_keep(il - w * 32);      // keep columns t >= row
           }
+          nz += (x != 0);
         }
+      }
+      if (a != b) {
 #pragma unroll
         for (int off = 1; off < G::CHUNKS; off <<= 1) {
           uint32_t o[10];
@@ -474,17 +560,6 @@ eps_tile_kernel(const TileArgs args) {
         }
       }
 
-      // append the non-zero words (upper triangle only on the diagonal tile)
-      uint32_t nz = 0;
-      for (int r = 0; r < G::ROWS; ++r) {
-        uint32_t x = col[r * G::CHUNKS];
-        if (a == b) {
-          const int il = c + r * G::CHUNKS;
-          const int rel = il - w * 32;  // keep columns t >= rel
-          x &= diag_keep(rel);
-        }
-        nz += (x != 0);
-      }
       uint32_t incl = nz;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -510,18 +585,23 @@ eps_tile_kernel(const TileArgs args) {
         }
       }
       __syncthreads();
+      // pass 2: append the words
       unsigned long long pos = base_sh + scan_sh[tid >> 5] + (incl - nz);
       if (nz) {
-        for (int r = 0; r < G::ROWS; ++r) {
-          uint32_t x = col[r * G::CHUNKS];
-          const int il = c + r * G::CHUNKS;
-          if (a == b) {
-            const int rel = il - w * 32;
-            x &= diag_keep(rel);
-          }
-          if (x) {
-            if (pos < args.words_cap) args.words[pos] = make_uint2(x, (uint32_t)(il << 4 | w));
-            ++pos;
+        for (int r0 = 0; r0 < G::ROWS; r0 += SEG) {
+          const int lb0 = ((c + r0 * G::CHUNKS) % NTH) / 32;
+          if (!unit_active[lb0 * WPR + w]) continue;
+#pragma unroll
+          for (int r = r0; r < r0 + SEG; ++r) {
+            uint32_t x = col[r * G::CHUNKS];
+            if (!x) continue;
+            const int p = c + r * G::CHUNKS;
+            const int il = (p % NTH) * KP + p / NTH;
+            if (a == b) x &= diag_keep(il - w * 32);
+            if (x) {
+              if (pos < args.words_cap) args.words[pos] = make_uint2(x, (uint32_t)(il << 4 | w));
+              ++pos;
+            }
           }
         }
       }
@@ -597,6 +677,35 @@ __global__ void tile_bounds_kernel(const float* __restrict__ rec, int64_t n, int
       }
     }
     __syncthreads();
+  }
+}
+
+// Per 32-point block (one warp each): box and max squared norm, in the layout
+// blk[block][lo 0..dpad-1, hi 0..dpad-1, maxnorm] the tile kernel reads.
+__global__ void block_bounds_kernel(const float* __restrict__ rec, int64_t n, int dpad, int S,
+                                   float* __restrict__ blk) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk = (n + 31) / 32;
+  if (warp >= nblk) return;
+  const int64_t i = warp * 32 + lane;
+  const bool valid = i < n;
+  float* out = blk + warp * (2 * dpad + 1);
+  for (int k = 0; k <= dpad; ++k) {
+    const float v = valid ? rec[i * S + k] : 0.f;
+    float mn = valid ? v : INFINITY, mx = valid ? v : -INFINITY;
+    for (int off = 16; off; off >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    if (lane == 0) {
+      if (k < dpad) {
+        out[k] = mn;
+        out[dpad + k] = mx;
+      } else {
+        out[2 * dpad] = mx;
+      }
+    }
   }
 }
 
@@ -752,6 +861,14 @@ cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int for
   if (e != cudaSuccess) return e;
   cull_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(lo, hi, maxnorm, dp, T, eps32, formula,
                                                        unsafe_flag, flags, total_kept, list, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s) {
+  const int dp = pad_dim(d);
+  const int S = ((dp + 1) + 3) / 4 * 4;
+  const int64_t warps = (n + 31) / 32;
+  block_bounds_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(rec, n, dp, S, blk);
   return cudaGetLastError();
 }
 

@@ -323,3 +323,39 @@ def test_schedules_shuffled_input(ds, oracle, rng, prune, order):
             np.sqrt(0.03), 6), ds.KernelVariant(ds.VariantId.FUSED_ALGEBRAIC))
         obits, _ = oracle.neighborhood(coords, np.sqrt(0.03) ** 2, 1)
         assert np.array_equal(nbr.bits, obits)
+
+
+def test_full_size_configs_schedule_invariance(ds):
+    """C3 (1M) and C5 (2M, chain + dense blobs): the default schedule (spatial
+    order + culling + sub-tile skipping) equals the paper's dense schedule, and
+    repeated runs are identical. (Oracle parity at C3/C4 full size is recorded in
+    DESIGN.md §5 from tools/run_configs.py: the C oracle needs minutes.)"""
+    for name in ("C3", "C5"):
+        cfg = ds.CONFIGS[name]
+        pts = cfg.points()
+        params = ds.validate_params(cfg.eps, cfg.min_pts)
+        fast = ds.default_config()
+        fast.mem_cap = 64 * 1024**3
+        a, ta = ds.run_dbscan(pts, params, fast)
+        b, _ = ds.run_dbscan(pts, params, fast)
+        assert np.array_equal(a.labels, b.labels)
+        dense = ds.default_config()
+        dense.mem_cap = 64 * 1024**3
+        dense.prune = False
+        dense.spatial_order = False
+        c, tc = ds.run_dbscan(pts, params, dense)
+        assert np.array_equal(a.labels, c.labels), name
+        assert ta.pairs_evaluated < 0.05 * tc.pairs_evaluated
+
+
+def test_c4_shape_against_oracle(ds):
+    """16-D blobs (C4's generator at 60k points): parity with the C oracle."""
+    from oracle import c_oracle
+    pts = ds.generate_blobs(60_000, 8, 0.5, 0.0, 4, 16)
+    params = ds.validate_params(1.6, 8)
+    labeling, _ = ds.run_dbscan(pts, params, ds.default_config())
+    want, wc = c_oracle.dbscan(pts.coords_aos, params.eps_sq, 8, 1)
+    assert np.array_equal(labeling.labels, want)
+    ctx = ds._native.context()
+    _, counts, _ = ctx.run_dbscan(pts.coords_aos, params.eps_sq, 8, 1, 0, want_counts=True)
+    assert np.array_equal(counts, wc)
