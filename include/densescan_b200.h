@@ -100,8 +100,10 @@ void ds_ctx_destroy(ds_ctx* ctx);
  * results are bit-identical with 0 (the paper's dense schedule).
  * DS_OPT_SPATIAL_SORT (default 1): visit points in Morton order of their
  * coordinates so tiles are compact (more tile pairs culled); index-dependent
- * rules still use original indices, results are bit-identical with 0. */
-enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2 };
+ * rules still use original indices, results are bit-identical with 0.
+ * DS_OPT_CUDA_GRAPH (default 1): record the device pipeline into a CUDA graph
+ * on the second call with an identical shape/buffers/options and replay it. */
+enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3 };
 ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
 int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
 

@@ -20,7 +20,7 @@ LIB_NAME = "libdensescan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
-DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT = 1, 2
+DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT, DS_OPT_CUDA_GRAPH = 1, 2, 3
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
@@ -183,6 +183,11 @@ class Context:
     def set_spatial_sort(self, on: bool) -> None:
         """Visit points in Morton order (compact tiles; exact, default on)."""
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_SPATIAL_SORT, 1 if on else 0),
+                  self.lib)
+
+    def set_cuda_graph(self, on: bool) -> None:
+        """Record the device pipeline into a CUDA graph and replay it (default on)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_CUDA_GRAPH, 1 if on else 0),
                   self.lib)
 
     def configure(self, prune: bool = True, spatial_order: bool = True) -> None:

@@ -68,6 +68,12 @@ struct ds_ctx {
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
       keys_alt, kidx, sort_temp, bbox, blk;
   int cull = 1;          // DS_OPT_TILE_CULL
+  int use_graph = 1;     // DS_OPT_CUDA_GRAPH
+  // CUDA graph of the device pipeline, replayed while the key matches
+  cudaGraphExec_t gexec = nullptr;
+  unsigned long long gkey[12] = {};
+  unsigned long long seen_key[12] = {};
+  bool capturing = false;  // events become external graph nodes while recording
   int sort = 1;          // DS_OPT_SPATIAL_SORT
   bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
@@ -76,9 +82,12 @@ struct ds_ctx {
 
 namespace {
 
+static unsigned long long g_alloc_generation = 0;  // bumped whenever a buffer moves
+
 cudaError_t ensure(Buf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return cudaSuccess;
+  ++g_alloc_generation;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.bytes = 0;
@@ -185,6 +194,11 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->scalars, sizeof(Scalars)));
   DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));
   return DS_OK;
+}
+
+cudaError_t record(ds_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  return c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                      : cudaEventRecord(e, s);
 }
 
 struct Plan {
@@ -302,9 +316,9 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.unsafe_flag = &sc->unsafe_flag;
   a.blk = block_skip ? (const float*)c->blk.p : nullptr;
   a.pairs_done = &sc->pairs_done;
-  DS_CK(cudaEventRecord(c->ev[1], s));
+  DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_tile(a, formula, c->sm_count, s));
-  DS_CK(cudaEventRecord(c->ev[2], s));
+  DS_CK(record(c, c->ev[2], s));
   return DS_OK;
 }
 
@@ -348,27 +362,108 @@ void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* 
   t->pairs_evaluated = (int64_t)c->h_scalars->pairs_done;
 }
 
+// Device part of the pipeline: stage 1+2, core flags, merge, labels (+ counts).
+ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
+                         int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
+                         int64_t* d_counts64, cudaStream_t s, Plan& pl, bool captured) {
+  c->capturing = captured;
+  auto rec = [&](cudaEvent_t e) { return record(c, e, s); };
+  DS_CK(rec(c->ev[0]));
+  ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl);
+  if (st != DS_OK) return st;
+  MergeWs w = merge_ws(c, n);
+  Scalars* sc = (Scalars*)c->scalars.p;
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(rec(c->ev[3]));
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+                            &sc->nonempty_count, s));
+  DS_CK(launch_finalize(w, d_labels, s));
+  if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
+  DS_CK(rec(c->ev[4]));
+  c->capturing = false;
+  return DS_OK;
+}
+
 // The whole pipeline, enqueued without host round trips; the optional host
-// copies of labels / counts are enqueued before the single final sync.
+// copies of labels / counts are enqueued before the single final sync. The
+// device part is recorded into a CUDA graph on the second call with the same
+// shape, buffers and options, and replayed from then on (no per-kernel launch
+// cost); an adjacency-word overflow invalidates the graph.
 ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                    int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
                    int64_t* d_counts64, cudaStream_t s, ds_timings* t, int64_t* h_labels = nullptr,
                    int64_t* h_counts = nullptr) {
   Plan pl;
   for (int attempt = 1;; ++attempt) {
-    DS_CK(cudaEventRecord(c->ev[0], s));
-    ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl);
-    if (st != DS_OK) return st;
-    MergeWs w = merge_ws(c, n);
-    Scalars* sc = (Scalars*)c->scalars.p;
-    DS_CK(launch_core_init(w, min_pts, s));
-    DS_CK(cudaEventRecord(c->ev[3], s));
-    DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
-                              &sc->nonempty_count, s));
-    DS_CK(launch_finalize(w, d_labels, s));
-    if (d_counts64)
-      DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
-    DS_CK(cudaEventRecord(c->ev[4], s));
+    unsigned long long key[12];
+    uint64_t eps_bits;
+    std::memcpy(&eps_bits, &eps_sq, 8);
+    key[0] = (unsigned long long)n;
+    key[1] = (unsigned long long)d | ((unsigned long long)formula << 8) |
+             ((unsigned long long)c->cull << 16) | ((unsigned long long)c->sort << 17) | 1ull << 40;
+    key[2] = eps_bits;
+    key[3] = (unsigned long long)min_pts;
+    key[4] = (unsigned long long)(uintptr_t)d_coords;
+    key[5] = (unsigned long long)(uintptr_t)d_labels;
+    key[6] = (unsigned long long)(uintptr_t)d_counts64;
+    key[7] = c->words_cap;
+    key[8] = g_alloc_generation;
+    key[9] = (unsigned long long)mem_cap;
+    key[10] = (unsigned long long)c->device;
+    key[11] = 0;
+    const bool graph_hit = c->use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
+    if (graph_hit) {
+      DS_CK(cudaGraphLaunch(c->gexec, s));
+      // plan fields the timings need (no device work)
+      pl.T = n_tiles(n);
+      pl.all_items = n_items(pl.T);
+      pl.cull = c->cull != 0 && pl.T > 1;
+      pl.item_lo = 0;
+      pl.item_hi = pl.all_items;
+      pl.base = base_bytes(n, d);
+    } else if (c->use_graph && std::memcmp(key, c->seen_key, sizeof key) == 0) {
+      // second call with this key: record the device pipeline and replay it
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      const unsigned long long gen0 = g_alloc_generation;
+      // the legacy default stream cannot be captured: record on the context's own
+      // stream (nothing executes while recording) and launch on the caller's
+      cudaStream_t cap = (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread)
+                             ? c->stream
+                             : s;
+      DS_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      ds_status st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap,
+                                    d_labels, d_counts64, cap, pl, true);
+      c->capturing = false;
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+      if (st != DS_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      DS_CK(ce);
+      if (gen0 != g_alloc_generation) {  // a buffer moved while recording: run eagerly
+        cudaGraphDestroy(graph);
+        st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap, d_labels,
+                            d_counts64, s, pl, false);
+        if (st != DS_OK) return st;
+      } else {
+        DS_CK(cudaGraphInstantiate(&c->gexec, graph, 0));
+        cudaGraphDestroy(graph);
+        std::memcpy(c->gkey, key, sizeof key);
+        DS_CK(cudaGraphLaunch(c->gexec, s));
+      }
+    } else {
+      ds_status st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap,
+                                    d_labels, d_counts64, s, pl, false);
+      if (st != DS_OK) return st;
+      // key after this call's allocations: the next identical call records the graph
+      key[7] = c->words_cap;
+      key[8] = g_alloc_generation;
+      std::memcpy(c->seen_key, key, sizeof key);
+    }
     if (h_labels)
       DS_CK(cudaMemcpyAsync(h_labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
     if (h_counts && d_counts64)
@@ -378,9 +473,15 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
                           s));
     DS_CK(cudaStreamSynchronize(s));
     bool retry = false;
-    st = check_words(c, pl, mem_cap, &retry);
+    ds_status st = check_words(c, pl, mem_cap, &retry);
     if (st != DS_OK) return st;
-    if (retry && attempt < 3) continue;
+    if (retry) {
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      if (attempt < 3) continue;
+    }
     stage12_timings(c, pl, attempt, t);
     break;
   }
@@ -462,6 +563,7 @@ void ds_ctx_destroy(ds_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->h_scalars) cudaFreeHost(c->h_scalars);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
   delete c;
 }
 
@@ -590,6 +692,10 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
     c->sort = value ? 1 : 0;
     return DS_OK;
   }
+  if (option == DS_OPT_CUDA_GRAPH) {
+    c->use_graph = value ? 1 : 0;
+    return DS_OK;
+  }
   set_error("option: unknown option id");
   return DS_EINVAL;
 }
@@ -597,6 +703,7 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
 int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   if (c && option == DS_OPT_TILE_CULL) return c->cull;
   if (c && option == DS_OPT_SPATIAL_SORT) return c->sort;
+  if (c && option == DS_OPT_CUDA_GRAPH) return c->use_graph;
   return -1;
 }
 

@@ -359,3 +359,21 @@ def test_c4_shape_against_oracle(ds):
     ctx = ds._native.context()
     _, counts, _ = ctx.run_dbscan(pts.coords_aos, params.eps_sq, 8, 1, 0, want_counts=True)
     assert np.array_equal(counts, wc)
+
+
+def test_graph_replay_with_new_data(ds, oracle):
+    """Call 1 runs eagerly, call 2 records the CUDA graph, later calls replay it:
+    replays on different data of the same shape must still be exact, and a
+    word-buffer overflow on a denser input must fall back and stay exact."""
+    ctx = ds._native.context()
+    params = ds.validate_params(0.2, 5)
+    sets = [ds.generate_blobs(6000, 5, 0.3, 0.1, s, 2).coords_aos for s in (1, 1, 2, 3)]
+    sets.append(ds.generate_blobs(6000, 1, 0.05, 0.0, 4, 2).coords_aos)  # far denser
+    for coords in sets + sets[:2]:
+        labels, counts, t = ctx.run_dbscan(coords, params.eps_sq, 5, 1, 0, want_counts=True)
+        want, wc = oracle.dbscan(coords, params.eps_sq, 5, 1)
+        assert np.array_equal(counts, wc) and np.array_equal(labels, want)
+    ctx.set_cuda_graph(False)
+    labels, _, _ = ctx.run_dbscan(sets[2], params.eps_sq, 5, 1, 0)
+    ctx.set_cuda_graph(True)
+    assert np.array_equal(labels, oracle.dbscan(sets[2], params.eps_sq, 5, 1)[0])
