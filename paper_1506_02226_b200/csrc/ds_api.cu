@@ -66,7 +66,7 @@ struct ds_ctx {
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, bbox, blk;
+      keys_alt, kidx, sort_temp, bbox, blk, diag;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -106,7 +106,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                      &c->sort_temp, &c->bbox, &c->blk};
+                      &c->sort_temp, &c->bbox, &c->blk, &c->diag};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -172,6 +172,7 @@ MergeWs merge_ws(ds_ctx* c, int64_t n) {
   w.partials = (int32_t*)c->partials.p;
   w.nclusters = &sc->nclusters;
   w.ncore = &sc->ncore;
+  w.diag_idx = (int32_t*)c->diag.p;
   if (c->sorted) {
     w.perm = (const int32_t*)c->perm.p;
     w.inv = (const int32_t*)c->inv.p;
@@ -193,6 +194,7 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->partials, (size_t)scan_partials_len(n) * 4));
   DS_CK(ensure(c->scalars, sizeof(Scalars)));
   DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));
+  DS_CK(ensure(c->diag, (size_t)n_tiles(n) * 4));
   return DS_OK;
 }
 
@@ -556,7 +558,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                &c->sort_temp, &c->bbox, &c->blk};
+                &c->sort_temp, &c->bbox, &c->blk, &c->diag};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)

@@ -96,6 +96,7 @@ struct MergeWs {
   int32_t* partials;      // scan block partials
   int32_t* nclusters;     // device scalar
   unsigned long long* ncore;
+  int32_t* diag_idx = nullptr;    // chunk index of each diagonal tile pair (-1: none)
   const int32_t* perm = nullptr;  // sorted -> original index (nullptr: identity)
   const int32_t* inv = nullptr;   // original -> sorted index
 };

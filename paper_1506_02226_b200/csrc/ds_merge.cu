@@ -193,8 +193,19 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 }
 
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
+__global__ void diag_index_kernel(const uint4* __restrict__ chunks,
+                                  const unsigned long long* __restrict__ nchunks,
+                                  int32_t* __restrict__ diag_idx) {
+  const unsigned long long total = *nchunks;
+  for (unsigned long long c = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; c < total;
+       c += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 ch = chunks[c];
+    if (ch.x == ch.y) diag_idx[ch.x] = (int32_t)c;
+  }
+}
+
 __global__ void __launch_bounds__(512) union_diag_kernel(
-    const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
+    const uint4* __restrict__ chunks, const int32_t* __restrict__ diag_idx, int64_t ntiles,
     const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
     const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
@@ -212,11 +223,11 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   __shared__ int ntrees_sh;
   const int tid = threadIdx.x;
   const int w = tid % WPR, cblk = tid / WPR;
-  const unsigned long long total = *nchunks;
   const int64_t nw = (n + 31) / 32;
-  for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int c = diag_idx[tile];
+    if (c < 0) continue;  // uniform per CTA
     const ChunkInfo ci = decode_chunk(chunks[c]);
-    if (ci.a != ci.b) continue;  // uniform per CTA
     if (ci.base + ci.count > words_cap) continue;  // overflowed run: the host re-runs
     const int base = ci.a * TILE;
     if (tid < WPR) {
@@ -439,11 +450,9 @@ __global__ void __launch_bounds__(THREADS) union_pair_kernel(
     }
     __syncthreads();
     const int gb = dom[1];
-    for (int ww = tid; ww < WPR; ww += THREADS) {
-      uint32_t m = 0;
-      for (int t = 0; t < 32; ++t)
-        if (gb >= 0 && la[TILE + ww * 32 + t] == gb) m |= 0x80000000u >> t;
-      mb[ww] = m;
+    for (int ww = tid >> 5; ww < WPR; ww += THREADS / 32) {  // one ballot per word
+      const uint32_t bal = __ballot_sync(0xffffffffu, gb >= 0 && la[TILE + ww * 32 + (tid & 31)] == gb);
+      if ((tid & 31) == 0) mb[ww] = __brev(bal);
     }
     __syncthreads();
     const int ga = dom[0];
@@ -730,8 +739,15 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned l
                          (int)diag_smem);
     diag_cfg = true;
   }
-  union_diag_kernel<<<sms * 2, 512, diag_smem, s>>>(chunks, nchunks, words, words_cap, w.n,
-                                                    w.corew, w.parent, w.bmin, w.perm);
+  const int64_t ntiles = (w.n + TILE - 1) / TILE;
+  cudaError_t e = cudaMemsetAsync(w.diag_idx, 0xff, (size_t)ntiles * 4, s);
+  if (e != cudaSuccess) return e;
+  diag_index_kernel<<<sms, 256, 0, s>>>(chunks, nchunks, w.diag_idx);
+  // one CTA per tile (one wave: up to 4 resident per SM)
+  const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
+  union_diag_kernel<<<(unsigned)grid, 512, diag_smem, s>>>(chunks, w.diag_idx, ntiles, words,
+                                                          words_cap, w.n, w.corew, w.parent,
+                                                          w.bmin, w.perm);
   union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(chunks, nchunks, words, words_cap, w.n, w.corew,
                                                  w.parent, w.bmin, w.perm);
   return cudaGetLastError();

@@ -9,9 +9,9 @@
 // merge.py:116-130, and first-appearance numbering, core.py:116-132) is applied
 // to ORIGINAL indices through perm / inv (ds_merge.cu).
 //
-// Keys: up to 4 leading dimensions quantised to a 2^(24/k)-per-dimension grid
-// over the global bounding box (24-bit keys: three radix passes; 4096 cells per
-// dimension in 2-D is far finer than a 512-point tile). The sort is CUB's stable LSD radix sort on
+// Keys: up to 4 leading dimensions quantised to a 2^(b/k)-per-dimension grid over
+// the global bounding box, b = 16 bits (two radix passes) for 1-2-D inputs up to
+// 2^20 points and 24 bits otherwise — far finer than a 512-point tile. The sort is CUB's stable LSD radix sort on
 // (key, original index), so the permutation is deterministic and identical on
 // every rank.
 #include <cuda_runtime.h>
@@ -24,7 +24,9 @@
 namespace ds {
 namespace {
 
-constexpr int KEY_BITS = 24;
+// total key bits: 16 (two radix passes, a 256 x 256 grid) for 1-2-D inputs up to
+// 2^20 points, 24 (three passes) otherwise
+inline int key_bits(int64_t n, int kd) { return (kd <= 2 && n <= (1 << 20)) ? 16 : 24; }
 
 __device__ __forceinline__ unsigned int ord_bits(float f) {
   const unsigned int u = __float_as_uint(f);
@@ -67,13 +69,13 @@ __device__ __forceinline__ float unord(unsigned int u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-__global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, int kd,
+__global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits,
                               const unsigned int* __restrict__ lo_bits,
                               const unsigned int* __restrict__ hi_bits,
                               unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int bits = KEY_BITS / kd;
+  const int bits = total_bits / kd;
   const double levels = (double)((1ull << bits) - 1);
   uint32_t q[4] = {0, 0, 0, 0};
   for (int k = 0; k < kd; ++k) {
@@ -126,9 +128,10 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   (void)dp;
   bbox_kernel<<<148, 512, 0, s>>>(rec, n, S, kd, bbox, bbox + 4);
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, bbox, bbox + 4, keys, idx);
+  const int kb = key_bits(n, kd);
+  morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, kb, bbox, bbox + 4, keys, idx);
   e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, idx, perm, (int)n, 0,
-                                      KEY_BITS, s);
+                                      (kb / kd) * kd, s);
   if (e != cudaSuccess) return e;
   permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted, inv);
   return cudaGetLastError();
