@@ -53,28 +53,52 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 2 ms) during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    Falls back to `nvidia-smi` queries when NVML is unavailable.
+    """
 
-    def __init__(self, index: int = 0, period_ms: int = 50):
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap",
+    }
+
+    def __init__(self, index: int = 0, period_ms: float = 2.0):
         self.index = index
         self.period = period_ms / 1000.0
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            try:
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            return float(sm), float(mx), int(rs)
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5)
+        sm, mx, act = [p.strip() for p in out.stdout.strip().split(",")]
+        return float(sm), float(mx), int(act, 16)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in out.stdout.strip().split(",")]
-                if len(parts) >= 8:
-                    self.samples.append(parts)
+                self.samples.append(self._sample())
             except Exception:
                 pass
             self._stop.wait(self.period)
@@ -92,14 +116,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if s[4 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        reasons = sorted({name for _, _, bits in self.samples
+                          for bit, name in self.REASONS.items() if bits & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def tile_traffic(config: str):
@@ -269,6 +291,19 @@ def run_b200(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e = float(tt.item())
 
+    # the paper's dense all-pairs schedule on the same input (stage 1+2 only): the
+    # eps-tile kernel at full occupancy of work, for the FP32 roofline comparison
+    dense = None
+    if world == 1:
+        ctx.configure(False, False)
+        dts = []
+        for _ in range(3):
+            _, _, _, dt = ctx.fused_build(pts.coords_aos, params.eps_sq, params.min_pts, formula,
+                                          mem_cap, want_bits=False)
+            dts.append(dt)
+        ctx.configure(True, True)
+        dense = {"tile_ms": statistics.mean(t.tile_ms for t in dts[1:]),
+                 "pairs_per_launch": dts[-1].pairs_evaluated}
     peaks = load_peaks()
     clocks = clk.summary()
     sm_max = peaks.get("sm_max_mhz", 1965.0)
@@ -314,6 +349,12 @@ def run_b200(args):
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
                      "ops_per_pair": ops, "pairs_per_launch": pairs,
                      "tile_ms": statistics.mean(tile_ms)},
+        "dense_schedule": (None if dense is None else {
+            "what": "prune=False, spatial_order=False: all 512x512 upper-triangle tile pairs",
+            "tile_ms": dense["tile_ms"], "pairs_per_launch": dense["pairs_per_launch"],
+            "achieved": dense["pairs_per_launch"] * ops / (dense["tile_ms"] / 1e3) / 1e12,
+            "frac": dense["pairs_per_launch"] * ops / (dense["tile_ms"] / 1e3) / 1e12 / fp32_peak,
+            "gpair_evals_per_s": dense["pairs_per_launch"] / (dense["tile_ms"] / 1e3) / 1e9}),
         "gpair_evals_per_s": pairs / tile_s / 1e9,
         "n2_decisions_per_s": (n * n if world == 1 else n * n / world) / tile_s / 1e9,
         "stages_ms": last[2],
