@@ -52,9 +52,11 @@ struct Scalars {
   unsigned long long kept;  // tile pairs surviving the culling test
   unsigned long long ncore;
   unsigned long long pairs_done;
+  unsigned long long unit_count;  // units in the culled unit list
   int32_t kept32;
   uint32_t unsafe_flag;
   int32_t nclusters;
+  int32_t units32;
 };
 
 }  // namespace
@@ -66,7 +68,7 @@ struct ds_ctx {
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, bbox, blk, diag;
+      keys_alt, kidx, sort_temp, bbox, blk, diag, ulist, uchunks, ucnt;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -77,6 +79,7 @@ struct ds_ctx {
   int sort = 1;          // DS_OPT_SPATIAL_SORT
   bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
+  unsigned long long units_cap = 0;  // culled unit list capacity (units)
   Scalars* h_scalars = nullptr;      // pinned
 };
 
@@ -106,7 +109,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                      &c->sort_temp, &c->bbox, &c->blk, &c->diag};
+                      &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -147,7 +150,7 @@ constexpr size_t WORD_BYTES = 8;  // one adjacency record
 size_t base_bytes(int64_t n, int d) {
   const size_t N = (size_t)n;
   return N * rec_stride(d) * 4      // rec
-         + (size_t)n_items(n_tiles(n)) * (16 + 4 + 4)  // chunk table + item list + flags
+         + (size_t)n_items(n_tiles(n)) * (16 + 4 + 4 + 4)  // dir + item list + flags + units
          + (size_t)n_tiles(n) * (2 * padded_dim(d) + 1) * 4  // tile boxes
          + N * rec_stride(d) * 4 + N * (4 + 4 + 8 + 8 + 4)  // spatial order
          + ((N + 31) / 32) * (2 * padded_dim(d) + 1) * 4      // 32-point block boxes
@@ -193,7 +196,7 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->flag, N * 4));
   DS_CK(ensure(c->partials, (size_t)scan_partials_len(n) * 4));
   DS_CK(ensure(c->scalars, sizeof(Scalars)));
-  DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));
+  DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));  // tile-pair directory
   DS_CK(ensure(c->diag, (size_t)n_tiles(n) * 4));
   return DS_OK;
 }
@@ -204,7 +207,8 @@ cudaError_t record(ds_ctx* c, cudaEvent_t e, cudaStream_t s) {
 }
 
 struct Plan {
-  int64_t T = 0, all_items = 0, item_lo = 0, item_hi = 0;
+  int64_t T = 0, all_items = 0, item_lo = 0, item_hi = 0, dense_units = 0;
+  unsigned long long units_cap = 0;
   bool cull = false;
   size_t base = 0;
   int rank = 0, world = 1;
@@ -224,6 +228,10 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     return DS_EINVAL;
   }
   pl.T = n_tiles(n);
+  if (pl.T > 65536) {  // tile pairs are packed as a << 16 | b
+    set_error("n: more than 2^25 points per call is not supported");
+    return DS_EINVAL;
+  }
   pl.all_items = n_items(pl.T);
   pl.cull = c->cull != 0 && pl.T > 1;
   pl.rank = rank;
@@ -232,8 +240,16 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   // slice of the device-side kept list is taken inside the kernel
   pl.item_lo = pl.all_items * rank / world;
   pl.item_hi = pl.all_items * (rank + 1) / world;
-  pl.base = base_bytes(n, d);
   const int64_t T = pl.T;
+  const int upt = units_per_tile(d);
+  pl.dense_units = pl.all_items * upt;
+  if (pl.cull) {  // unit list + chunk table sized from earlier calls (lazy, like the words)
+    const unsigned long long guess = (unsigned long long)n / 2 + 4096;
+    pl.units_cap = std::max<unsigned long long>(c->units_cap, guess);
+  } else {
+    pl.units_cap = (unsigned long long)pl.dense_units;
+  }
+  pl.base = base_bytes(n, d) + (size_t)pl.units_cap * (pl.cull ? 16 : 8);
 
   unsigned long long want =
       std::max<unsigned long long>(c->words_cap, (unsigned long long)n * 8 + (1ull << 20));
@@ -290,37 +306,44 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
                       lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p,
                       &sc->kept32, (uint32_t*)c->items.p, &sc->kept, s));
   }
-  const bool block_skip = pl.cull && padded_dim(d) <= 4;
-  if (block_skip) {
-    DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * padded_dim(d) + 1) * 4));
-    DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
-  }
-  TileArgs a;
+  UnitArgs a;
   a.rec = rec;
   a.n = n;
   a.T = (int32_t)T;
-  a.d = d;
-  a.item_lo = pl.item_lo;
-  a.item_hi = pl.item_hi;
-  a.item_list = pl.cull ? (const uint32_t*)c->items.p : nullptr;
-  a.item_count = &sc->kept;
-  a.shard_rank = rank;
-  a.shard_world = world;
-  a.work_ctr = &sc->work_ctr;
   a.eps32 = eps32;
   a.cnt = (int32_t*)c->cnt.p;
   a.words = (uint2*)c->words.p;
   a.words_cap = c->words_cap;
   a.words_count = &sc->words_count;
-  a.chunks = (uint4*)c->chunks.p;
-  a.chunks_cap = (unsigned long long)pl.all_items;
-  a.nonempty_count = &sc->nonempty_count;
+  a.item_list = pl.cull ? (const uint32_t*)c->items.p : nullptr;
+  a.unit_count = &sc->unit_count;
+  a.units_cap = pl.units_cap;
+  a.dense_units = pl.dense_units;
+  a.shard_rank = rank;
+  a.shard_world = world;
   a.unsafe_flag = &sc->unsafe_flag;
-  a.blk = block_skip ? (const float*)c->blk.p : nullptr;
   a.pairs_done = &sc->pairs_done;
+  a.unit_list = nullptr;
+  if (pl.cull) {
+    const int dp = padded_dim(d);
+    DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * dp + 1) * 4));
+    DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
+    DS_CK(ensure(c->ucnt, (size_t)pl.all_items * 4));
+    DS_CK(ensure(c->ulist, (size_t)pl.units_cap * 8));
+    c->units_cap = pl.units_cap;
+    DS_CK(launch_unit_list((const float*)c->blk.p, n, d, eps32, formula, &sc->unsafe_flag,
+                           (const uint32_t*)c->items.p, &sc->kept, pl.all_items,
+                           (int32_t*)c->ucnt.p, (int32_t*)c->ipartials.p, &sc->units32,
+                           (uint2*)c->ulist.p, pl.units_cap, &sc->unit_count, s));
+    a.unit_list = (const uint2*)c->ulist.p;
+  }
+  DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * 8));
+  a.uchunks = (uint2*)c->uchunks.p;
   DS_CK(record(c, c->ev[1], s));
-  DS_CK(launch_tile(a, formula, c->sm_count, s));
+  DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
   DS_CK(record(c, c->ev[2], s));
+  DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const int32_t*)c->ucnt.p : nullptr,
+                        &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count, s));
   return DS_OK;
 }
 
@@ -328,6 +351,19 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
 // buffer to the exact need (+6%) and ask for a re-run.
 ds_status check_words(ds_ctx* c, const Plan& pl, int64_t mem_cap, bool* retry) {
   *retry = false;
+  if (pl.cull && c->h_scalars->unit_count > pl.units_cap) {  // unit list overflowed: grow, re-run
+    const unsigned long long nu = c->h_scalars->unit_count;
+    const unsigned long long grow = nu + nu / 16 + 1024;
+    const int64_t required = (int64_t)(pl.base + (grow - pl.units_cap) * 16);
+    if (mem_cap > 0 && required > mem_cap) {
+      set_capacity(required, mem_cap);
+      set_error("work-unit list exceeds the memory cap");
+      return DS_ECAPACITY;
+    }
+    c->units_cap = grow;
+    *retry = true;
+    return DS_OK;
+  }
   const unsigned long long need = c->h_scalars->words_count;
   if (need <= c->words_cap) return DS_OK;
   const unsigned long long grow = need + need / 16 + 1024;
@@ -377,7 +413,8 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(launch_core_init(w, min_pts, s));
   DS_CK(rec(c->ev[3]));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap,
+                            (const uint2*)c->uchunks.p, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
@@ -412,7 +449,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[8] = g_alloc_generation;
     key[9] = (unsigned long long)mem_cap;
     key[10] = (unsigned long long)c->device;
-    key[11] = 0;
+    key[11] = c->units_cap;
     const bool graph_hit = c->use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
     if (graph_hit) {
       DS_CK(cudaGraphLaunch(c->gexec, s));
@@ -422,7 +459,9 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       pl.cull = c->cull != 0 && pl.T > 1;
       pl.item_lo = 0;
       pl.item_hi = pl.all_items;
-      pl.base = base_bytes(n, d);
+      pl.dense_units = pl.all_items * units_per_tile(d);
+      pl.units_cap = pl.cull ? c->units_cap : (unsigned long long)pl.dense_units;
+      pl.base = base_bytes(n, d) + (size_t)pl.units_cap * (pl.cull ? 16 : 8);
     } else if (c->use_graph && std::memcmp(key, c->seen_key, sizeof key) == 0) {
       // second call with this key: record the device pipeline and replay it
       if (c->gexec) {
@@ -464,6 +503,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       // key after this call's allocations: the next identical call records the graph
       key[7] = c->words_cap;
       key[8] = g_alloc_generation;
+      key[11] = c->units_cap;
       std::memcpy(c->seen_key, key, sizeof key);
     }
     if (h_labels)
@@ -558,7 +598,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                &c->sort_temp, &c->bbox, &c->blk, &c->diag};
+                &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -651,7 +691,8 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
       DS_CK(ensure(c->dense, dense));
       DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
       Scalars* sc = (Scalars*)c->scalars.p;
-      DS_CK(launch_export_bits((const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+      DS_CK(launch_export_bits((const uint2*)c->words.p, c->words_cap,
+                               (const uint2*)c->uchunks.p, (const uint4*)c->chunks.p,
                                &sc->nonempty_count, perm, (uint32_t*)c->dense.p, stride, s));
       DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
       const size_t row_bytes = (size_t)(n + 7) / 8;
@@ -797,7 +838,8 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
   DS_CK(launch_core_init(w, min_pts, s));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap, (const uint4*)c->chunks.p,
+  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap,
+                            (const uint2*)c->uchunks.p, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(cudaMemcpyAsync(d_parent, c->parent.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   DS_CK(cudaMemcpyAsync(d_bmin, c->bmin.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));

@@ -9,8 +9,9 @@
 //   words    uint2   [cap]       {32-bit adjacency word, local row << 4 | column word}: the
 //                                non-zero words of the upper-triangle tile pairs, i.e. the
 //                                bit-packed neighbourhood matrix without its empty part,
-//                                grouped in one contiguous chunk per tile pair
-//   chunks   uint4   [items]     {a, b, first word lo, count | first word hi << 16}
+//                                grouped in one contiguous chunk per work unit
+//   uchunks  uint2   [units]     {first word lo, count | first word hi << 16}
+//   dir      uint4   [items]     tile pairs with words: {a << 16 | b, first unit, units, hi}
 //   parent   int32   [n]         union-find forest over core points (root = min index)
 //   bmin     int32   [n]         lowest in-range core of each non-core point
 //   root/cmin/flag/id int32 [n]  canonical relabel workspace
@@ -43,33 +44,49 @@ inline int64_t n_items(int64_t T) { return T * (T + 1) / 2; }
 // arithmetic (|d2| <= 4*d*max|c|^2); such inputs take the compare-based path
 constexpr float SAFE_ABS = 1.0e17f;
 
-struct TileArgs {
+// Work unit of the eps-tile kernel: (a block of 32*KP consecutive points of tile a,
+// held in registers by one warp) x (a block of 32 points of tile b, staged in
+// shared memory). KP = 4 / 2 / 1 lane points per lane for d <= 8 / 32 / 64.
+inline int unit_kp(int d) { return padded_dim(d) <= 8 ? 4 : (padded_dim(d) <= 32 ? 2 : 1); }
+inline int units_per_tile(int d) { return (TILE / (32 * unit_kp(d))) * WPR; }
+
+struct UnitArgs {
   const float* rec;
   int64_t n;
-  int32_t T;               // tiles per side
-  int32_t d;               // runtime dimension (generic instantiation only)
-  int64_t item_lo, item_hi;
-  unsigned long long* work_ctr;
+  int32_t T;                            // tiles per side
   float eps32;
   int32_t* cnt;
-  uint2* words;                        // {32-bit word, local row << 4 | column word}
+  uint2* words;                         // {32-bit word, local row << 4 | column word}
   unsigned long long words_cap;
   unsigned long long* words_count;
-  uint4* chunks;                       // {a, b, base lo, count | base hi << 16}
-  unsigned long long chunks_cap;
-  unsigned long long* nonempty_count;  // = chunks emitted
+  uint2* uchunks;                       // per unit {first word lo, count | first word hi << 16}
+  const uint32_t* item_list;            // culled tile pairs (a << 16 | b), or nullptr: triangle
+  const uint2* unit_list;               // culled units {item, sub}, or nullptr: q * UPT + sub
+  const unsigned long long* unit_count; // length of unit_list (device)
+  unsigned long long units_cap;         // capacity of unit_list / uchunks (culled)
+  int64_t dense_units;                  // all_items * UPT (dense schedule)
+  int32_t shard_rank, shard_world;      // slice of the units this launch evaluates
   const uint32_t* unsafe_flag;
-  const uint32_t* item_list;           // culled items (a << 16 | b), or nullptr: dense triangle
-  const unsigned long long* item_count; // length of item_list (device)
-  int32_t shard_rank, shard_world;     // slice of item_list this launch evaluates
-  const float* blk;                    // 32-point block boxes (nullptr: no sub-tile culling)
-  unsigned long long* pairs_done;      // ordered pairs evaluated (32 x 32*KP per word group)
+  unsigned long long* pairs_done;       // ordered pairs evaluated (32 x 32*KP per unit)
 };
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
                         cudaStream_t s);
-cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream_t s);
+cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
+                                cudaStream_t s);
+// culled schedule: per kept tile pair, the units that are not provably empty
+// (ucnt: per-item unit count, scanned in place into the item's first unit)
+cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, int formula,
+                             const uint32_t* unsafe_flag, const uint32_t* item_list,
+                             const unsigned long long* kept, int64_t all_items, int32_t* ucnt,
+                             int32_t* partials, int32_t* total32, uint2* unit_list,
+                             unsigned long long units_cap, unsigned long long* unit_count,
+                             cudaStream_t s);
+// per tile pair with words: {a << 16 | b, first unit lo, units, first unit hi} (atomic append)
+cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const int32_t* item_off,
+                            const unsigned long long* kept, uint4* dir,
+                            unsigned long long* dir_count, cudaStream_t s);
 // 32-point block boxes [block][lo(dpad), hi(dpad), maxnorm] for sub-tile culling
 cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s);
 // tile bounding boxes + list of tile pairs that are not provably empty
@@ -96,23 +113,23 @@ struct MergeWs {
   int32_t* partials;      // scan block partials
   int32_t* nclusters;     // device scalar
   unsigned long long* ncore;
-  int32_t* diag_idx = nullptr;    // chunk index of each diagonal tile pair (-1: none)
+  int32_t* diag_idx = nullptr;    // dir index of each diagonal tile pair (-1: none)
   const int32_t* perm = nullptr;  // sorted -> original index (nullptr: identity)
   const int32_t* inv = nullptr;   // original -> sorted index
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
 cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
-                                const uint4* chunks, const unsigned long long* nchunks,
-                                cudaStream_t s);
+                                const uint2* uchunks, const uint4* dir,
+                                const unsigned long long* ndir, cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
                               cudaStream_t s);
-cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint4* chunks,
-                               const unsigned long long* nchunks, const int32_t* perm,
+cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint2* uchunks,
+                               const uint4* dir, const unsigned long long* ndir, const int32_t* perm,
                                uint32_t* bits32, int64_t stride_words, cudaStream_t s);
 cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* perm, int to_original,
                                int32_t* dst, cudaStream_t s);

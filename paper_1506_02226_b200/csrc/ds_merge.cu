@@ -138,19 +138,82 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
 // covered by one global link per chunk; the other bits link their two
 // ancestors directly (rare). Border minima (lowest ORIGINAL core index,
 // merge.py:116-130) are reduced per chunk in shared memory, then once per point.
-struct ChunkInfo {
-  int a, b;
-  unsigned long long base;
-  int count;
+// A directory entry names one tile pair with words and its range of unit chunks;
+// the words of a tile pair are the concatenation of its units' chunks. ItemWords
+// holds the prefix sums of the chunk lengths in shared memory so that a CTA can
+// walk the tile pair's words as one flat index space (word k lives in the last
+// chunk whose prefix is <= k).
+constexpr int MAX_UPT = (TILE / 32) * WPR;  // 256 units per tile pair (KP = 1)
+
+struct ItemWords {
+  uint32_t pre[MAX_UPT + 1];
+  unsigned long long base[MAX_UPT];
+  int nunits;
+  int total;
+  int ok;
 };
 
-__device__ __forceinline__ ChunkInfo decode_chunk(uint4 c) {
-  ChunkInfo ci;
-  ci.a = (int)c.x;
-  ci.b = (int)c.y;
-  ci.base = (unsigned long long)c.z | ((unsigned long long)(c.w >> 16) << 32);
-  ci.count = (int)(c.w & 0xffffu);
-  return ci;
+struct DirInfo {
+  int a, b;
+  unsigned long long ulo;
+  int nunits;
+};
+
+__device__ __forceinline__ DirInfo decode_dir(uint4 e) {
+  DirInfo di;
+  di.a = (int)(e.x >> 16);
+  di.b = (int)(e.x & 0xffffu);
+  di.ulo = (unsigned long long)e.y | ((unsigned long long)e.w << 32);
+  di.nunits = (int)e.z;
+  return di;
+}
+
+// Called by every thread of the CTA (contains __syncthreads).
+__device__ void load_item_words(const DirInfo& di, const uint2* __restrict__ uchunks,
+                               unsigned long long words_cap, ItemWords& iw) {
+  __syncthreads();  // the previous entry's readers are done with iw
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t run = 0;
+    bool bad = false;
+    for (int c0 = 0; c0 < di.nunits; c0 += 32) {
+      const int c = c0 + lane;
+      const uint2 e = c < di.nunits ? uchunks[di.ulo + c] : make_uint2(0u, 0u);
+      const uint32_t cnt = e.y & 0xffffu;
+      const unsigned long long base = (unsigned long long)e.x | ((unsigned long long)(e.y >> 16) << 32);
+      bad |= cnt != 0 && base + cnt > words_cap;  // overflowed run: the host re-runs
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      if (c < di.nunits) {
+        iw.pre[c] = run + incl - cnt;
+        iw.base[c] = base;
+      }
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const bool any_bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      iw.pre[di.nunits] = run;
+      iw.nunits = di.nunits;
+      iw.total = (int)run;
+      iw.ok = !any_bad;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint2 item_word(const ItemWords& iw, const uint2* __restrict__ words,
+                                           uint32_t k) {
+  int lo = 0, hi = iw.nunits;  // pre[lo] <= k < pre[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (iw.pre[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  return words[iw.base[lo] + (k - iw.pre[lo])];
 }
 
 __device__ __forceinline__ int find_local(int* lp, int v) {
@@ -193,19 +256,20 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 }
 
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
-__global__ void diag_index_kernel(const uint4* __restrict__ chunks,
-                                  const unsigned long long* __restrict__ nchunks,
+__global__ void diag_index_kernel(const uint4* __restrict__ dir,
+                                  const unsigned long long* __restrict__ ndir,
                                   int32_t* __restrict__ diag_idx) {
-  const unsigned long long total = *nchunks;
+  const unsigned long long total = *ndir;
   for (unsigned long long c = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; c < total;
        c += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint4 ch = chunks[c];
-    if (ch.x == ch.y) diag_idx[ch.x] = (int32_t)c;
+    const uint32_t ab = dir[c].x;
+    if ((ab >> 16) == (ab & 0xffffu)) diag_idx[ab >> 16] = (int32_t)c;
   }
 }
 
 __global__ void __launch_bounds__(512) union_diag_kernel(
-    const uint4* __restrict__ chunks, const int32_t* __restrict__ diag_idx, int64_t ntiles,
+    const uint4* __restrict__ dir, const uint2* __restrict__ uchunks,
+    const int32_t* __restrict__ diag_idx, int64_t ntiles,
     const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
     const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
@@ -221,14 +285,16 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   __shared__ uint32_t adj[32];
   __shared__ int wroots[WPR], wpre[WPR], slot_root[32];
   __shared__ int ntrees_sh;
+  __shared__ ItemWords iw;
   const int tid = threadIdx.x;
   const int w = tid % WPR, cblk = tid / WPR;
   const int64_t nw = (n + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int c = diag_idx[tile];
     if (c < 0) continue;  // uniform per CTA
-    const ChunkInfo ci = decode_chunk(chunks[c]);
-    if (ci.base + ci.count > words_cap) continue;  // overflowed run: the host re-runs
+    const DirInfo ci = decode_dir(dir[c]);
+    load_item_words(ci, uchunks, words_cap, iw);
+    if (!iw.ok) continue;  // uniform per CTA
     const int base = ci.a * TILE;
     if (tid < WPR) {
       const int64_t gw = (int64_t)ci.a * WPR + tid;
@@ -243,8 +309,8 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     __syncthreads();
     // scatter the chunk into the dense matrix (core rows, core columns only);
     // non-core rows give their own border candidate directly
-    for (int k = tid; k < ci.count; k += THREADS) {
-      const uint2 rec = words[ci.base + k];
+    for (int k = tid; k < iw.total; k += THREADS) {
+      const uint2 rec = item_word(iw, words, (uint32_t)k);
       const int u = (int)(rec.y >> 4);
       const int ww = (int)(rec.y & 15u);
       const uint32_t cw = lcw[ww];
@@ -386,10 +452,11 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) union_pair_kernel(
-    const uint4* __restrict__ chunks, const unsigned long long* __restrict__ nchunks,
-    const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
-    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
-    const int32_t* __restrict__ perm) {
+    const uint4* __restrict__ dir, const unsigned long long* __restrict__ ndir,
+    const uint2* __restrict__ uchunks, const uint2* __restrict__ words,
+    unsigned long long words_cap, int64_t n, const uint32_t* __restrict__ corew, int32_t* parent,
+    int32_t* bmin, const int32_t* __restrict__ perm) {
+  __shared__ ItemWords iw;
   __shared__ int la[2 * TILE];    // current ancestor of each point (-1: not core)
   __shared__ int lb[2 * TILE];    // border minima (original indices)
   __shared__ int hist[2 * TILE];  // ancestors that are local indices of the own tile
@@ -398,12 +465,13 @@ __global__ void __launch_bounds__(THREADS) union_pair_kernel(
   __shared__ int dom[2];
   __shared__ int link_ab;
   const int tid = threadIdx.x;
-  const unsigned long long total = *nchunks;
+  const unsigned long long total = *ndir;
   const int64_t nw = (n + 31) / 32;
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
-    const ChunkInfo ci = decode_chunk(chunks[c]);
+    const DirInfo ci = decode_dir(dir[c]);
     if (ci.a == ci.b) continue;  // uniform per CTA
-    if (ci.base + ci.count > words_cap) continue;  // overflowed run: the host re-runs
+    load_item_words(ci, uchunks, words_cap, iw);
+    if (!iw.ok) continue;
     if (tid < 2 * WPR) {
       const int64_t gw = (int64_t)(tid < WPR ? ci.a : ci.b) * WPR + (tid & (WPR - 1));
       lcw[tid] = gw < nw ? corew[gw] : 0u;
@@ -456,8 +524,8 @@ __global__ void __launch_bounds__(THREADS) union_pair_kernel(
     }
     __syncthreads();
     const int ga = dom[0];
-    for (int k = tid; k < ci.count; k += THREADS) {
-      const uint2 rec = words[ci.base + k];
+    for (int k = tid; k < iw.total; k += THREADS) {
+      const uint2 rec = item_word(iw, words, (uint32_t)k);
       const uint32_t x = rec.x;
       const int u = (int)(rec.y >> 4);
       const int w = (int)(rec.y & 15u);
@@ -665,16 +733,18 @@ __global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n,
 // chunks -> dense native-word rows in ORIGINAL index order, both orientations
 // (the chunks only hold a <= b)
 __global__ void export_bits_kernel(const uint2* __restrict__ words, unsigned long long words_cap,
-                                   const uint4* __restrict__ chunks,
-                                   const unsigned long long* __restrict__ nchunks,
+                                   const uint2* __restrict__ uchunks, const uint4* __restrict__ dir,
+                                   const unsigned long long* __restrict__ ndir,
                                    const int32_t* __restrict__ perm, uint32_t* bits32,
                                    int64_t stride_words) {
-  const unsigned long long total = *nchunks;
+  __shared__ ItemWords iw;
+  const unsigned long long total = *ndir;
   for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
-    const ChunkInfo ci = decode_chunk(chunks[c]);
-    if (ci.base + ci.count > words_cap) continue;
-    for (int k = threadIdx.x; k < ci.count; k += blockDim.x) {
-      const uint2 rec = words[ci.base + k];
+    const DirInfo ci = decode_dir(dir[c]);
+    load_item_words(ci, uchunks, words_cap, iw);
+    if (!iw.ok) continue;
+    for (int k = threadIdx.x; k < iw.total; k += blockDim.x) {
+      const uint2 rec = item_word(iw, words, (uint32_t)k);
       uint32_t x = rec.x;
       const int64_t is = (int64_t)ci.a * TILE + (rec.y >> 4);
       const int64_t i = perm ? perm[is] : is;
@@ -726,8 +796,8 @@ cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) 
 }
 
 cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
-                                const uint4* chunks, const unsigned long long* nchunks,
-                                cudaStream_t s) {
+                                const uint2* uchunks, const uint4* dir,
+                                const unsigned long long* ndir, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -742,14 +812,14 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned l
   const int64_t ntiles = (w.n + TILE - 1) / TILE;
   cudaError_t e = cudaMemsetAsync(w.diag_idx, 0xff, (size_t)ntiles * 4, s);
   if (e != cudaSuccess) return e;
-  diag_index_kernel<<<sms, 256, 0, s>>>(chunks, nchunks, w.diag_idx);
+  diag_index_kernel<<<sms, 256, 0, s>>>(dir, ndir, w.diag_idx);
   // one CTA per tile (one wave: up to 4 resident per SM)
   const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
-  union_diag_kernel<<<(unsigned)grid, 512, diag_smem, s>>>(chunks, w.diag_idx, ntiles, words,
-                                                          words_cap, w.n, w.corew, w.parent,
-                                                          w.bmin, w.perm);
-  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(chunks, nchunks, words, words_cap, w.n, w.corew,
-                                                 w.parent, w.bmin, w.perm);
+  union_diag_kernel<<<(unsigned)grid, 512, diag_smem, s>>>(dir, uchunks, w.diag_idx, ntiles,
+                                                          words, words_cap, w.n, w.corew,
+                                                          w.parent, w.bmin, w.perm);
+  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(dir, ndir, uchunks, words, words_cap, w.n,
+                                                 w.corew, w.parent, w.bmin, w.perm);
   return cudaGetLastError();
 }
 
@@ -818,10 +888,10 @@ cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm
   return cudaGetLastError();
 }
 
-cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint4* chunks,
-                               const unsigned long long* nchunks, const int32_t* perm,
+cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint2* uchunks,
+                               const uint4* dir, const unsigned long long* ndir, const int32_t* perm,
                                uint32_t* bits32, int64_t stride_words, cudaStream_t s) {
-  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, words_cap, chunks, nchunks, perm, bits32,
+  export_bits_kernel<<<148 * 4, 256, 0, s>>>(words, words_cap, uchunks, dir, ndir, perm, bits32,
                                              stride_words);
   return cudaGetLastError();
 }

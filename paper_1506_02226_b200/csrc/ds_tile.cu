@@ -41,40 +41,8 @@
 namespace ds {
 namespace {
 
-// ---- PTX helpers: mbarrier + TMA bulk copy -------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "DS_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra DS_WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // ---- item <-> tile pair --------------------------------------------------------
@@ -96,19 +64,6 @@ __device__ __forceinline__ void decode_item(int64_t q, int64_t T, int& a, int& b
 // is needed by the reference-layout export and is a no-op for the merge).
 __device__ __forceinline__ uint32_t diag_keep(int rel) {
   return rel <= 0 ? 0xffffffffu : (rel > 31 ? 0u : ((1u << (32 - rel)) - 1u));
-}
-
-// Item q -> tile pair: through the culled item list when one is given, else the
-// dense upper-triangle enumeration.
-__device__ __forceinline__ void item_tiles(const TileArgs& args, int64_t q, int64_t T, int& a,
-                                           int& b) {
-  if (args.item_list) {
-    const uint32_t ab = args.item_list[q];
-    a = (int)(ab >> 16);
-    b = (int)(ab & 0xffffu);
-  } else {
-    decode_item(q, T, a, b);
-  }
 }
 
 __device__ __forceinline__ uint32_t valid_mask(int m) {
@@ -259,358 +214,479 @@ __device__ __forceinline__ void pack_bits(const float (&d2)[KP], float eps32, in
 
 template <int D>
 struct Geo {
-  static constexpr int KP = D <= 8 ? 4 : (D <= 32 ? 2 : 1);  // lane points per thread
-  static constexpr int THREADS = TILE / KP;
+  static constexpr int KP = D <= 8 ? 4 : (D <= 32 ? 2 : 1);  // lane points per lane
   static constexpr int S = ((D + 1) + 3) / 4 * 4;           // floats per record
-  static constexpr int NBUF = (2 * TILE * S * 4 <= 96 * 1024) ? 2 : 1;
-  static constexpr int CHUNKS = THREADS / WPR;               // row chunks per word column
-  static constexpr int ROWS = TILE / CHUNKS;                 // rows per chunk
-  static constexpr int SL0 = ROWS == 64 ? 7 : (ROWS == 32 ? 6 : 5);  // slices per chunk
-  static constexpr size_t SMEM = (size_t)NBUF * TILE * S * 4 + (size_t)WPR * BSTRIDE * 4;
+  static constexpr int WARPS = 4;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int STAGE = 32 * S;                       // floats per staged block
+  static constexpr size_t SMEM = (size_t)WARPS * 2 * STAGE * 4;
+  static constexpr int UNROLL = D <= 4 ? 32 : 8;
+  static constexpr int MINB = D <= 32 ? 4 : 3;  // 16 (d <= 32) or 12 resident warps per SM
 };
 
-// Bit-sliced add of a partner counter (10 slices) into ours.
-__device__ __forceinline__ void sliced_add(uint32_t (&s)[10], const uint32_t (&o)[10]) {
-  uint32_t carry = 0;
+// Column-side counts of one unit: the number of set bits of every column over the
+// warp's 32*KP words. Per lane the KP words are added bit-sliced (carry-save), then
+// five butterfly rounds add the lanes' slice vectors; lane j extracts column j.
+template <int KP>
+__device__ __forceinline__ uint32_t column_counts(const uint32_t (&w)[KP], int lane) {
+  constexpr int W0 = KP == 4 ? 3 : (KP == 2 ? 2 : 1);
+  uint32_t s[W0 + 5];
 #pragma unroll
-  for (int l = 0; l < 10; ++l) {
-    const uint32_t a = s[l], b = o[l];
-    s[l] = a ^ b ^ carry;
-    carry = (a & b) | (carry & (a ^ b));
+  for (int l = 0; l < W0 + 5; ++l) s[l] = 0u;
+  if constexpr (KP == 4) {
+    const uint32_t x = w[0] ^ w[1] ^ w[2];
+    const uint32_t c1 = (w[0] & w[1]) | (w[2] & (w[0] ^ w[1]));
+    s[0] = x ^ w[3];
+    const uint32_t c2 = x & w[3];
+    s[1] = c1 ^ c2;
+    s[2] = c1 & c2;
+  } else if constexpr (KP == 2) {
+    s[0] = w[0] ^ w[1];
+    s[1] = w[0] & w[1];
+  } else {
+    s[0] = w[0];
   }
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int width = W0 + r;
+    uint32_t carry = 0u;
+#pragma unroll
+    for (int l = 0; l < W0 + 4; ++l) {
+      if (l < width) {
+        const uint32_t t = s[l];
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, t, 16 >> r);
+        s[l] = t ^ o ^ carry;
+        carry = (t & o) | (carry & (t ^ o));
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < W0 + 5; ++l)
+      if (l == width) s[l] = carry;
+  }
+  const int p = 31 - lane;  // bit (31 - j) <-> column j
+  uint32_t v = 0u;
+#pragma unroll
+  for (int l = 0; l < W0 + 5; ++l) v |= ((s[l] >> p) & 1u) << l;
+  return v;
 }
 
+// Unit -> (tile pair, lane block, column block); `self` = the column block lies
+// inside the lane block of a diagonal tile. Units that need no evaluation (ragged
+// tail, or below the diagonal of a diagonal tile: their pairs are covered by the
+// mirrored unit) report skip.
+struct UnitInfo {
+  int a, b, lb, jw;
+  bool self, skip;
+};
+
+// Walks a warp's slice of the units. Culled schedule: one 8-byte list entry
+// {a << 16 | b, sub} per unit. Dense schedule: units are q * UPT + sub over the
+// upper triangle in row order, so only the slice start is decoded (decode_item);
+// later units step (sub, b, a) incrementally.
+template <int KP>
+struct UnitCursor {
+  static constexpr int UPT = (TILE / (32 * KP)) * WPR;
+  const uint2* list;
+  int T, n;
+  int a, b, sub;
+
+  __device__ __forceinline__ void start(const UnitArgs& A, long long u) {
+    list = A.unit_list;
+    T = A.T;
+    n = (int)A.n;
+    if (!list) {
+      const long long q = u / UPT;
+      sub = (int)(u - q * UPT);
+      decode_item(q, T, a, b);
+    }
+  }
+  // info of unit u (the previous call, if any, was for u - 1)
+  __device__ __forceinline__ UnitInfo get(long long u, bool first) {
+    if (list) {
+      const uint2 e = __ldg(list + u);
+      a = (int)(e.x >> 16);
+      b = (int)(e.x & 0xffffu);
+      sub = (int)e.y;
+    } else if (!first) {
+      if (++sub == UPT) {
+        sub = 0;
+        if (++b == T) b = ++a;
+      }
+    }
+    UnitInfo ui;
+    ui.a = a;
+    ui.b = b;
+    ui.lb = sub / WPR;
+    ui.jw = sub % WPR;
+    const int na = min(TILE, n - a * TILE);
+    const int nb = min(TILE, n - b * TILE);
+    ui.skip = ui.jw * 32 >= nb || ui.lb * 32 * KP >= na || (a == b && ui.jw < ui.lb * KP);
+    ui.self = a == b && ui.jw < (ui.lb + 1) * KP;
+    return ui;
+  }
+};
+
+// cp.async staging of one column block (16 bytes per instruction, zero-filled past n)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// The eps-tile kernel. Every warp owns a contiguous slice of the unit list and works
+// through it without any block-level synchronisation:
+//   * the unit's 32 staged points (one contiguous 32*S*4-byte run of the record
+//     array) are copied into the warp's double buffer with cp.async (one 16-byte
+//     copy per lane and record quarter), issued one unit ahead;
+//   * the lane block (32*KP consecutive points of tile a) is held in registers and
+//     only reloaded when the slice moves to another lane block;
+//   * per staged point every lane evaluates its KP points in the reference's exact
+//     operation order (eval_d2) and packs the predicates (pack_bits);
+//   * lane-side counts are popcounts accumulated in registers across the units of a
+//     lane block; column-side counts (off-diagonal units only: each unordered pair
+//     is evaluated once) come from column_counts, one atomic per column;
+//   * the unit's non-zero words are appended with one warp-aggregated atomic and
+//     the unit's chunk entry records where they went. Units without a single bit
+//     (most of a dense schedule) skip both.
 template <int D, int F, bool SAFE>
-__global__ void __launch_bounds__(Geo<D>::THREADS, (D <= 8 ? 4 : (D <= 32 ? 2 : 1)))
-eps_tile_kernel(const TileArgs args) {
+__global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
   using G = Geo<D>;
   constexpr int KP = G::KP;
-  constexpr int NTH = G::THREADS;
   constexpr int S = G::S;
   constexpr int KC = Pack<KP, SAFE>::KC;
 
-  if ((*args.unsafe_flag != 0) == SAFE) return;  // the other instantiation owns this input
+  if ((*A.unsafe_flag != 0) == SAFE) return;  // the other instantiation owns this input
 
   extern __shared__ __align__(128) unsigned char smem[];
-  float* bc = reinterpret_cast<float*>(smem);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + (size_t)G::NBUF * TILE * S * 4);
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ long long item_sh[2];
-  __shared__ unsigned int scan_sh[NTH / 32 + 1];
-  __shared__ unsigned long long base_sh;
-  __shared__ uint8_t unit_active[(NTH / 32) * WPR];
-  __shared__ uint16_t unit_list[(NTH / 32) * WPR];
-  __shared__ int unit_count;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  float* stage = reinterpret_cast<float*>(smem) + (size_t)warp * 2 * G::STAGE;
 
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int64_t n = args.n;
-  const int64_t T = args.T;
-  const float eps32 = args.eps32;
-
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_fence_init();
+  const int n = (int)A.n;
+  const float eps32 = A.eps32;
+  long long U = A.dense_units;
+  if (A.unit_list) {
+    const unsigned long long c = *A.unit_count;
+    U = (long long)(c < A.units_cap ? c : A.units_cap);
   }
-  __syncthreads();
+  const long long r_lo = U * A.shard_rank / A.shard_world;
+  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  const long long nw = (long long)gridDim.x * G::WARPS;
+  const long long gw = (long long)blockIdx.x * G::WARPS + warp;
+  const long long u_lo = r_lo + (r_hi - r_lo) * gw / nw;
+  const long long u_hi = r_lo + (r_hi - r_lo) * (gw + 1) / nw;
+  if (u_lo >= u_hi) return;
 
-  auto issue = [&](long long q, int buf) {  // thread 0 only
-    int a, b;
-    item_tiles(args, q, T, a, b);
-    const int64_t nb = min((int64_t)TILE, n - (int64_t)b * TILE);
-    const uint32_t bytes = (uint32_t)(nb * S * 4);
-    mbar_expect_tx(&mbar[buf], bytes);
-    bulk_g2s(bc + (size_t)buf * TILE * S, args.rec + (size_t)b * TILE * S, bytes, &mbar[buf]);
+  UnitCursor<KP> cursor;
+  cursor.start(A, u_lo);
+  // next unit to evaluate after u (skipped units get an empty chunk)
+  auto next_unit = [&](long long u, UnitInfo& ui, bool first) -> long long {
+    for (; u < u_hi; ++u, first = false) {
+      ui = cursor.get(u, first);
+      if (!ui.skip) return u;
+      if (lane == 0) A.uchunks[u] = make_uint2(0u, 0u);
+    }
+    return u;
+  };
+  auto issue = [&](const UnitInfo& ui, int buf) {  // all lanes: record `lane` of the block
+    const int j = ui.b * TILE + ui.jw * 32 + lane;
+    const bool v = j < n;
+    const float* src = A.rec + (size_t)(v ? j : 0) * S;
+    float* dst = stage + (size_t)buf * G::STAGE + lane * S;
+#pragma unroll
+    for (int q = 0; q < S / 4; ++q) cp_async16(dst + 4 * q, src + 4 * q, v ? 16u : 0u);
+    cp_async_commit();
   };
 
-  __shared__ long long range_sh[2];
-  if (tid == 0) {
-    long long lo = args.item_lo, hi = args.item_hi;
-    if (args.item_list) {  // culled list: this shard's slice of the device-side count
-      const long long total = (long long)*args.item_count;
-      lo = total * args.shard_rank / args.shard_world;
-      hi = total * (args.shard_rank + 1) / args.shard_world;
-    }
-    range_sh[0] = lo;
-    range_sh[1] = hi;
-  }
-  __syncthreads();
-  const long long item_lo = range_sh[0], item_hi = range_sh[1];
-  if (tid == 0) {
-    const long long q0 = item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
-    item_sh[0] = q0;
-    if (q0 < item_hi) issue(q0, 0);
-  }
-  __syncthreads();
-
-  long long q = item_sh[0];
-  uint32_t phase = 0;  // bit b = parity of buffer b's next completion
+  UnitInfo cur;
+  long long u = next_unit(u_lo, cur, true);
+  if (u < u_hi) issue(cur, 0);
   int it = 0;
-  while (q < item_hi) {
-    const int cur = (G::NBUF == 2) ? (it & 1) : 0;
-    if (tid == 0) {
-      const long long qn = item_lo + (long long)atomicAdd(args.work_ctr, 1ull);
-      item_sh[(it + 1) & 1] = qn;
-      if (G::NBUF == 2 && qn < item_hi) issue(qn, cur ^ 1);
-    }
-    int a, b;
-    item_tiles(args, q, T, a, b);
-    const int na = (int)min((int64_t)TILE, n - (int64_t)a * TILE);
-    const int nb = (int)min((int64_t)TILE, n - (int64_t)b * TILE);
+  int la = -1, llb = -1;  // lane block held in registers
+  Lanes<D, KP> L;
+  bool lvalid[KP];
+  uint32_t lcnt[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    lvalid[k] = false;
+    lcnt[k] = 0u;
+  }
+  unsigned long long units_done = 0;
 
-    // ---- work units: (lane block of 32*KP points) x (32-column group) ------------
-    // LB = NTH/32 lane blocks x WPR column groups. A unit is inactive when its
-    // columns are past the ragged end or (SAFE, d <= 4, culling on) the union box
-    // of the lane block and the 32-point column block are provably out of range
-    // (the bound of keep_item, evaluated in float with a 1e-5 relative and a 4x
-    // rounding-error margin). Active units are split evenly across the warps, so
-    // a warp whose own points are far from tile b still does its share.
-    constexpr int LB = NTH / 32;
-    constexpr int NU = LB * WPR;
-    constexpr bool kBlockSkip = SAFE && D <= 4;
-    const bool block_skip = kBlockSkip && args.blk != nullptr;
-    mbar_wait(&mbar[cur], (phase >> cur) & 1u);
-    phase ^= (1u << cur);
-    const float* bcb = bc + (size_t)cur * TILE * S;
-    for (int u = tid; u < NU; u += NTH) {
-      const int lb = u / WPR, jw = u % WPR;
-      bool active = jw * 32 < nb && lb * 32 * KP < na;
-      if (kBlockSkip && block_skip && active) {
-        constexpr int BS = 2 * D + 1;
-        const float* cb = args.blk + (size_t)(b * (TILE / 32) + jw) * BS;
-        const float* lbb = args.blk + (size_t)(a * (TILE / 32) + lb * KP) * BS;
-        float L = 0.f, wn = 0.f;
+  auto flush = [&]() {
+    if (la < 0) return;
 #pragma unroll
-        for (int q = 0; q < D; ++q) {
-          float lo = INFINITY, hi = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < KP; ++k) {
-            lo = fminf(lo, __ldg(lbb + k * BS + q));
-            hi = fmaxf(hi, __ldg(lbb + k * BS + D + q));
-          }
-          const float g = fmaxf(0.f, fmaxf(__ldg(cb + q) - hi, lo - __ldg(cb + D + q)));
-          L += g * g;
-        }
-#pragma unroll
-        for (int k = 0; k < KP; ++k) wn = fmaxf(wn, __ldg(lbb + k * BS + 2 * D));
-        float bound = L * (1.0f - 1e-5f);
-        if (F == DS_FORMULA_ALGEBRAIC)
-          bound -= 4.0f * (2.0f * D + 3.0f) * 5.97e-8f * (wn + __ldg(cb + 2 * D)) * 1.01f;
-        active = !(bound > eps32);  // NaN keeps the unit
-      }
-      unit_active[u] = active ? 1 : 0;
+    for (int k = 0; k < KP; ++k) {
+      if (lcnt[k]) atomicAdd(&A.cnt[la * TILE + (llb * 32 + lane) * KP + k], (int)lcnt[k]);
+      lcnt[k] = 0u;
     }
-    __syncthreads();
-    if (tid < 32 && NU > 0) {
-      // compact the active units in (lane block, column group) order
-      int cnt_total = 0;
-      for (int u0 = 0; u0 < NU; u0 += 32) {
-        const bool act = (u0 + tid < NU) && unit_active[u0 + tid];
-        const uint32_t bal = __ballot_sync(0xffffffffu, act);
-        if (act) unit_list[cnt_total + __popc(bal & ((1u << tid) - 1u))] = (uint16_t)(u0 + tid);
-        cnt_total += __popc(bal);
-      }
-      if (tid == 0) unit_count = cnt_total;
-    }
-    __syncthreads();
-    const int nact = unit_count;
-    const int warp = tid >> 5;
-    // zero the rows of inactive units (their words are 0)
-    for (int u = warp; u < NU; u += LB) {
-      if (unit_active[u]) continue;
-      const int lb = u / WPR, jw = u % WPR;
-#pragma unroll
-      for (int k = 0; k < KP; ++k) bits[jw * BSTRIDE + k * NTH + lb * 32 + lane] = 0u;
-    }
+  };
 
-    uint32_t any = 0;
-    uint32_t groups = 0;
-    int cur_lb = -1;
-    Lanes<D, KP> L;
-    bool lvalid[KP];
-    const int u_lo = nact * warp / LB, u_hi = nact * (warp + 1) / LB;
-    for (int ui = u_lo; ui < u_hi; ++ui) {
-      const int u = unit_list[ui];
-      const int lb = u / WPR, jw = u % WPR;
-      if (lb != cur_lb) {  // (re)load the lane block's points into registers
-        cur_lb = lb;
+  while (u < u_hi) {
+    const int buf = it & 1;
+    __syncwarp();  // every lane is done reading the other buffer
+    UnitInfo nxt;
+    const long long un = next_unit(u + 1, nxt, false);
+    if (un < u_hi) issue(nxt, buf ^ 1);
+
+    if (cur.a != la || cur.lb != llb) {  // (re)load the lane block into registers
+      flush();
+      la = cur.a;
+      llb = cur.lb;
+      const int na = min(TILE, n - la * TILE);
 #pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          const int il = (lb * 32 + lane) * KP + k;  // 32*KP consecutive points per block
-          lvalid[k] = il < na;
-          const int64_t i = (int64_t)a * TILE + (lvalid[k] ? il : 0);
-          const float4* r4 = reinterpret_cast<const float4*>(args.rec + (size_t)i * S);
-          float tmp[S];
-#pragma unroll
-          for (int v = 0; v < S / 4; ++v) {
-            const float4 x = __ldg(r4 + v);
-            tmp[4 * v + 0] = x.x;
-            tmp[4 * v + 1] = x.y;
-            tmp[4 * v + 2] = x.z;
-            tmp[4 * v + 3] = x.w;
-          }
-          float c[D];
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-            c[q] = (F == DS_FORMULA_ALGEBRAIC) ? __fadd_rn(tmp[q], tmp[q]) : -tmp[q];
-#pragma unroll
-          for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
-          L.v1[k] = c[D - 1];
-          L.t[k] = tmp[D];
-        }
-      }
-      ++groups;
-      uint32_t acc[KP];
-#pragma unroll
-      for (int k = 0; k < KP; ++k) acc[k] = 0;
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        const float4* p4 = reinterpret_cast<const float4*>(bcb + (size_t)(jw * 32 + jj) * S);
-        float xj[S];
+      for (int k = 0; k < KP; ++k) {
+        const int il = (llb * 32 + lane) * KP + k;  // 32*KP consecutive points per block
+        lvalid[k] = il < na;
+        const int i = la * TILE + (lvalid[k] ? il : 0);
+        const float4* r4 = reinterpret_cast<const float4*>(A.rec + (size_t)i * S);
+        float tmp[S];
 #pragma unroll
         for (int v = 0; v < S / 4; ++v) {
-          const float4 x = p4[v];
-          xj[4 * v + 0] = x.x;
-          xj[4 * v + 1] = x.y;
-          xj[4 * v + 2] = x.z;
-          xj[4 * v + 3] = x.w;
+          const float4 x = __ldg(r4 + v);
+          tmp[4 * v + 0] = x.x;
+          tmp[4 * v + 1] = x.y;
+          tmp[4 * v + 2] = x.z;
+          tmp[4 * v + 3] = x.w;
         }
-        float d2[KP];
-        eval_d2<D, F, KP>(L, xj, xj[D], d2);
-        pack_bits<KP, SAFE>(d2, eps32, jj, acc);
-      }
-      const uint32_t vm = valid_mask(nb - jw * 32);
+        float c[D];
 #pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        const uint32_t w = lvalid[k] ? ((k < KC ? acc[k] : ~acc[k]) & vm) : 0u;
-        bits[jw * BSTRIDE + k * NTH + lb * 32 + lane] = w;
-        any |= w;
+        for (int q = 0; q < D; ++q)
+          c[q] = (F == DS_FORMULA_ALGEBRAIC) ? __fadd_rn(tmp[q], tmp[q]) : -tmp[q];
+#pragma unroll
+        for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
+        L.v1[k] = c[D - 1];
+        L.t[k] = tmp[D];
       }
     }
 
-    // ---- epilogue --------------------------------------------------------------
-    if (lane == 0 && groups)  // pairs actually evaluated: groups x 32 columns x 32*KP lane points
-      atomicAdd(args.pairs_done, (unsigned long long)groups * 32ull * 32ull * KP);
-    const int any_all = __syncthreads_or(any != 0);
-    if (any_all) {  // lane-side counts: popcount of each row's active words (slot k*NTH + tid)
+    if (un < u_hi) cp_async_wait<1>();  // this unit's group is complete
+    else cp_async_wait<0>();
+    __syncwarp();
+    const float* st = stage + (size_t)buf * G::STAGE;
+    uint32_t acc[KP];
 #pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        uint32_t cnt_k = 0;
+    for (int k = 0; k < KP; ++k) acc[k] = 0u;
+    // full unroll for d <= 4; wider records unroll by 8 to keep the independent
+    // warps' code inside the instruction cache
+#pragma unroll(G::UNROLL)
+    for (int jj = 0; jj < 32; ++jj) {
+      const float4* p4 = reinterpret_cast<const float4*>(st + jj * S);
+      float xj[S];
 #pragma unroll
-        for (int jw = 0; jw < WPR; ++jw)
-          if (unit_active[warp * WPR + jw]) cnt_k += __popc(bits[jw * BSTRIDE + k * NTH + tid]);
-        if (cnt_k) atomicAdd(&args.cnt[(int64_t)a * TILE + tid * KP + k], (int)cnt_k);
+      for (int v = 0; v < S / 4; ++v) {
+        const float4 x = p4[v];
+        xj[4 * v + 0] = x.x;
+        xj[4 * v + 1] = x.y;
+        xj[4 * v + 2] = x.z;
+        xj[4 * v + 3] = x.w;
       }
+      float d2[KP];
+      eval_d2<D, F, KP>(L, xj, xj[D], d2);
+      pack_bits<KP, SAFE>(d2, eps32, jj, acc);
     }
+    ++units_done;
 
-    if (any_all) {
-      const int w = tid / G::CHUNKS;   // word column handled by this thread
-      const int c = tid % G::CHUNKS;   // row chunk: slots c, c + CHUNKS, ...
-      const uint32_t* col = bits + w * BSTRIDE + c;
-      // slots c + CHUNKS*r for r in [r0, r0 + SEG) all belong to one lane block, so
-      // an inactive (lane block, w) unit skips SEG rows at once
-      constexpr int SEG = 32 / G::CHUNKS;
-
-      // pass 1: staged-side counts (vertical popcount of word column w) and the
-      // number of words to append (upper triangle only on the diagonal tile)
-      uint32_t s[10];
+    const int nb = min(TILE, n - cur.b * TILE);
+    const uint32_t vm = valid_mask(nb - cur.jw * 32);
+    uint32_t w[KP];
+    uint32_t any = 0u;
 #pragma unroll
-      for (int l = 0; l < 10; ++l) s[l] = 0;
-      uint32_t nz = 0;
-      for (int r0 = 0; r0 < G::ROWS; r0 += SEG) {
-        const int lb0 = ((c + r0 * G::CHUNKS) % NTH) / 32;
-        if (!unit_active[lb0 * WPR + w]) continue;
+    for (int k = 0; k < KP; ++k) {
+      w[k] = lvalid[k] ? ((k < KC ? acc[k] : ~acc[k]) & vm) : 0u;
+      lcnt[k] += __popc(w[k]);
+      any |= w[k];
+    }
+    unsigned long long base = 0;
+    int total = 0;
+    if (__any_sync(0xffffffffu, any != 0u)) {
+      if (!cur.self) {
+        const uint32_t v = column_counts<KP>(w, lane);
+        if (v) atomicAdd(&A.cnt[cur.b * TILE + cur.jw * 32 + lane], (int)v);
+      } else {
 #pragma unroll
-        for (int r = r0; r < r0 + SEG; ++r) {
-          uint32_t x = col[r * G::CHUNKS];
-          if (!x) continue;
-          if (a != b) {
-            uint32_t carry = x;
-#pragma unroll
-            for (int l = 0; l < G::SL0; ++l) {
-              const uint32_t t2 = s[l] & carry;
-              s[l] ^= carry;
-              carry = t2;
-            }
-          } else {
-            const int p = c + r * G::CHUNKS;  // smem slot -> point (slot k*NTH + t holds t*KP + k)
-            const int il = (p % NTH) * KP + p / NTH;
-            x &= diag_keep(il - w * 32);      // keep columns t >= row
-          }
-          nz += (x != 0);
-        }
+        for (int k = 0; k < KP; ++k)  // keep columns j >= row (incl. the self pair)
+          w[k] &= diag_keep((llb * 32 + lane) * KP + k - cur.jw * 32);
       }
-      if (a != b) {
+      // append the unit's non-zero words (one warp-aggregated atomic)
+      int nz = 0;
 #pragma unroll
-        for (int off = 1; off < G::CHUNKS; off <<= 1) {
-          uint32_t o[10];
-#pragma unroll
-          for (int l = 0; l < 10; ++l) o[l] = __shfl_xor_sync(0xffffffffu, s[l], off);
-          sliced_add(s, o);
-        }
-        constexpr int PER = 32 / G::CHUNKS;
-#pragma unroll
-        for (int qq = 0; qq < PER; ++qq) {
-          const int p = c * PER + qq;  // bit position
-          uint32_t v = 0;
-#pragma unroll
-          for (int l = 0; l < 10; ++l) v |= ((s[l] >> p) & 1u) << l;
-          if (v) atomicAdd(&args.cnt[(int64_t)b * TILE + w * 32 + (31 - p)], (int)v);
-        }
-      }
-
-      uint32_t incl = nz;
+      for (int k = 0; k < KP; ++k) nz += w[k] != 0u;
+      int incl = nz;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += y;
       }
-      if (lane == 31) scan_sh[tid >> 5] = incl;
-      __syncthreads();
-      if (tid == 0) {
-        unsigned int run = 0;
-        for (int wi = 0; wi < NTH / 32; ++wi) {
-          const unsigned int t2 = scan_sh[wi];
-          scan_sh[wi] = run;
-          run += t2;
-        }
-        base_sh = run ? atomicAdd(args.words_count, (unsigned long long)run) : 0ull;
-        if (run) {
-          // one chunk per non-empty tile pair: its words are contiguous
-          const unsigned long long ci = atomicAdd(args.nonempty_count, 1ull);
-          if (ci < args.chunks_cap)
-            args.chunks[ci] = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)base_sh,
-                                         run | ((uint32_t)(base_sh >> 32) << 16));
-        }
-      }
-      __syncthreads();
-      // pass 2: append the words
-      unsigned long long pos = base_sh + scan_sh[tid >> 5] + (incl - nz);
-      if (nz) {
-        for (int r0 = 0; r0 < G::ROWS; r0 += SEG) {
-          const int lb0 = ((c + r0 * G::CHUNKS) % NTH) / 32;
-          if (!unit_active[lb0 * WPR + w]) continue;
+      total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) base = atomicAdd(A.words_count, (unsigned long long)total);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      unsigned long long pos = base + (unsigned long long)(incl - nz);
 #pragma unroll
-          for (int r = r0; r < r0 + SEG; ++r) {
-            uint32_t x = col[r * G::CHUNKS];
-            if (!x) continue;
-            const int p = c + r * G::CHUNKS;
-            const int il = (p % NTH) * KP + p / NTH;
-            if (a == b) x &= diag_keep(il - w * 32);
-            if (x) {
-              if (pos < args.words_cap) args.words[pos] = make_uint2(x, (uint32_t)(il << 4 | w));
-              ++pos;
-            }
-          }
+      for (int k = 0; k < KP; ++k) {
+        if (w[k]) {
+          if (pos < A.words_cap)
+            A.words[pos] = make_uint2(w[k], (uint32_t)(((llb * 32 + lane) * KP + k) << 4 | cur.jw));
+          ++pos;
         }
       }
     }
-    __syncthreads();
-    const long long qn = item_sh[(it + 1) & 1];
-    if (G::NBUF == 1 && tid == 0 && qn < item_hi) issue(qn, 0);
-    q = qn;
+    if (lane == 0)
+      A.uchunks[u] = make_uint2((uint32_t)base, (uint32_t)total | ((uint32_t)(base >> 32) << 16));
+
+    u = un;
+    cur = nxt;
     ++it;
+  }
+  flush();
+  if (lane == 0 && units_done)
+    atomicAdd(A.pairs_done, units_done * 32ull * 32ull * (unsigned long long)KP);
+}
+
+// ---- culled schedule: unit list ------------------------------------------------------
+// Unit (lb, jw) of kept tile pair (a, b) is kept unless it is structurally empty
+// (UnitCursor's skip) or, for d <= 4, the union box of its lane block and the box
+// of its column block are provably out of range: the bound of keep_item, in double,
+// on the 32-point block boxes (block_bounds_kernel).
+__device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpad, int64_t n, int KP,
+                                          int a, int b, int lb, int jw, float eps32, int formula,
+                                          bool unsafe) {
+  const int64_t na = min((int64_t)TILE, n - (int64_t)a * TILE);
+  const int64_t nb = min((int64_t)TILE, n - (int64_t)b * TILE);
+  if (jw * 32 >= nb || lb * 32 * KP >= na) return false;
+  if (a == b && jw < lb * KP) return false;
+  if (unsafe || !blk || (a == b && jw < (lb + 1) * KP)) return true;
+  const int BS = 2 * dpad + 1;
+  const int64_t nblk = (n + 31) / 32;
+  const float* cb = blk + ((int64_t)b * WPR + jw) * BS;
+  const int64_t l0 = (int64_t)a * WPR + (int64_t)lb * KP;
+  const int kl = (int)min((int64_t)KP, nblk - l0);
+  const double u = 1.0 / 16777216.0;
+  double L = 0.0, wn = (double)cb[2 * dpad];
+  for (int k = 0; k < kl; ++k) wn = fmax(wn, (double)blk[(l0 + k) * BS + 2 * dpad]);
+  for (int q = 0; q < dpad; ++q) {
+    float lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < kl; ++k) {
+      lo = fminf(lo, blk[(l0 + k) * BS + q]);
+      hi = fmaxf(hi, blk[(l0 + k) * BS + dpad + q]);
+    }
+    const double g = fmax(0.0, fmax((double)cb[q] - (double)hi, (double)lo - (double)cb[dpad + q]));
+    L += g * g;
+  }
+  double bound = L * (1.0 - 4.0 * 3.0 * dpad * u) * (1.0 - 1e-12);
+  if (formula == DS_FORMULA_ALGEBRAIC) bound -= 4.0 * (2.0 * dpad + 3.0) * u * wn * 2.0 * 1.001;
+  return !(bound > (double)eps32);  // NaN bounds keep the unit
+}
+
+// pass 1: units per kept item (warp per item); items past the kept count get 0
+__global__ void unit_count_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
+                                  float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
+                                  const uint32_t* __restrict__ items,
+                                  const unsigned long long* __restrict__ kept, int64_t all_items,
+                                  int32_t* __restrict__ ucnt) {
+  const int64_t K = (int64_t)*kept;
+  const bool unsafe = *unsafe_flag != 0;
+  const int upt = (TILE / (32 * KP)) * WPR;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = K + tid; q < all_items; q += nth) ucnt[q] = 0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = tid >> 5; q < K; q += nth >> 5) {
+    const uint32_t ab = items[q];
+    const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
+    int c = 0;
+    for (int s0 = 0; s0 < upt; s0 += 32) {
+      const int sub = s0 + lane;
+      const bool keep = unit_keep(blk, dpad, n, KP, a, b, sub / WPR, sub % WPR, eps32, formula, unsafe);
+      c += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (lane == 0) ucnt[q] = c;
+  }
+}
+
+// pass 3: scatter {item, sub} at the scanned offsets (deterministic, item order)
+__global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
+                                    float eps32, int formula,
+                                    const uint32_t* __restrict__ unsafe_flag,
+                                    const uint32_t* __restrict__ items,
+                                    const unsigned long long* __restrict__ kept,
+                                    const int32_t* __restrict__ off, const int32_t* __restrict__ total,
+                                    uint2* __restrict__ list, unsigned long long cap,
+                                    unsigned long long* __restrict__ count) {
+  const int64_t K = (int64_t)*kept;
+  const bool unsafe = *unsafe_flag != 0;
+  const int upt = (TILE / (32 * KP)) * WPR;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) *count = (unsigned long long)*total;
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = tid >> 5; q < K; q += nth >> 5) {
+    const uint32_t ab = items[q];
+    const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
+    unsigned long long pos = (unsigned long long)off[q];
+    for (int s0 = 0; s0 < upt; s0 += 32) {
+      const int sub = s0 + lane;
+      const bool keep = unit_keep(blk, dpad, n, KP, a, b, sub / WPR, sub % WPR, eps32, formula, unsafe);
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      const unsigned long long p = pos + __popc(bal & ((1u << lane) - 1u));
+      if (keep && p < cap) list[p] = make_uint2(ab, (uint32_t)sub);
+      pos += __popc(bal);
+    }
+  }
+}
+
+// ---- directory of tile pairs with words (for the union kernels) ------------------
+template <int KP>
+__global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32_t* __restrict__ item_off,
+                                const unsigned long long* __restrict__ kept, uint4* __restrict__ dir,
+                                unsigned long long* __restrict__ dir_count) {
+  constexpr int UPT = (TILE / (32 * KP)) * WPR;
+  long long U = A.dense_units;
+  int64_t K = all_items;
+  if (A.unit_list) {
+    const unsigned long long c = *A.unit_count;
+    U = (long long)(c < A.units_cap ? c : A.units_cap);
+    K = (int64_t)*kept;
+  }
+  const long long r_lo = U * A.shard_rank / A.shard_world;
+  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < K; q += nwarps) {
+    long long lo, hi;
+    if (A.unit_list) {
+      lo = item_off[q];
+      hi = q + 1 < all_items ? (long long)item_off[q + 1] : (long long)*A.unit_count;
+      if (q + 1 == K) hi = (long long)*A.unit_count;
+    } else {
+      lo = q * UPT;
+      hi = lo + UPT;
+    }
+    lo = lo > r_lo ? lo : r_lo;
+    hi = hi < r_hi ? hi : r_hi;
+    if (lo >= hi) continue;
+    uint32_t words = 0;
+    for (long long u = lo + lane; u < hi; u += 32) words += A.uchunks[u].y & 0xffffu;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) words += __shfl_xor_sync(0xffffffffu, words, off);
+    if (lane == 0 && words) {
+      int a, b;
+      if (A.item_list) {
+        const uint32_t ab = A.item_list[q];
+        a = (int)(ab >> 16);
+        b = (int)(ab & 0xffffu);
+      } else {
+        decode_item(q, A.T, a, b);
+      }
+      const unsigned long long ci = atomicAdd(dir_count, 1ull);
+      dir[ci] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)lo, (uint32_t)(hi - lo),
+                           (uint32_t)((unsigned long long)lo >> 32));
+    }
   }
 }
 
@@ -779,9 +855,9 @@ int pad_dim(int d) {
 }
 
 template <int D, int F, bool SAFE>
-cudaError_t launch_one(const TileArgs& a, int sm_count, cudaStream_t s) {
+cudaError_t launch_one(const UnitArgs& a, int sm_count, cudaStream_t s) {
   using G = Geo<D>;
-  auto kern = eps_tile_kernel<D, F, SAFE>;
+  auto kern = eps_unit_kernel<D, F, SAFE>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
@@ -793,11 +869,7 @@ cudaError_t launch_one(const TileArgs& a, int sm_count, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
-  const int64_t items = a.item_list ? (int64_t)1 << 40 : a.item_hi - a.item_lo;
-  int64_t grid = (int64_t)sm_count * per_sm;
-  if (grid > items) grid = items;
-  if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, G::THREADS, G::SMEM, s>>>(a);
+  kern<<<(unsigned)(sm_count * per_sm), G::THREADS, G::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -805,14 +877,14 @@ cudaError_t launch_one(const TileArgs& a, int sm_count, cudaStream_t s) {
 // the prep kernel and the one that does not own the input exits immediately, so
 // the host never waits for the range check.
 template <int D, int F>
-cudaError_t launch_df(const TileArgs& a, int sm_count, cudaStream_t s) {
+cudaError_t launch_df(const UnitArgs& a, int sm_count, cudaStream_t s) {
   cudaError_t e = launch_one<D, F, true>(a, sm_count, s);
   if (e != cudaSuccess) return e;
   return launch_one<D, F, false>(a, sm_count, s);
 }
 
 template <int D>
-cudaError_t launch_d(const TileArgs& a, int formula, int sm_count, cudaStream_t s) {
+cudaError_t launch_d(const UnitArgs& a, int formula, int sm_count, cudaStream_t s) {
   return formula == DS_FORMULA_ALGEBRAIC ? launch_df<D, DS_FORMULA_ALGEBRAIC>(a, sm_count, s)
                                          : launch_df<D, DS_FORMULA_DIRECT>(a, sm_count, s);
 }
@@ -820,19 +892,6 @@ cudaError_t launch_d(const TileArgs& a, int formula, int sm_count, cudaStream_t 
 }  // namespace
 
 int padded_dim(int d) { return pad_dim(d); }
-
-size_t tile_smem_bytes(int d) {
-  switch (pad_dim(d)) {
-    case 1: return Geo<1>::SMEM;
-    case 2: return Geo<2>::SMEM;
-    case 3: return Geo<3>::SMEM;
-    case 4: return Geo<4>::SMEM;
-    case 8: return Geo<8>::SMEM;
-    case 16: return Geo<16>::SMEM;
-    case 32: return Geo<32>::SMEM;
-    default: return Geo<64>::SMEM;
-  }
-}
 
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
                         cudaStream_t s) {
@@ -872,8 +931,9 @@ cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream_t s) {
-  switch (pad_dim(a.d)) {
+cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
+                                cudaStream_t s) {
+  switch (pad_dim(d)) {
     case 1: return launch_d<1>(a, formula, sm_count, s);
     case 2: return launch_d<2>(a, formula, sm_count, s);
     case 3: return launch_d<3>(a, formula, sm_count, s);
@@ -883,6 +943,47 @@ cudaError_t launch_tile(const TileArgs& a, int formula, int sm_count, cudaStream
     case 32: return launch_d<32>(a, formula, sm_count, s);
     default: return launch_d<64>(a, formula, sm_count, s);
   }
+}
+
+cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, int formula,
+                             const uint32_t* unsafe_flag, const uint32_t* item_list,
+                             const unsigned long long* kept, int64_t all_items, int32_t* ucnt,
+                             int32_t* partials, int32_t* total32, uint2* unit_list,
+                             unsigned long long units_cap, unsigned long long* unit_count,
+                             cudaStream_t s) {
+  const int dp = pad_dim(d);
+  const int KP = unit_kp(d);
+  const float* box = dp <= 4 ? blk : nullptr;  // block boxes only pay off in low dimension
+  int64_t blocks = (all_items * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  unit_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
+                                                     item_list, kept, all_items, ucnt);
+  cudaError_t e = launch_exclusive_scan(ucnt, all_items, partials, total32, s);
+  if (e != cudaSuccess) return e;
+  unit_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
+                                                       item_list, kept, ucnt, total32, unit_list,
+                                                       units_cap, unit_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const int32_t* item_off,
+                            const unsigned long long* kept, uint4* dir,
+                            unsigned long long* dir_count, cudaStream_t s) {
+  int64_t blocks = (all_items * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  switch (unit_kp(d)) {
+    case 4:
+      unit_dir_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+      break;
+    case 2:
+      unit_dir_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+      break;
+    default:
+      unit_dir_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace ds

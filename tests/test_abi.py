@@ -88,15 +88,16 @@ def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
     """Parity needs every product and sum rounded separately: the eps-tile
     kernels must contain no FFMA/FFMA2 (ptxas would otherwise be free to fuse
     packed mul+add, SURVEY §0 finding 4), and they must use the packed FP32
-    instructions and the TMA bulk copy the design relies on."""
+    instructions and the asynchronous shared-memory staging (cp.async ->
+    LDGSTS) the design relies on."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True,
                           check=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
-    tile = [f for f in funcs if f.startswith("_ZN2ds") and "eps_tile_kernel" in f.split("\n")[0]]
+    tile = [f for f in funcs if f.startswith("_ZN2ds") and "eps_unit_kernel" in f.split("\n")[0]]
     assert len(tile) >= 16
     for body in tile:
         name = body.split("\n")[0]
         assert not re.search(r"\bFFMA2?\b", body), name
-    k2 = [f for f in tile if "eps_tile_kernelILi2ELi1ELb1E" in f.split("\n")[0]]
+    k2 = [f for f in tile if "eps_unit_kernelILi2ELi1ELb1E" in f.split("\n")[0]]
     assert k2 and "FMUL2" in k2[0] and "FADD2" in k2[0]
-    assert "UBLKCP" in k2[0] or "UTMALDG" in k2[0]
+    assert "LDGSTS" in k2[0]

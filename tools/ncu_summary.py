@@ -82,15 +82,31 @@ def report(path):
         out.append((name, vals, top))
     src = ncu_csv(["-i", path, "--page", "source", "--csv", "--print-source", "sass"])
     hot = []
-    if len(src) > 2:
-        h = src[1]
-        if "Warp Stall Sampling (All Samples)" in h:
-            i_s = h.index("Warp Stall Sampling (All Samples)")
-            i_src = h.index("Source")
-            data = [r for r in src[2:] if len(r) == len(h)]
-            tot = sum(float(r[i_s] or 0) for r in data) or 1.0
-            for r in sorted(data, key=lambda r: -float(r[i_s] or 0))[:10]:
-                hot.append(f"{float(r[i_s]) / tot * 100:5.1f}%  {r[i_src].strip()[:90]}")
+    # one section per profiled kernel, each starting with its own header row
+    sections, h = [], None
+    for r in src:
+        if "Warp Stall Sampling (All Samples)" in r:
+            h = r
+            sections.append((h, []))
+        elif h is not None and len(r) == len(h):
+            sections[-1][1].append(r)
+    for si, (h, data) in enumerate(sections):
+        i_s = h.index("Warp Stall Sampling (All Samples)")
+        i_src = h.index("Source")
+
+        def val(r):
+            try:
+                return float(r[i_s] or 0)
+            except ValueError:
+                return 0.0
+
+        tot = sum(val(r) for r in data)
+        if tot <= 0:
+            continue
+        if len(sections) > 1:
+            hot.append(f"-- kernel {si} --")
+        for r in sorted(data, key=lambda r: -val(r))[:12]:
+            hot.append(f"{val(r) / tot * 100:5.1f}%  {r[i_src].strip()[:90]}")
     return out, hot
 
 
