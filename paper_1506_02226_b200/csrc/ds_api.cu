@@ -206,6 +206,9 @@ cudaError_t record(ds_ctx* c, cudaEvent_t e, cudaStream_t s) {
                       : cudaEventRecord(e, s);
 }
 
+// device bytes per row unit: chunk entries (WPR x 8 B) + the culled list entry (8 B)
+inline size_t unit_bytes(bool cull) { return (size_t)WPR * 8 + (cull ? 8 : 0); }
+
 struct Plan {
   int64_t T = 0, all_items = 0, item_lo = 0, item_hi = 0, dense_units = 0;
   unsigned long long units_cap = 0;
@@ -241,18 +244,18 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   pl.item_lo = pl.all_items * rank / world;
   pl.item_hi = pl.all_items * (rank + 1) / world;
   const int64_t T = pl.T;
-  const int upt = units_per_tile(d);
-  pl.dense_units = pl.all_items * upt;
-  if (pl.cull) {  // unit list + chunk table sized from earlier calls (lazy, like the words)
-    const unsigned long long guess = (unsigned long long)n / 2 + 4096;
+  pl.dense_units = pl.all_items * lane_blocks(d);
+  if (pl.cull) {  // row-unit list + chunk table sized from earlier calls (lazy, like the words)
+    const unsigned long long guess = (unsigned long long)n / 8 + 4096;
     pl.units_cap = std::max<unsigned long long>(c->units_cap, guess);
   } else {
     pl.units_cap = (unsigned long long)pl.dense_units;
   }
-  pl.base = base_bytes(n, d) + (size_t)pl.units_cap * (pl.cull ? 16 : 8);
+  pl.base = base_bytes(n, d) + (size_t)pl.units_cap * unit_bytes(pl.cull);
 
-  unsigned long long want =
-      std::max<unsigned long long>(c->words_cap, (unsigned long long)n * 8 + (1ull << 20));
+  const unsigned long long run_slack = (unsigned long long)c->sm_count * 16 * WORD_RUN;
+  unsigned long long want = std::max<unsigned long long>(
+      c->words_cap, (unsigned long long)n * 8 + (1ull << 20) + run_slack);
   if (mem_cap > 0) {
     const int64_t room = mem_cap - (int64_t)pl.base;
     if (room < 16 * 1024) {
@@ -323,6 +326,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.shard_world = world;
   a.unsafe_flag = &sc->unsafe_flag;
   a.pairs_done = &sc->pairs_done;
+  a.work_ctr = &sc->work_ctr;
   a.unit_list = nullptr;
   if (pl.cull) {
     const int dp = padded_dim(d);
@@ -337,7 +341,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
                            (uint2*)c->ulist.p, pl.units_cap, &sc->unit_count, s));
     a.unit_list = (const uint2*)c->ulist.p;
   }
-  DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * 8));
+  DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * WPR * 8));
   a.uchunks = (uint2*)c->uchunks.p;
   DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
@@ -354,7 +358,7 @@ ds_status check_words(ds_ctx* c, const Plan& pl, int64_t mem_cap, bool* retry) {
   if (pl.cull && c->h_scalars->unit_count > pl.units_cap) {  // unit list overflowed: grow, re-run
     const unsigned long long nu = c->h_scalars->unit_count;
     const unsigned long long grow = nu + nu / 16 + 1024;
-    const int64_t required = (int64_t)(pl.base + (grow - pl.units_cap) * 16);
+    const int64_t required = (int64_t)(pl.base + (grow - pl.units_cap) * unit_bytes(true));
     if (mem_cap > 0 && required > mem_cap) {
       set_capacity(required, mem_cap);
       set_error("work-unit list exceeds the memory cap");
@@ -364,9 +368,12 @@ ds_status check_words(ds_ctx* c, const Plan& pl, int64_t mem_cap, bool* retry) {
     *retry = true;
     return DS_OK;
   }
-  const unsigned long long need = c->h_scalars->words_count;
+  const unsigned long long need = c->h_scalars->words_count;  // reserved slots (runs)
   if (need <= c->words_cap) return DS_OK;
-  const unsigned long long grow = need + need / 16 + 1024;
+  // reservations of a re-run differ only by warp scheduling (need >= words); +25% and
+  // a run per resident warp covers that in practice, another overflow re-runs again
+  const unsigned long long grow =
+      need + need / 4 + (unsigned long long)c->sm_count * 16 * WORD_RUN + 1024;
   const int64_t required = (int64_t)(pl.base + grow * WORD_BYTES);
   if (mem_cap > 0 && required > mem_cap) {
     set_capacity((int64_t)(pl.base + need * WORD_BYTES), mem_cap);
@@ -459,9 +466,9 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       pl.cull = c->cull != 0 && pl.T > 1;
       pl.item_lo = 0;
       pl.item_hi = pl.all_items;
-      pl.dense_units = pl.all_items * units_per_tile(d);
+      pl.dense_units = pl.all_items * lane_blocks(d);
       pl.units_cap = pl.cull ? c->units_cap : (unsigned long long)pl.dense_units;
-      pl.base = base_bytes(n, d) + (size_t)pl.units_cap * (pl.cull ? 16 : 8);
+      pl.base = base_bytes(n, d) + (size_t)pl.units_cap * unit_bytes(pl.cull);
     } else if (c->use_graph && std::memcmp(key, c->seen_key, sizeof key) == 0) {
       // second call with this key: record the device pipeline and replay it
       if (c->gexec) {

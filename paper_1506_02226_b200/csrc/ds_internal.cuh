@@ -44,11 +44,20 @@ inline int64_t n_items(int64_t T) { return T * (T + 1) / 2; }
 // arithmetic (|d2| <= 4*d*max|c|^2); such inputs take the compare-based path
 constexpr float SAFE_ABS = 1.0e17f;
 
-// Work unit of the eps-tile kernel: (a block of 32*KP consecutive points of tile a,
-// held in registers by one warp) x (a block of 32 points of tile b, staged in
-// shared memory). KP = 4 / 2 / 1 lane points per lane for d <= 8 / 32 / 64.
-inline int unit_kp(int d) { return padded_dim(d) <= 8 ? 4 : (padded_dim(d) <= 32 ? 2 : 1); }
-inline int units_per_tile(int d) { return (TILE / (32 * unit_kp(d))) * WPR; }
+// Row unit of the eps-tile kernel: (a block of 32*KP consecutive points of tile a,
+// held in registers by one warp) x (a mask of the 32-point column blocks of tile b
+// it evaluates, staged through shared memory one block at a time). KP = 4 / 2 / 1
+// lane points per lane for d <= 8 / 32 / 64; each column block of a row unit owns
+// one chunk entry (unit * WPR + column block).
+inline int unit_kp(int d) { return padded_dim(d) <= 16 ? 4 : (padded_dim(d) <= 32 ? 2 : 1); }
+inline int lane_blocks(int d) { return TILE / (32 * unit_kp(d)); }
+// chunk entries per tile pair: one per (lane block, column block)
+inline int units_per_tile(int d) { return lane_blocks(d) * WPR; }
+// Each warp of the eps-tile kernel reserves adjacency-word slots WORD_RUN at a time
+// (one global atomic per run instead of one per unit); a unit emits at most 32*KP
+// <= 128 words, so a run's unused tail is < 128 slots. Bound on the reserved total:
+// words * WORD_RUN / (WORD_RUN - 128) + warps * WORD_RUN.
+constexpr int WORD_RUN = 256;
 
 struct UnitArgs {
   const float* rec;
@@ -59,15 +68,18 @@ struct UnitArgs {
   uint2* words;                         // {32-bit word, local row << 4 | column word}
   unsigned long long words_cap;
   unsigned long long* words_count;
-  uint2* uchunks;                       // per unit {first word lo, count | first word hi << 16}
+  uint2* uchunks;                       // per (unit, column block) {first word lo,
+                                        //   count | first word hi << 16}
   const uint32_t* item_list;            // culled tile pairs (a << 16 | b), or nullptr: triangle
-  const uint2* unit_list;               // culled units {item, sub}, or nullptr: q * UPT + sub
+  const uint2* unit_list;               // culled row units {a << 16 | b, lb << 16 | column mask},
+                                        // or nullptr: unit q * LB + lb of the triangle
   const unsigned long long* unit_count; // length of unit_list (device)
-  unsigned long long units_cap;         // capacity of unit_list / uchunks (culled)
-  int64_t dense_units;                  // all_items * UPT (dense schedule)
+  unsigned long long units_cap;         // capacity of unit_list (culled); uchunks: * WPR
+  int64_t dense_units;                  // all_items * LB (dense schedule)
   int32_t shard_rank, shard_world;      // slice of the units this launch evaluates
   const uint32_t* unsafe_flag;
   unsigned long long* pairs_done;       // ordered pairs evaluated (32 x 32*KP per unit)
+  unsigned long long* work_ctr;         // batch counter (zeroed before the launch)
 };
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------

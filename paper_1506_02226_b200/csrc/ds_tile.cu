@@ -185,15 +185,18 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
 // sign and x - x = +0), so the sign bit is exactly the out-of-range bit. Mixing
 // the two balances the FP32 and ALU pipes; SAFE=false (inputs whose squares can
 // overflow) compares every lane point.
-template <int KP, bool SAFE>
+// Measured on B200 (tools/tile_bench.py): d <= 4 runs best with 3 of 4 lane points
+// compared (the FP32 pipe is the tighter one there), wider records with all lane
+// points on the sign-bit path (the cross-product chain leaves the ALU idle).
+template <int KP, bool SAFE, int D>
 struct Pack {
-  static constexpr int KC = SAFE ? KP / 2 : KP;
+  static constexpr int KC = !SAFE ? KP : (D <= 4 ? (3 * KP) / 4 : 0);
 };
 
-template <int KP, bool SAFE>
+template <int KP, bool SAFE, int D>
 __device__ __forceinline__ void pack_bits(const float (&d2)[KP], float eps32, int jj,
                                           uint32_t (&acc)[KP]) {
-  constexpr int KC = Pack<KP, SAFE>::KC;
+  constexpr int KC = Pack<KP, SAFE, D>::KC;
 #pragma unroll
   for (int k = 0; k < KC; ++k) acc[k] |= (d2[k] <= eps32 ? 1u : 0u) << (31 - jj);
   if constexpr (KC < KP) {
@@ -214,14 +217,14 @@ __device__ __forceinline__ void pack_bits(const float (&d2)[KP], float eps32, in
 
 template <int D>
 struct Geo {
-  static constexpr int KP = D <= 8 ? 4 : (D <= 32 ? 2 : 1);  // lane points per lane
+  static constexpr int KP = D <= 16 ? 4 : (D <= 32 ? 2 : 1);  // lane points per lane
   static constexpr int S = ((D + 1) + 3) / 4 * 4;           // floats per record
   static constexpr int WARPS = 4;
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int STAGE = 32 * S;                       // floats per staged block
   static constexpr size_t SMEM = (size_t)WARPS * 2 * STAGE * 4;
   static constexpr int UNROLL = D <= 4 ? 32 : 8;
-  static constexpr int MINB = D <= 32 ? 4 : 3;  // 16 (d <= 32) or 12 resident warps per SM
+  static constexpr int MINB = (D <= 8 || D == 32) ? 4 : 3;  // 16 or 12 resident warps per SM
 };
 
 // Column-side counts of one unit: the number of set bits of every column over the
@@ -270,60 +273,32 @@ __device__ __forceinline__ uint32_t column_counts(const uint32_t (&w)[KP], int l
   return v;
 }
 
-// Unit -> (tile pair, lane block, column block); `self` = the column block lies
-// inside the lane block of a diagonal tile. Units that need no evaluation (ragged
-// tail, or below the diagonal of a diagonal tile: their pairs are covered by the
-// mirrored unit) report skip.
-struct UnitInfo {
+// ---- row units ---------------------------------------------------------------------
+// A row unit is (tile pair (a, b), lane block lb) plus a 16-bit mask of the column
+// blocks jw (32 points of tile b each) it evaluates. The warp holds the lane block
+// (32*KP consecutive points of tile a) in registers for the whole unit and streams
+// the masked column blocks through shared memory. Column block jw of unit u owns
+// chunk entry u * WPR + jw (its words), so a tile pair's words are the chunk entries
+// of its units. LB = TILE / (32*KP) lane blocks per tile.
+//
+// Structural mask: column blocks inside tile b (ragged tail) and, on a diagonal tile
+// (a == b), not entirely below the lane block — pairs below the diagonal are covered
+// by the mirrored unit. `self` column blocks (a == b, jw < (lb+1)*KP) overlap the
+// lane block and keep only j >= i.
+__device__ __forceinline__ uint32_t struct_mask(int n, int KP, int a, int b, int lb) {
+  const int na = min(TILE, n - a * TILE);
+  const int nb = min(TILE, n - b * TILE);
+  if (lb * 32 * KP >= na) return 0u;
+  const int nblk = (nb + 31) / 32;
+  uint32_t m = (1u << nblk) - 1u;  // nblk <= 16
+  if (a == b) m &= ~((1u << (lb * KP)) - 1u);
+  return m;
+}
+
+// One column-block step of a row unit.
+struct Step {
+  long long u;
   int a, b, lb, jw;
-  bool self, skip;
-};
-
-// Walks a warp's slice of the units. Culled schedule: one 8-byte list entry
-// {a << 16 | b, sub} per unit. Dense schedule: units are q * UPT + sub over the
-// upper triangle in row order, so only the slice start is decoded (decode_item);
-// later units step (sub, b, a) incrementally.
-template <int KP>
-struct UnitCursor {
-  static constexpr int UPT = (TILE / (32 * KP)) * WPR;
-  const uint2* list;
-  int T, n;
-  int a, b, sub;
-
-  __device__ __forceinline__ void start(const UnitArgs& A, long long u) {
-    list = A.unit_list;
-    T = A.T;
-    n = (int)A.n;
-    if (!list) {
-      const long long q = u / UPT;
-      sub = (int)(u - q * UPT);
-      decode_item(q, T, a, b);
-    }
-  }
-  // info of unit u (the previous call, if any, was for u - 1)
-  __device__ __forceinline__ UnitInfo get(long long u, bool first) {
-    if (list) {
-      const uint2 e = __ldg(list + u);
-      a = (int)(e.x >> 16);
-      b = (int)(e.x & 0xffffu);
-      sub = (int)e.y;
-    } else if (!first) {
-      if (++sub == UPT) {
-        sub = 0;
-        if (++b == T) b = ++a;
-      }
-    }
-    UnitInfo ui;
-    ui.a = a;
-    ui.b = b;
-    ui.lb = sub / WPR;
-    ui.jw = sub % WPR;
-    const int na = min(TILE, n - a * TILE);
-    const int nb = min(TILE, n - b * TILE);
-    ui.skip = ui.jw * 32 >= nb || ui.lb * 32 * KP >= na || (a == b && ui.jw < ui.lb * KP);
-    ui.self = a == b && ui.jw < (ui.lb + 1) * KP;
-    return ui;
-  }
 };
 
 // cp.async staging of one column block (16 bytes per instruction, zero-filled past n)
@@ -338,27 +313,29 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// The eps-tile kernel. Every warp owns a contiguous slice of the unit list and works
-// through it without any block-level synchronisation:
-//   * the unit's 32 staged points (one contiguous 32*S*4-byte run of the record
-//     array) are copied into the warp's double buffer with cp.async (one 16-byte
-//     copy per lane and record quarter), issued one unit ahead;
-//   * the lane block (32*KP consecutive points of tile a) is held in registers and
-//     only reloaded when the slice moves to another lane block;
+// The eps-tile kernel. Warps work independently (no block-level synchronisation):
+//   * row units come in batches of B consecutive units from a global atomic counter
+//     (about four batches per warp); the next batch's index and its list entries (one
+//     per lane, coalesced) are fetched one batch ahead, so neither the atomic nor the
+//     list load is on the critical path;
+//   * the unit's lane block is held in registers; the masked column blocks are copied
+//     into the warp's double buffer with cp.async (one 16-byte copy per lane and
+//     record quarter), issued one column block ahead, across unit boundaries;
 //   * per staged point every lane evaluates its KP points in the reference's exact
 //     operation order (eval_d2) and packs the predicates (pack_bits);
 //   * lane-side counts are popcounts accumulated in registers across the units of a
-//     lane block; column-side counts (off-diagonal units only: each unordered pair
-//     is evaluated once) come from column_counts, one atomic per column;
-//   * the unit's non-zero words are appended with one warp-aggregated atomic and
-//     the unit's chunk entry records where they went. Units without a single bit
-//     (most of a dense schedule) skip both.
+//     lane block; column-side counts (off-diagonal column blocks only: each unordered
+//     pair is evaluated once) come from column_counts, one atomic per column;
+//   * non-zero words go to a run of word slots the warp reserved earlier (one global
+//     atomic per WORD_RUN slots) and the chunk entry records where they went. Column
+//     blocks without a single bit (most of a dense schedule) skip both.
 template <int D, int F, bool SAFE>
 __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
   using G = Geo<D>;
   constexpr int KP = G::KP;
   constexpr int S = G::S;
-  constexpr int KC = Pack<KP, SAFE>::KC;
+  constexpr int KC = Pack<KP, SAFE, D>::KC;
+  constexpr int LB = TILE / (32 * KP);
 
   if ((*A.unsafe_flag != 0) == SAFE) return;  // the other instantiation owns this input
 
@@ -368,33 +345,87 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
   float* stage = reinterpret_cast<float*>(smem) + (size_t)warp * 2 * G::STAGE;
 
   const int n = (int)A.n;
+  const int T = A.T;
   const float eps32 = A.eps32;
+  const uint2* list = A.unit_list;
   long long U = A.dense_units;
-  if (A.unit_list) {
+  if (list) {
     const unsigned long long c = *A.unit_count;
     U = (long long)(c < A.units_cap ? c : A.units_cap);
   }
   const long long r_lo = U * A.shard_rank / A.shard_world;
   const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
-  const long long nw = (long long)gridDim.x * G::WARPS;
-  const long long gw = (long long)blockIdx.x * G::WARPS + warp;
-  const long long u_lo = r_lo + (r_hi - r_lo) * gw / nw;
-  const long long u_hi = r_lo + (r_hi - r_lo) * (gw + 1) / nw;
-  if (u_lo >= u_hi) return;
+  if (r_lo >= r_hi) return;
 
-  UnitCursor<KP> cursor;
-  cursor.start(A, u_lo);
-  // next unit to evaluate after u (skipped units get an empty chunk)
-  auto next_unit = [&](long long u, UnitInfo& ui, bool first) -> long long {
-    for (; u < u_hi; ++u, first = false) {
-      ui = cursor.get(u, first);
-      if (!ui.skip) return u;
-      if (lane == 0) A.uchunks[u] = make_uint2(0u, 0u);
-    }
-    return u;
+  // ---- batches of row units: [lo, hi) + list entries (lane i: entry lo + i) ----
+  // about 16 batches per warp; batch indices come from a 32-bit atomic counter
+  const long long nw = (long long)gridDim.x * G::WARPS;
+  long long B = (r_hi - r_lo) / (nw * 16);
+  B = B < 1 ? 1 : (B > 32 ? 32 : B);
+  unsigned int* const ctr = reinterpret_cast<unsigned int*>(A.work_ctr);
+  auto load_entries = [&](long long lo) -> uint2 {
+    return (list && lo + lane < r_hi && lane < B) ? __ldg(list + lo + lane) : make_uint2(0u, 0u);
   };
-  auto issue = [&](const UnitInfo& ui, int buf) {  // all lanes: record `lane` of the block
-    const int j = ui.b * TILE + ui.jw * 32 + lane;
+  auto batch_lo = [&](unsigned int x) -> long long {
+    const long long lo = r_lo + (long long)x * B;
+    return lo < r_hi ? lo : r_hi;
+  };
+  unsigned int pend = 0;
+  if (lane == 0) pend = atomicAdd(ctr, 1u);
+  long long gpos = batch_lo(__shfl_sync(0xffffffffu, pend, 0));  // next unit of the batch
+  long long cb_lo = gpos;
+  long long cb_hi = gpos + B < r_hi ? gpos + B : r_hi;
+  uint2 cent = load_entries(cb_lo);
+  if (lane == 0) pend = atomicAdd(ctr, 1u);
+  long long nb_lo = batch_lo(__shfl_sync(0xffffffffu, pend, 0));
+  uint2 nent = load_entries(nb_lo);
+  if (lane == 0) pend = atomicAdd(ctr, 1u);
+
+  // ---- step generator: (unit, column block) in order ----
+  uint32_t grem = 0u;  // column blocks of unit gu not yet handed out
+  long long gu = 0;
+  uint32_t gab = 0u;  // a << 16 | b
+  int glb = 0;
+  auto next_step = [&](Step& st) -> bool {
+    while (grem == 0u) {
+      if (gpos >= cb_hi) {  // switch to the prefetched batch, prefetch the one after
+        if (nb_lo >= r_hi) return false;
+        cb_lo = gpos = nb_lo;
+        cb_hi = nb_lo + B < r_hi ? nb_lo + B : r_hi;
+        cent = nent;
+        nb_lo = batch_lo(__shfl_sync(0xffffffffu, pend, 0));
+        nent = load_entries(nb_lo);
+        if (lane == 0) pend = atomicAdd(ctr, 1u);
+      }
+      const long long u = gpos++;
+      uint32_t m;
+      if (list) {
+        const int src = (int)(u - cb_lo);
+        gab = __shfl_sync(0xffffffffu, cent.x, src);
+        const uint32_t ey = __shfl_sync(0xffffffffu, cent.y, src);
+        glb = (int)(ey >> 16);
+        m = ey & 0xffffu;
+      } else {
+        int a, b;
+        decode_item(u / LB, T, a, b);
+        glb = (int)(u % LB);
+        gab = ((uint32_t)a << 16) | (uint32_t)b;
+        m = struct_mask(n, KP, a, b, glb);
+      }
+      gu = u;
+      if (lane < WPR && !((m >> lane) & 1u)) A.uchunks[u * WPR + lane] = make_uint2(0u, 0u);
+      grem = m;
+    }
+    st.u = gu;
+    st.a = (int)(gab >> 16);
+    st.b = (int)(gab & 0xffffu);
+    st.lb = glb;
+    st.jw = __ffs(grem) - 1;
+    grem &= grem - 1u;
+    return true;
+  };
+  auto issue = [&](const Step& st, int buf) {  // all lanes: record `lane` of the block
+    const int j = st.b * TILE + st.jw * 32 + lane;
     const bool v = j < n;
     const float* src = A.rec + (size_t)(v ? j : 0) * S;
     float* dst = stage + (size_t)buf * G::STAGE + lane * S;
@@ -403,9 +434,9 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
     cp_async_commit();
   };
 
-  UnitInfo cur;
-  long long u = next_unit(u_lo, cur, true);
-  if (u < u_hi) issue(cur, 0);
+  Step cur, nxt;
+  bool have = next_step(cur);
+  if (have) issue(cur, 0);
   int it = 0;
   int la = -1, llb = -1;  // lane block held in registers
   Lanes<D, KP> L;
@@ -416,7 +447,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
     lvalid[k] = false;
     lcnt[k] = 0u;
   }
-  unsigned long long units_done = 0;
+  unsigned long long steps_done = 0;
+  unsigned long long wpos = 0, wend = 0;  // the warp's reserved run of word slots
 
   auto flush = [&]() {
     if (la < 0) return;
@@ -427,12 +459,11 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
     }
   };
 
-  while (u < u_hi) {
+  while (have) {
     const int buf = it & 1;
     __syncwarp();  // every lane is done reading the other buffer
-    UnitInfo nxt;
-    const long long un = next_unit(u + 1, nxt, false);
-    if (un < u_hi) issue(nxt, buf ^ 1);
+    const bool hn = next_step(nxt);
+    if (hn) issue(nxt, buf ^ 1);
 
     if (cur.a != la || cur.lb != llb) {  // (re)load the lane block into registers
       flush();
@@ -465,7 +496,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
       }
     }
 
-    if (un < u_hi) cp_async_wait<1>();  // this unit's group is complete
+    if (hn) cp_async_wait<1>();  // this step's group is complete
     else cp_async_wait<0>();
     __syncwarp();
     const float* st = stage + (size_t)buf * G::STAGE;
@@ -488,12 +519,13 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
       }
       float d2[KP];
       eval_d2<D, F, KP>(L, xj, xj[D], d2);
-      pack_bits<KP, SAFE>(d2, eps32, jj, acc);
+      pack_bits<KP, SAFE, D>(d2, eps32, jj, acc);
     }
-    ++units_done;
+    ++steps_done;
 
     const int nb = min(TILE, n - cur.b * TILE);
     const uint32_t vm = valid_mask(nb - cur.jw * 32);
+    const bool self = cur.a == cur.b && cur.jw < (cur.lb + 1) * KP;
     uint32_t w[KP];
     uint32_t any = 0u;
 #pragma unroll
@@ -505,7 +537,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
     unsigned long long base = 0;
     int total = 0;
     if (__any_sync(0xffffffffu, any != 0u)) {
-      if (!cur.self) {
+      if (!self) {
         const uint32_t v = column_counts<KP>(w, lane);
         if (v) atomicAdd(&A.cnt[cur.b * TILE + cur.jw * 32 + lane], (int)v);
       } else {
@@ -513,7 +545,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
         for (int k = 0; k < KP; ++k)  // keep columns j >= row (incl. the self pair)
           w[k] &= diag_keep((llb * 32 + lane) * KP + k - cur.jw * 32);
       }
-      // append the unit's non-zero words (one warp-aggregated atomic)
+      // append the non-zero words into the warp's reserved run
       int nz = 0;
 #pragma unroll
       for (int k = 0; k < KP; ++k) nz += w[k] != 0u;
@@ -524,8 +556,14 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
         if (lane >= off) incl += y;
       }
       total = __shfl_sync(0xffffffffu, incl, 31);
-      if (lane == 0) base = atomicAdd(A.words_count, (unsigned long long)total);
-      base = __shfl_sync(0xffffffffu, base, 0);
+      if (wpos + (unsigned long long)total > wend) {  // reserve WORD_RUN more slots
+        unsigned long long r = 0;
+        if (lane == 0) r = atomicAdd(A.words_count, (unsigned long long)WORD_RUN);
+        wpos = __shfl_sync(0xffffffffu, r, 0);
+        wend = wpos + WORD_RUN;
+      }
+      base = wpos;
+      wpos += (unsigned long long)total;
       unsigned long long pos = base + (unsigned long long)(incl - nz);
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
@@ -537,22 +575,23 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
       }
     }
     if (lane == 0)
-      A.uchunks[u] = make_uint2((uint32_t)base, (uint32_t)total | ((uint32_t)(base >> 32) << 16));
+      A.uchunks[cur.u * WPR + cur.jw] =
+          make_uint2((uint32_t)base, (uint32_t)total | ((uint32_t)(base >> 32) << 16));
 
-    u = un;
     cur = nxt;
+    have = hn;
     ++it;
   }
   flush();
-  if (lane == 0 && units_done)
-    atomicAdd(A.pairs_done, units_done * 32ull * 32ull * (unsigned long long)KP);
+  if (lane == 0 && steps_done)
+    atomicAdd(A.pairs_done, steps_done * 32ull * 32ull * (unsigned long long)KP);
 }
 
-// ---- culled schedule: unit list ------------------------------------------------------
-// Unit (lb, jw) of kept tile pair (a, b) is kept unless it is structurally empty
-// (UnitCursor's skip) or, for d <= 4, the union box of its lane block and the box
-// of its column block are provably out of range: the bound of keep_item, in double,
-// on the 32-point block boxes (block_bounds_kernel).
+// ---- culled schedule: row-unit list ----------------------------------------------------
+// Column block jw of lane block lb in kept tile pair (a, b) is evaluated unless it is
+// structurally empty (struct_mask) or, for d <= 4, the union box of the lane block's
+// KP 32-point blocks and the box of the column block are provably out of range: the
+// bound of keep_item, in double, on the block boxes (block_bounds_kernel).
 __device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpad, int64_t n, int KP,
                                           int a, int b, int lb, int jw, float eps32, int formula,
                                           bool unsafe) {
@@ -583,7 +622,23 @@ __device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpa
   return !(bound > (double)eps32);  // NaN bounds keep the unit
 }
 
-// pass 1: units per kept item (warp per item); items past the kept count get 0
+// Column masks of two lane blocks (2p, 2p + 1) of item (a, b): lanes 0-15 test the 16
+// column blocks of the first, lanes 16-31 those of the second.
+__device__ __forceinline__ uint32_t pair_masks(const float* __restrict__ blk, int dpad, int64_t n,
+                                               int KP, int a, int b, int p, float eps32, int formula,
+                                               bool unsafe, int lane) {
+  const int lb = 2 * p + (lane >> 4);
+  const bool keep = unit_keep(blk, dpad, n, KP, a, b, lb, lane & 15, eps32, formula, unsafe);
+  return __ballot_sync(0xffffffffu, keep);
+}
+
+// For KP = 4 (d <= 8) a (lane block, tile pair) with many kept column blocks is
+// listed as several row units of at most 4 column blocks each (finer work balance at
+// the tail); a tile pair then has at most 16 units x WPR = 256 chunk entries, the
+// bound the union kernels hold in shared memory (MAX_UPT), as for KP <= 2 unsplit.
+__device__ __forceinline__ int unit_cols(int KP) { return KP == 4 ? 4 : 16; }
+
+// pass 1: row units per kept item (warp per item); items past the kept count get 0
 __global__ void unit_count_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
                                   float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
                                   const uint32_t* __restrict__ items,
@@ -591,7 +646,7 @@ __global__ void unit_count_kernel(const float* __restrict__ blk, int dpad, int64
                                   int32_t* __restrict__ ucnt) {
   const int64_t K = (int64_t)*kept;
   const bool unsafe = *unsafe_flag != 0;
-  const int upt = (TILE / (32 * KP)) * WPR;
+  const int LB = TILE / (32 * KP);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = K + tid; q < all_items; q += nth) ucnt[q] = 0;
@@ -600,16 +655,16 @@ __global__ void unit_count_kernel(const float* __restrict__ blk, int dpad, int64
     const uint32_t ab = items[q];
     const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
     int c = 0;
-    for (int s0 = 0; s0 < upt; s0 += 32) {
-      const int sub = s0 + lane;
-      const bool keep = unit_keep(blk, dpad, n, KP, a, b, sub / WPR, sub % WPR, eps32, formula, unsafe);
-      c += __popc(__ballot_sync(0xffffffffu, keep));
+    for (int p = 0; p < LB / 2; ++p) {
+      const uint32_t bal = pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane);
+      const int uc = unit_cols(KP);
+      c += (__popc(bal & 0xffffu) + uc - 1) / uc + (__popc(bal >> 16) + uc - 1) / uc;
     }
     if (lane == 0) ucnt[q] = c;
   }
 }
 
-// pass 3: scatter {item, sub} at the scanned offsets (deterministic, item order)
+// pass 3: scatter {a << 16 | b, lb << 16 | mask} at the scanned offsets (item order)
 __global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
                                     float eps32, int formula,
                                     const uint32_t* __restrict__ unsafe_flag,
@@ -620,7 +675,7 @@ __global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int
                                     unsigned long long* __restrict__ count) {
   const int64_t K = (int64_t)*kept;
   const bool unsafe = *unsafe_flag != 0;
-  const int upt = (TILE / (32 * KP)) * WPR;
+  const int LB = TILE / (32 * KP);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   if (tid == 0) *count = (unsigned long long)*total;
@@ -629,23 +684,36 @@ __global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int
     const uint32_t ab = items[q];
     const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
     unsigned long long pos = (unsigned long long)off[q];
-    for (int s0 = 0; s0 < upt; s0 += 32) {
-      const int sub = s0 + lane;
-      const bool keep = unit_keep(blk, dpad, n, KP, a, b, sub / WPR, sub % WPR, eps32, formula, unsafe);
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-      const unsigned long long p = pos + __popc(bal & ((1u << lane) - 1u));
-      if (keep && p < cap) list[p] = make_uint2(ab, (uint32_t)sub);
-      pos += __popc(bal);
+    for (int p = 0; p < LB / 2; ++p) {
+      const uint32_t bal = pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane);
+      if (lane == 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t m = h ? bal >> 16 : bal & 0xffffu;
+          while (m) {  // pieces of at most unit_cols(KP) column blocks
+            uint32_t piece = 0u;
+            for (int k = 0; k < unit_cols(KP) && m; ++k) {
+              piece |= m & (0u - m);
+              m &= m - 1u;
+            }
+            if (pos < cap) list[pos] = make_uint2(ab, ((uint32_t)(2 * p + h) << 16) | piece);
+            ++pos;
+          }
+        }
+      }
+      pos = __shfl_sync(0xffffffffu, pos, 0);
     }
   }
 }
 
 // ---- directory of tile pairs with words (for the union kernels) ------------------
+// Per item: its row units [lo, hi) (clipped to this launch's shard) own chunk entries
+// [lo * WPR, hi * WPR); the item gets a directory entry if any of them holds words.
 template <int KP>
 __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32_t* __restrict__ item_off,
                                 const unsigned long long* __restrict__ kept, uint4* __restrict__ dir,
                                 unsigned long long* __restrict__ dir_count) {
-  constexpr int UPT = (TILE / (32 * KP)) * WPR;
+  constexpr int LB = TILE / (32 * KP);
   long long U = A.dense_units;
   int64_t K = all_items;
   if (A.unit_list) {
@@ -661,17 +729,17 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32
     long long lo, hi;
     if (A.unit_list) {
       lo = item_off[q];
-      hi = q + 1 < all_items ? (long long)item_off[q + 1] : (long long)*A.unit_count;
-      if (q + 1 == K) hi = (long long)*A.unit_count;
+      hi = q + 1 < K ? (long long)item_off[q + 1] : U;
     } else {
-      lo = q * UPT;
-      hi = lo + UPT;
+      lo = q * LB;
+      hi = lo + LB;
     }
     lo = lo > r_lo ? lo : r_lo;
     hi = hi < r_hi ? hi : r_hi;
     if (lo >= hi) continue;
+    const long long c_lo = lo * WPR, c_hi = hi * WPR;
     uint32_t words = 0;
-    for (long long u = lo + lane; u < hi; u += 32) words += A.uchunks[u].y & 0xffffu;
+    for (long long e = c_lo + lane; e < c_hi; e += 32) words += A.uchunks[e].y & 0xffffu;
 #pragma unroll
     for (int off = 16; off; off >>= 1) words += __shfl_xor_sync(0xffffffffu, words, off);
     if (lane == 0 && words) {
@@ -684,8 +752,8 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32
         decode_item(q, A.T, a, b);
       }
       const unsigned long long ci = atomicAdd(dir_count, 1ull);
-      dir[ci] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)lo, (uint32_t)(hi - lo),
-                           (uint32_t)((unsigned long long)lo >> 32));
+      dir[ci] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)c_lo, (uint32_t)(c_hi - c_lo),
+                           (uint32_t)((unsigned long long)c_lo >> 32));
     }
   }
 }

@@ -15,6 +15,7 @@ params = ds.validate_params(cfg.eps, cfg.min_pts)
 conf = ds.default_config()
 conf.mem_cap = 150 * 1024**3
 lab, t = ds.run_dbscan(pts, params, conf)
+lab, t = ds.run_dbscan(pts, params, conf)
 print("culled", t.tile_ms, t.pairs_evaluated)
 if os.environ.get("DS_DENSE", "1") == "0":
     sys.exit(0)
