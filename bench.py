@@ -294,7 +294,7 @@ def run_b200(args):
     # the paper's dense all-pairs schedule on the same input (stage 1+2 only): the
     # eps-tile kernel at full occupancy of work, for the FP32 roofline comparison
     dense = None
-    if world == 1:
+    if world == 1 and not args.no_dense:
         ctx.configure(False, False)
         dts = []
         for _ in range(3):
@@ -412,6 +412,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-dense", action="store_true",
+                    help="skip the dense-schedule comparison leg (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -80,6 +80,8 @@ struct ds_ctx {
   bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
   unsigned long long units_cap = 0;  // culled unit list capacity (units)
+  UnitArgs units{};                  // the last eps-tile launch (read by stage 3)
+  int unit_lb = 4;                   // its lane blocks per tile
   Scalars* h_scalars = nullptr;      // pinned
 };
 
@@ -343,6 +345,8 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   }
   DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * WPR * 8));
   a.uchunks = (uint2*)c->uchunks.p;
+  c->units = a;
+  c->unit_lb = lane_blocks(d);
   DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
   DS_CK(record(c, c->ev[2], s));
@@ -420,8 +424,7 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(launch_core_init(w, min_pts, s));
   DS_CK(rec(c->ev[3]));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap,
-                            (const uint2*)c->uchunks.p, (const uint4*)c->chunks.p,
+  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
@@ -845,8 +848,7 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
   DS_CK(launch_core_init(w, min_pts, s));
-  DS_CK(launch_union_chunks(w, (const uint2*)c->words.p, c->words_cap,
-                            (const uint2*)c->uchunks.p, (const uint4*)c->chunks.p,
+  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
   DS_CK(cudaMemcpyAsync(d_parent, c->parent.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   DS_CK(cudaMemcpyAsync(d_bmin, c->bmin.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));

@@ -82,6 +82,21 @@ struct UnitArgs {
   unsigned long long* work_ctr;         // batch counter (zeroed before the launch)
 };
 
+// ---- item <-> tile pair: items enumerate the upper triangle a <= b in row order ----
+__device__ __forceinline__ int64_t row_offset(int64_t a, int64_t T) {
+  return a * T - a * (a - 1) / 2;
+}
+__device__ __forceinline__ void decode_item(int64_t q, int64_t T, int& a, int& b) {
+  const double tt = 2.0 * (double)T + 1.0;
+  int64_t r = (int64_t)floor((tt - sqrt(tt * tt - 8.0 * (double)q)) * 0.5);
+  if (r < 0) r = 0;
+  if (r > T - 1) r = T - 1;
+  while (r + 1 <= T - 1 && row_offset(r + 1, T) <= q) ++r;
+  while (r > 0 && row_offset(r, T) > q) --r;
+  a = (int)r;
+  b = (int)(r + (q - row_offset(r, T)));
+}
+
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
                         cudaStream_t s);
@@ -131,9 +146,10 @@ struct MergeWs {
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
-cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
-                                const uint2* uchunks, const uint4* dir,
-                                const unsigned long long* ndir, cudaStream_t s);
+// stage 3 over the stage-1 output: diagonal tile pairs from the directory (dir), the
+// off-diagonal ones walked per row unit of `units` (the eps-tile launch's arguments)
+cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lane_blocks,
+                                const uint4* dir, const unsigned long long* ndir, cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);

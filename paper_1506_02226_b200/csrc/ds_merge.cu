@@ -41,9 +41,7 @@ __device__ __forceinline__ int find_root(int32_t* parent, int v) {
   return par;
 }
 
-// Read-only find for the compress pass: a path-halving write racing with the
-// compress store could otherwise re-point an already compressed node at a
-// non-root ancestor.
+// Read-only find (roots pass, after every union is done).
 __device__ __forceinline__ int find_root_ro(const int32_t* parent, int v) {
   const volatile int32_t* p = parent;
   int par = p[v];
@@ -450,125 +448,126 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   }
 }
 
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) union_pair_kernel(
-    const uint4* __restrict__ dir, const unsigned long long* __restrict__ ndir,
-    const uint2* __restrict__ uchunks, const uint2* __restrict__ words,
-    unsigned long long words_cap, int64_t n, const uint32_t* __restrict__ corew, int32_t* parent,
-    int32_t* bmin, const int32_t* __restrict__ perm) {
-  __shared__ ItemWords iw;
-  __shared__ int la[2 * TILE];    // current ancestor of each point (-1: not core)
-  __shared__ int lb[2 * TILE];    // border minima (original indices)
-  __shared__ int hist[2 * TILE];  // ancestors that are local indices of the own tile
-  __shared__ uint32_t lcw[2 * WPR];
-  __shared__ uint32_t mb[WPR];    // tile-b points under tile b's dominant ancestor
-  __shared__ int dom[2];
-  __shared__ int link_ab;
-  const int tid = threadIdx.x;
-  const unsigned long long total = *ndir;
-  const int64_t nw = (n + 31) / 32;
-  for (unsigned long long c = blockIdx.x; c < total; c += gridDim.x) {
-    const DirInfo ci = decode_dir(dir[c]);
-    if (ci.a == ci.b) continue;  // uniform per CTA
-    load_item_words(ci, uchunks, words_cap, iw);
-    if (!iw.ok) continue;
-    if (tid < 2 * WPR) {
-      const int64_t gw = (int64_t)(tid < WPR ? ci.a : ci.b) * WPR + (tid & (WPR - 1));
-      lcw[tid] = gw < nw ? corew[gw] : 0u;
+// Round 2, off-diagonal tile pairs, one warp per row unit of the eps-tile launch
+// (lane block lb of tile a x the column blocks of tile b it evaluated). After round
+// 1 every core point's parent is its tile-local root. Per unit the warp stages the
+// parents and core flags of its 32*KP rows in shared memory; per non-empty column
+// block it stages that block's 32 parents and checks whether all of its core points
+// share one local root ("uniform", the common case inside a cluster). Then per word
+// (row u, column block jw, 32 bits):
+//   * core u, core columns: link root(u) with the uniform root, or with each core
+//     column's root; a per-lane cache of the last linked pair skips repeats;
+//   * core u, non-core columns: border candidates, atomicMin of u's ORIGINAL index;
+//   * non-core u with core columns: u's border candidate, the lowest ORIGINAL index
+//     among those columns (merge.py:116-130).
+// Links go through the global lock-free union-find (link_root: CAS hooks the larger
+// root under the smaller), so the result does not depend on the order.
+constexpr int LINK_WARPS = 8;
+__global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
+    const UnitArgs A, int LB, const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
+    const int32_t* __restrict__ perm) {
+  __shared__ int rows_sh[LINK_WARPS][TILE / WPR * 4];  // up to 128 rows per lane block
+  __shared__ int cols_sh[LINK_WARPS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* rows = rows_sh[warp];
+  int* cols = cols_sh[warp];
+  const int n = (int)A.n;
+  const int KPL = TILE / LB;  // rows per lane block (32 * KP)
+  long long U = A.dense_units;
+  if (A.unit_list) {
+    const unsigned long long c = *A.unit_count;
+    U = (long long)(c < A.units_cap ? c : A.units_cap);
+  }
+  const long long r_lo = U * A.shard_rank / A.shard_world;
+  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  const long long nw = (long long)gridDim.x * LINK_WARPS;
+  int last_a = -1, last_b = -1;  // this lane's last linked pair of roots
+  for (long long u = r_lo + (long long)blockIdx.x * LINK_WARPS + warp; u < r_hi; u += nw) {
+    int a, b, lb;
+    if (A.unit_list) {
+      const uint2 e = __ldg(A.unit_list + u);
+      a = (int)(e.x >> 16);
+      b = (int)(e.x & 0xffffu);
+      lb = (int)(e.y >> 16);
+    } else {
+      decode_item(u / LB, A.T, a, b);
+      lb = (int)(u % LB);
     }
-    for (int v = tid; v < 2 * TILE; v += THREADS) {
-      hist[v] = 0;
-      lb[v] = NONE;
+    if (a == b) continue;  // round 1
+    uint2 ce = make_uint2(0u, 0u);
+    if (lane < WPR) ce = A.uchunks[u * WPR + lane];
+    const uint32_t cnt = ce.y & 0xffffu;
+    const unsigned long long base = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
+    const bool ok = cnt != 0u && base + cnt <= A.words_cap;  // overflowed run: the host re-runs
+    uint32_t todo = __ballot_sync(0xffffffffu, ok);
+    if (!todo) continue;
+    // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not core)
+    const int r0 = a * TILE + lb * KPL;
+    for (int k = lane; k < KPL; k += 32) {
+      const int g = r0 + k;
+      const bool c = g < n && ((corew[g >> 5] >> (31 - (g & 31))) & 1u);
+      rows[k] = c ? parent[g] : -1;
     }
-    if (tid == 0) link_ab = 0;
-    __syncthreads();
-    for (int v = tid; v < 2 * TILE; v += THREADS) {
-      const int tb = v < TILE ? ci.a : ci.b;
-      const int64_t g = (int64_t)tb * TILE + (v & (TILE - 1));
-      const bool cv = g < n && ((lcw[v >> 5] >> (31 - (v & 31))) & 1u);
-      int anc = -1;
-      if (cv) {
-        anc = parent[g];
-        const int rel = anc - tb * TILE;
-        if (rel >= 0 && rel < TILE) atomicAdd(&hist[(v & TILE) + rel], 1);
-      }
-      la[v] = anc;
-    }
-    __syncthreads();
-    // dominant ancestor per tile: argmax of the histogram (one warp per tile)
-    if (tid < 64) {
-      const int half = tid >> 5, lane = tid & 31;
-      int best = -1, bestc = 0;
-      for (int r = lane; r < TILE; r += 32) {
-        const int h = hist[half * TILE + r];
-        if (h > bestc) {
-          bestc = h;
-          best = r;
-        }
-      }
-      for (int off = 16; off; off >>= 1) {
-        const int oc = __shfl_xor_sync(0xffffffffu, bestc, off);
-        const int ob = __shfl_xor_sync(0xffffffffu, best, off);
-        if (oc > bestc || (oc == bestc && ob >= 0 && (best < 0 || ob < best))) {
-          bestc = oc;
-          best = ob;
-        }
-      }
-      if (lane == 0) dom[half] = best < 0 ? -1 : (half ? ci.b : ci.a) * TILE + best;
-    }
-    __syncthreads();
-    const int gb = dom[1];
-    for (int ww = tid >> 5; ww < WPR; ww += THREADS / 32) {  // one ballot per word
-      const uint32_t bal = __ballot_sync(0xffffffffu, gb >= 0 && la[TILE + ww * 32 + (tid & 31)] == gb);
-      if ((tid & 31) == 0) mb[ww] = __brev(bal);
-    }
-    __syncthreads();
-    const int ga = dom[0];
-    for (int k = tid; k < iw.total; k += THREADS) {
-      const uint2 rec = item_word(iw, words, (uint32_t)k);
-      const uint32_t x = rec.x;
-      const int u = (int)(rec.y >> 4);
-      const int w = (int)(rec.y & 15u);
-      const uint32_t cw = lcw[WPR + w];
-      const int vb = TILE + w * 32;
-      if (la[u] >= 0) {
-        const int au = la[u];
-        const uint32_t um = x & cw;
-        const uint32_t hit = um & mb[w];
-        if (hit) {
-          if (au == ga) link_ab = 1;  // benign race: every writer stores 1
-          else if (au != gb) link_root(parent, find_plain(parent, au), gb);
-        }
-        uint32_t rest = um & ~mb[w];
-        while (rest) {
-          const int t = __clz(rest);
-          rest &= ~(0x80000000u >> t);
-          const int av = la[vb + t];
-          if (av != au) link_root(parent, find_plain(parent, au), av);
-        }
-        uint32_t bm = x & ~cw;
-        if (bm) {
-          const int gu = orig_of(perm, ci.a * TILE + u);
-          while (bm) {
-            const int t = __clz(bm);
-            bm &= ~(0x80000000u >> t);
-            atomicMin(&lb[vb + t], gu);
-          }
-        }
-      } else {
+    while (todo) {
+      const int jw = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const uint32_t wcnt = __shfl_sync(0xffffffffu, cnt, jw);
+      const unsigned long long wbase = __shfl_sync(0xffffffffu, base, jw);
+      const int c0 = b * TILE + jw * 32;
+      const uint32_t cw = corew[(b * TILE >> 5) + jw];
+      const bool cc = (cw >> (31 - lane)) & 1u;
+      const int pv = cc ? parent[c0 + lane] : -1;
+      cols[lane] = pv;
+      const unsigned same = __match_any_sync(0xffffffffu, pv);
+      const unsigned corel = __brev(cw);  // bit l <-> lane l
+      // uniform: every core lane in one match group
+      const int first = corel ? __ffs(corel) - 1 : 0;
+      const unsigned grp0 = __shfl_sync(0xffffffffu, same, first);
+      const int ub = (corel && (corel & ~grp0) == 0u) ? __shfl_sync(0xffffffffu, pv, first) : -1;
+      __syncwarp();
+      for (uint32_t k = lane; k < wcnt; k += 32) {
+        const uint2 rec = A.words[wbase + k];
+        const uint32_t x = rec.x;
+        const int ul = (int)(rec.y >> 4);
+        const int au = rows[ul - lb * KPL];
         const uint32_t cm = x & cw;
-        if (cm) atomicMin(&lb[u], min_orig(perm, ci.b * TILE + w * 32, cm));
+        if (au >= 0) {
+          if (cm) {
+            if (ub >= 0) {
+              if (au != ub && !(au == last_a && ub == last_b)) {
+                link_root(parent, find_plain(parent, au), ub);
+                last_a = au;
+                last_b = ub;
+              }
+            } else {
+              uint32_t bits = cm;
+              while (bits) {
+                const int t = __clz(bits);
+                bits &= ~(0x80000000u >> t);
+                const int av = cols[t];
+                if (av != au && !(au == last_a && av == last_b)) {
+                  link_root(parent, find_plain(parent, au), av);
+                  last_a = au;
+                  last_b = av;
+                }
+              }
+            }
+          }
+          uint32_t bm = x & ~cw;
+          if (bm) {
+            const int gu = orig_of(perm, a * TILE + ul);
+            while (bm) {
+              const int t = __clz(bm);
+              bm &= ~(0x80000000u >> t);
+              atomicMin(&bmin[c0 + t], gu);
+            }
+          }
+        } else if (cm) {
+          atomicMin(&bmin[a * TILE + ul], min_orig(perm, c0, cm));
+        }
       }
+      __syncwarp();  // cols is rewritten by the next column block
     }
-    __syncthreads();
-    if (tid == 0 && link_ab && ga >= 0 && gb >= 0 && ga != gb)
-      link_root(parent, find_plain(parent, ga), gb);
-    for (int v = tid; v < 2 * TILE; v += THREADS) {
-      if (lb[v] == NONE) continue;
-      const int64_t g = (int64_t)(v < TILE ? ci.a : ci.b) * TILE + (v & (TILE - 1));
-      atomicMin(&bmin[g], lb[v]);
-    }
-    __syncthreads();
   }
 }
 
@@ -606,11 +605,6 @@ __global__ void union_dense_kernel(const uint32_t* __restrict__ bits32, int64_t 
   }
 }
 
-__global__ void compress_kernel(const uint8_t* __restrict__ core, int64_t n, int32_t* parent) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && core[i]) parent[i] = find_root_ro(parent, (int)i);
-}
-
 // Runs over sorted indices s; bmin holds ORIGINAL indices of cores, cmin collects
 // the lowest ORIGINAL member index of each root (borders included).
 __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __restrict__ parent,
@@ -618,16 +612,22 @@ __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __
                              const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
                              int32_t* __restrict__ root, int32_t* cmin) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int r = -1;
-  if (core[i]) {
-    r = parent[i];
-  } else {
-    const int b = bmin[i];
-    if (b != NONE) r = parent[inv ? inv[b] : b];
+  int r = -1, o = NONE;
+  if (i < n) {
+    if (core[i]) {
+      r = find_root_ro(parent, (int)i);
+    } else {
+      const int b = bmin[i];
+      if (b != NONE) r = find_root_ro(parent, inv ? inv[b] : b);
+    }
+    root[i] = r;
+    o = perm ? perm[i] : (int)i;
   }
-  root[i] = r;
-  if (r >= 0) atomicMin(&cmin[r], perm ? perm[i] : (int)i);  // first appearance
+  // first appearance: one atomicMin per distinct root of the warp (spatially sorted
+  // neighbours mostly share a cluster, so this removes the same-address contention)
+  const unsigned grp = __match_any_sync(0xffffffffu, r);
+  const int m = (int)__reduce_min_sync(grp, (unsigned)o);  // o >= 0
+  if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicMin(&cmin[r], m);
 }
 
 // flag[o] = 1 iff original index o is the first appearance of its cluster
@@ -671,46 +671,55 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
   return excl;
 }
 
-__global__ void scan_partials_kernel(const int32_t* __restrict__ flag, int64_t n,
-                                     int32_t* __restrict__ partials) {
-  const int64_t base = (int64_t)blockIdx.x * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
-  int s = 0;
-#pragma unroll
-  for (int k = 0; k < SCAN_PER; ++k)
-    if (base + k < n) s += flag[base + k];
-  int total;
-  block_exclusive_scan(s, total);
-  if (threadIdx.x == 0) partials[blockIdx.x] = total;
-}
-
-__global__ void scan_top_kernel(int32_t* partials, int64_t np, int32_t* total_out) {
-  int carry = 0;
-  for (int64_t c0 = 0; c0 < np; c0 += SCAN_T) {
-    const int64_t idx = c0 + threadIdx.x;
-    const int v = idx < np ? partials[idx] : 0;
-    int total;
-    const int excl = block_exclusive_scan(v, total);
-    if (idx < np) partials[idx] = carry + excl;
-    carry += total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total_out = carry;
-}
-
-__global__ void scan_apply_kernel(int32_t* flag, int64_t n, const int32_t* __restrict__ partials) {
-  const int64_t base = (int64_t)blockIdx.x * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
+// Single-pass exclusive scan (decoupled look-back): tiles of SCAN_BLK elements are
+// taken in ticket order; each tile publishes its aggregate, then thread 0 walks back
+// over the predecessors' published {flag, value} words until it meets an inclusive
+// prefix, and publishes its own. state[] and the ticket are zeroed before the launch.
+constexpr unsigned long long SC_AGG = 1ull << 62, SC_PRE = 2ull << 62;
+__global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(int32_t* data, int64_t n,
+                                                               unsigned int* ticket,
+                                                               unsigned long long* state,
+                                                               int32_t* total) {
+  __shared__ unsigned int tile_sh;
+  __shared__ int prefix_sh;
+  if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const unsigned int tile = tile_sh;
+  const int64_t base = (int64_t)tile * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
   int v[SCAN_PER];
-  int s = 0;
+  int sum = 0;
 #pragma unroll
   for (int k = 0; k < SCAN_PER; ++k) {
-    v[k] = base + k < n ? flag[base + k] : 0;
-    s += v[k];
+    v[k] = base + k < n ? data[base + k] : 0;
+    sum += v[k];
   }
-  int total;
-  int run = block_exclusive_scan(s, total) + partials[blockIdx.x];
+  int agg;
+  const int excl = block_exclusive_scan(sum, agg);
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* st = state;
+    int prefix = 0;
+    if (tile == 0) {
+      st[0] = SC_PRE | (unsigned int)agg;
+    } else {
+      st[tile] = SC_AGG | (unsigned int)agg;
+      for (int64_t j = (int64_t)tile - 1; j >= 0;) {
+        const unsigned long long w = st[j];
+        if (!(w >> 62)) continue;  // predecessor not published yet
+        prefix += (int)(unsigned int)w;
+        if ((w >> 62) == 2) break;
+        --j;
+      }
+      __threadfence();
+      st[tile] = SC_PRE | (unsigned int)(prefix + agg);
+    }
+    prefix_sh = prefix;
+    if ((int64_t)(tile + 1) * SCAN_BLK >= n) *total = prefix + agg;  // last tile
+  }
+  __syncthreads();
+  int run = prefix_sh + excl;
 #pragma unroll
   for (int k = 0; k < SCAN_PER; ++k) {
-    if (base + k < n) flag[base + k] = run;
+    if (base + k < n) data[base + k] = run;
     run += v[k];
   }
 }
@@ -786,7 +795,7 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 }  // namespace
 
-int64_t scan_partials_len(int64_t n) { return (n + SCAN_BLK - 1) / SCAN_BLK; }
+int64_t scan_partials_len(int64_t n) { return 2 * ((n + SCAN_BLK - 1) / SCAN_BLK + 1); }
 
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) {
   const int t = 256;
@@ -795,9 +804,11 @@ cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) 
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned long long words_cap,
-                                const uint2* uchunks, const uint4* dir,
-                                const unsigned long long* ndir, cudaStream_t s) {
+cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lane_blocks,
+                                const uint4* dir, const unsigned long long* ndir, cudaStream_t s) {
+  const uint2* words = units.words;
+  const unsigned long long words_cap = units.words_cap;
+  const uint2* uchunks = units.uchunks;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -818,8 +829,8 @@ cudaError_t launch_union_chunks(const MergeWs& w, const uint2* words, unsigned l
   union_diag_kernel<<<(unsigned)grid, 512, diag_smem, s>>>(dir, uchunks, w.diag_idx, ntiles,
                                                           words, words_cap, w.n, w.corew,
                                                           w.parent, w.bmin, w.perm);
-  union_pair_kernel<256><<<sms * 8, 256, 0, s>>>(dir, ndir, uchunks, words, words_cap, w.n,
-                                                 w.corew, w.parent, w.bmin, w.perm);
+  union_links_kernel<<<sms * 8, LINK_WARPS * 32, 0, s>>>(units, lane_blocks, w.corew, w.parent,
+                                                         w.bmin, w.perm);
   return cudaGetLastError();
 }
 
@@ -836,13 +847,10 @@ cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
   const int t = 256;
   const unsigned b = blocks_for(w.n, t);
-  compress_kernel<<<b, t, 0, s>>>(w.core, w.n, w.parent);
   roots_kernel<<<b, t, 0, s>>>(w.core, w.parent, w.bmin, w.n, w.perm, w.inv, w.root, w.cmin);
   flags_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.n, w.perm, w.flag);
-  const int64_t np = scan_partials_len(w.n);
-  scan_partials_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
-  scan_top_kernel<<<1, SCAN_T, 0, s>>>(w.partials, np, w.nclusters);
-  scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(w.flag, w.n, w.partials);
+  cudaError_t e = launch_exclusive_scan(w.flag, w.n, w.partials, w.nclusters, s);
+  if (e != cudaSuccess) return e;
   label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, w.perm, labels);
   return cudaGetLastError();
 }
@@ -873,12 +881,16 @@ cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* per
   return cudaGetLastError();
 }
 
+// partials: scan_partials_len(n) int32 of workspace {ticket, pad, state[tiles]}
 cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
                                   cudaStream_t s) {
-  const int64_t np = scan_partials_len(n);
-  scan_partials_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(data, n, partials);
-  scan_top_kernel<<<1, SCAN_T, 0, s>>>(partials, np, total);
-  scan_apply_kernel<<<(unsigned)np, SCAN_T, 0, s>>>(data, n, partials);
+  if (n <= 0) return cudaMemsetAsync(total, 0, sizeof(int32_t), s);
+  const int64_t tiles = (n + SCAN_BLK - 1) / SCAN_BLK;
+  cudaError_t e = cudaMemsetAsync(partials, 0, (size_t)(tiles + 1) * 8, s);
+  if (e != cudaSuccess) return e;
+  scan_lookback_kernel<<<(unsigned)tiles, SCAN_T, 0, s>>>(
+      data, n, reinterpret_cast<unsigned int*>(partials),
+      reinterpret_cast<unsigned long long*>(partials) + 1, total);
   return cudaGetLastError();
 }
 

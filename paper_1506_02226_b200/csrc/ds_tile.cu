@@ -45,20 +45,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// ---- item <-> tile pair --------------------------------------------------------
-__device__ __forceinline__ int64_t row_offset(int64_t a, int64_t T) {
-  return a * T - a * (a - 1) / 2;
-}
-__device__ __forceinline__ void decode_item(int64_t q, int64_t T, int& a, int& b) {
-  const double tt = 2.0 * (double)T + 1.0;
-  int64_t r = (int64_t)floor((tt - sqrt(tt * tt - 8.0 * (double)q)) * 0.5);
-  if (r < 0) r = 0;
-  if (r > T - 1) r = T - 1;
-  while (r + 1 <= T - 1 && row_offset(r + 1, T) <= q) ++r;
-  while (r > 0 && row_offset(r, T) > q) --r;
-  a = (int)r;
-  b = (int)(r + (q - row_offset(r, T)));
-}
 
 // Diagonal tile: keep columns t >= rel (j >= i incl. the self pair; the self bit
 // is needed by the reference-layout export and is a no-op for the merge).
