@@ -280,10 +280,13 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
 
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
   DS_CK(cudaMemsetAsync(c->cnt.p, 0, (size_t)n * 4, s));
-  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, s));
+  const bool do_sort = c->sort && T > 1;
+  if (do_sort) DS_CK(ensure(c->bbox, 64));
+  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag,
+                    do_sort ? (unsigned int*)c->bbox.p : nullptr, s));
   const float* rec = (const float*)c->rec.p;
   c->sorted = false;
-  if (c->sort && T > 1) {  // Morton order: compact tiles (ds_sort.cu)
+  if (do_sort) {  // Morton order: compact tiles (ds_sort.cu)
     const size_t N = (size_t)n;
     DS_CK(ensure(c->rec_sorted, N * rec_stride(d) * 4));
     DS_CK(ensure(c->perm, N * 4));
@@ -291,7 +294,6 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     DS_CK(ensure(c->keys, N * 8));
     DS_CK(ensure(c->keys_alt, N * 8));
     DS_CK(ensure(c->kidx, N * 4));
-    DS_CK(ensure(c->bbox, 64));
     DS_CK(ensure(c->sort_temp, sort_temp_bytes(n)));
     DS_CK(launch_spatial_sort(rec, n, d, (float*)c->rec_sorted.p, (int32_t*)c->perm.p,
                               (int32_t*)c->inv.p, (unsigned long long*)c->keys.p,
@@ -334,13 +336,13 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     const int dp = padded_dim(d);
     DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * dp + 1) * 4));
     DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
-    DS_CK(ensure(c->ucnt, (size_t)pl.all_items * 4));
+    DS_CK(ensure(c->ucnt, (size_t)pl.all_items * 8));  // item_units
     DS_CK(ensure(c->ulist, (size_t)pl.units_cap * 8));
     c->units_cap = pl.units_cap;
     DS_CK(launch_unit_list((const float*)c->blk.p, n, d, eps32, formula, &sc->unsafe_flag,
-                           (const uint32_t*)c->items.p, &sc->kept, pl.all_items,
-                           (int32_t*)c->ucnt.p, (int32_t*)c->ipartials.p, &sc->units32,
-                           (uint2*)c->ulist.p, pl.units_cap, &sc->unit_count, s));
+                           (const uint32_t*)c->items.p, &sc->kept, pl.all_items, rank, world,
+                           (uint2*)c->ulist.p, pl.units_cap, &sc->unit_count, (uint2*)c->ucnt.p,
+                           s));
     a.unit_list = (const uint2*)c->ulist.p;
   }
   DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * WPR * 8));
@@ -350,7 +352,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
   DS_CK(record(c, c->ev[2], s));
-  DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const int32_t*)c->ucnt.p : nullptr,
+  DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const uint2*)c->ucnt.p : nullptr,
                         &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count, s));
   return DS_OK;
 }
@@ -400,8 +402,8 @@ void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* 
   t->tile_launches = launches;
   int64_t evaluated = pl.item_hi - pl.item_lo;
   if (pl.cull) {
-    const int64_t kept = (int64_t)c->h_scalars->kept;
-    evaluated = kept * (pl.rank + 1) / pl.world - kept * pl.rank / pl.world;
+    const int64_t kept = (int64_t)c->h_scalars->kept;  // dealt cyclically to the shards
+    evaluated = kept > pl.rank ? (kept - pl.rank + pl.world - 1) / pl.world : 0;
   }
   t->tiles_total = evaluated;
   t->tiles_nonempty = (int64_t)c->h_scalars->nonempty_count;

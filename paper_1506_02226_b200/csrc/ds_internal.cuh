@@ -71,8 +71,9 @@ struct UnitArgs {
   uint2* uchunks;                       // per (unit, column block) {first word lo,
                                         //   count | first word hi << 16}
   const uint32_t* item_list;            // culled tile pairs (a << 16 | b), or nullptr: triangle
-  const uint2* unit_list;               // culled row units {a << 16 | b, lb << 16 | column mask},
-                                        // or nullptr: unit q * LB + lb of the triangle
+  const uint2* unit_list;               // culled row units of this shard {a << 16 | b,
+                                        // lb << 16 | column mask}, or nullptr: unit
+                                        // q * LB + lb of the triangle
   const unsigned long long* unit_count; // length of unit_list (device)
   unsigned long long units_cap;         // capacity of unit_list (culled); uchunks: * WPR
   int64_t dense_units;                  // all_items * LB (dense schedule)
@@ -97,21 +98,42 @@ __device__ __forceinline__ void decode_item(int64_t q, int64_t T, int& a, int& b
   b = (int)(r + (q - row_offset(r, T)));
 }
 
+// Units this launch evaluates: the culled list is built per shard (its items), the
+// dense triangle order is sliced into equal unit ranges.
+__device__ __forceinline__ void unit_range(const UnitArgs& A, long long& lo, long long& hi) {
+  if (A.unit_list) {
+    const unsigned long long c = *A.unit_count;
+    lo = 0;
+    hi = (long long)(c < A.units_cap ? c : A.units_cap);
+  } else {
+    const long long U = A.dense_units;
+    lo = U * A.shard_rank / A.shard_world;
+    hi = U * (A.shard_rank + 1) / A.shard_world;
+  }
+}
+
+// order-preserving float -> uint (for atomicMin/Max bounding boxes)
+__device__ __forceinline__ unsigned int ord_bits(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
+// bbox (nullable): 8 uints {ord lo[4], ord hi[4]} of the first min(d, 4) dimensions,
+// reset here and reduced by the kernel (the spatial sort's grid)
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
-                        cudaStream_t s);
+                        unsigned int* bbox, cudaStream_t s);
 cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
                                 cudaStream_t s);
-// culled schedule: per kept tile pair, the units that are not provably empty
-// (ucnt: per-item unit count, scanned in place into the item's first unit)
+// culled schedule: the row-unit list of this shard (kept items q = rank + k * world),
+// pieces of unit_cols column blocks; item_units[q] = {first unit, units}
 cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, int formula,
                              const uint32_t* unsafe_flag, const uint32_t* item_list,
-                             const unsigned long long* kept, int64_t all_items, int32_t* ucnt,
-                             int32_t* partials, int32_t* total32, uint2* unit_list,
-                             unsigned long long units_cap, unsigned long long* unit_count,
-                             cudaStream_t s);
+                             const unsigned long long* kept, int64_t all_items, int rank, int world,
+                             uint2* unit_list, unsigned long long units_cap,
+                             unsigned long long* unit_count, uint2* item_units, cudaStream_t s);
 // per tile pair with words: {a << 16 | b, first unit lo, units, first unit hi} (atomic append)
-cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const int32_t* item_off,
+cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
                             unsigned long long* dir_count, cudaStream_t s);
 // 32-point block boxes [block][lo(dpad), hi(dpad), maxnorm] for sub-tile culling

@@ -473,13 +473,8 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
   int* cols = cols_sh[warp];
   const int n = (int)A.n;
   const int KPL = TILE / LB;  // rows per lane block (32 * KP)
-  long long U = A.dense_units;
-  if (A.unit_list) {
-    const unsigned long long c = *A.unit_count;
-    U = (long long)(c < A.units_cap ? c : A.units_cap);
-  }
-  const long long r_lo = U * A.shard_rank / A.shard_world;
-  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  long long r_lo, r_hi;
+  unit_range(A, r_lo, r_hi);
   const long long nw = (long long)gridDim.x * LINK_WARPS;
   int last_a = -1, last_b = -1;  // this lane's last linked pair of roots
   for (long long u = r_lo + (long long)blockIdx.x * LINK_WARPS + warp; u < r_hi; u += nw) {

@@ -10,9 +10,9 @@
 // to ORIGINAL indices through perm / inv (ds_merge.cu).
 //
 // Keys: up to 4 leading dimensions quantised to a 2^(b/k)-per-dimension grid over
-// the global bounding box, b = 16 bits (two radix passes) for 1-2-D inputs up to
+// the global bounding box (reduced by the prep kernel), b = 16 bits (two radix passes) for 1-2-D inputs up to
 // 2^20 points and 24 bits otherwise — far finer than a 512-point tile. The sort is CUB's stable LSD radix sort on
-// (key, original index), so the permutation is deterministic and identical on
+// (32-bit key, original index), so the permutation is deterministic and identical on
 // every rank.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,43 +28,6 @@ namespace {
 // 2^20 points, 24 (three passes) otherwise
 inline int key_bits(int64_t n, int kd) { return (kd <= 2 && n <= (1 << 20)) ? 16 : 24; }
 
-__device__ __forceinline__ unsigned int ord_bits(float f) {
-  const unsigned int u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving float -> uint
-}
-
-__global__ void bbox_kernel(const float* __restrict__ rec, int64_t n, int S, int kd,
-                            unsigned int* __restrict__ lo_bits, unsigned int* __restrict__ hi_bits) {
-  __shared__ unsigned int smin[4], smax[4];
-  if (threadIdx.x < 4) {
-    smin[threadIdx.x] = 0xffffffffu;
-    smax[threadIdx.x] = 0u;
-  }
-  __syncthreads();
-  for (int k = 0; k < kd; ++k) {
-    float mn = INFINITY, mx = -INFINITY;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      const float v = rec[i * S + k];
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, v);
-    }
-    for (int off = 16; off; off >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(&smin[k], ord_bits(mn));
-      atomicMax(&smax[k], ord_bits(mx));
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < kd) {
-    atomicMin(&lo_bits[threadIdx.x], smin[threadIdx.x]);
-    atomicMax(&hi_bits[threadIdx.x], smax[threadIdx.x]);
-  }
-}
-
 __device__ __forceinline__ float unord(unsigned int u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
@@ -72,7 +35,7 @@ __device__ __forceinline__ float unord(unsigned int u) {
 __global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits,
                               const unsigned int* __restrict__ lo_bits,
                               const unsigned int* __restrict__ hi_bits,
-                              unsigned long long* __restrict__ keys, int32_t* __restrict__ idx) {
+                              uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int bits = total_bits / kd;
@@ -85,7 +48,7 @@ __global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, i
     t = t < 0 ? 0 : (t > levels ? levels : t);  // NaN -> 0 via the comparisons below
     q[k] = (t == t) ? (uint32_t)t : 0u;
   }
-  unsigned long long key = 0;
+  uint32_t key = 0;  // <= 24 bits
   for (int b = bits - 1; b >= 0; --b)
     for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
   keys[i] = key;
@@ -108,9 +71,8 @@ __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
 
 size_t sort_temp_bytes(int64_t n) {
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, (const int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
   return bytes;
 }
 
@@ -121,17 +83,15 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   const int dp = padded_dim(d);
   const int S = rec_stride(d);
   const int kd = d < 4 ? d : 4;
-  cudaError_t e = cudaMemsetAsync(bbox, 0xff, 4 * sizeof(unsigned int), s);  // lo = max
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(bbox + 4, 0, 4 * sizeof(unsigned int), s);             // hi = min
-  if (e != cudaSuccess) return e;
   (void)dp;
-  bbox_kernel<<<148, 512, 0, s>>>(rec, n, S, kd, bbox, bbox + 4);
+  // the bounding box was reduced by the prep kernel (launch_prep with a bbox buffer)
   const unsigned blocks = (unsigned)((n + 255) / 256);
   const int kb = key_bits(n, kd);
-  morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, kb, bbox, bbox + 4, keys, idx);
-  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, idx, perm, (int)n, 0,
-                                      (kb / kd) * kd, s);
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(keys);
+  uint32_t* k32_alt = reinterpret_cast<uint32_t*>(keys_alt);
+  morton_kernel<<<blocks, 256, 0, s>>>(rec, n, S, kd, kb, bbox, bbox + 4, k32, idx);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k32, k32_alt, idx, perm,
+                                                  (int)n, 0, (kb / kd) * kd, s);
   if (e != cudaSuccess) return e;
   permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted, inv);
   return cudaGetLastError();

@@ -334,13 +334,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
   const int T = A.T;
   const float eps32 = A.eps32;
   const uint2* list = A.unit_list;
-  long long U = A.dense_units;
-  if (list) {
-    const unsigned long long c = *A.unit_count;
-    U = (long long)(c < A.units_cap ? c : A.units_cap);
-  }
-  const long long r_lo = U * A.shard_rank / A.shard_world;
-  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  long long r_lo, r_hi;
+  unit_range(A, r_lo, r_hi);
   if (r_lo >= r_hi) return;
 
   // ---- batches of row units: [lo, hi) + list entries (lane i: entry lo + i) ----
@@ -578,6 +573,50 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
 // structurally empty (struct_mask) or, for d <= 4, the union box of the lane block's
 // KP 32-point blocks and the box of the column block are provably out of range: the
 // bound of keep_item, in double, on the block boxes (block_bounds_kernel).
+// Box test of (lane block lb of tile a) x (column block jw of tile b), d <= 4 (KP = 4):
+// all loads independent (fully unrolled), so one round trip per test.
+template <int DP>
+__device__ __forceinline__ bool box_keep(const float* __restrict__ blk, int64_t n, int a, int b,
+                                         int lb, int jw, float eps32, int formula) {
+  constexpr int BS = 2 * DP + 1;
+  constexpr int KPB = 4;  // 32-point blocks per lane block
+  const int64_t nblk = (n + 31) / 32;
+  const float* cb = blk + ((int64_t)b * WPR + jw) * BS;
+  const int64_t l0 = (int64_t)a * WPR + (int64_t)lb * KPB;
+  float lo[DP], hi[DP], c[BS];
+  float wn = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < DP; ++q) {
+    lo[q] = INFINITY;
+    hi[q] = -INFINITY;
+  }
+#pragma unroll
+  for (int q = 0; q < BS; ++q) c[q] = cb[q];
+#pragma unroll
+  for (int k = 0; k < KPB; ++k) {
+    if (l0 + k < nblk) {
+      const float* lk = blk + (l0 + k) * BS;
+#pragma unroll
+      for (int q = 0; q < DP; ++q) {
+        lo[q] = fminf(lo[q], lk[q]);
+        hi[q] = fmaxf(hi[q], lk[DP + q]);
+      }
+      wn = fmaxf(wn, lk[2 * DP]);
+    }
+  }
+  const double u = 1.0 / 16777216.0;
+  double L = 0.0;
+#pragma unroll
+  for (int q = 0; q < DP; ++q) {
+    const double g = fmax(0.0, fmax((double)c[q] - (double)hi[q], (double)lo[q] - (double)c[DP + q]));
+    L += g * g;
+  }
+  const double w = fmax((double)wn, (double)c[2 * DP]);
+  double bound = L * (1.0 - 4.0 * 3.0 * DP * u) * (1.0 - 1e-12);
+  if (formula == DS_FORMULA_ALGEBRAIC) bound -= 4.0 * (2.0 * DP + 3.0) * u * w * 2.0 * 1.001;
+  return !(bound > (double)eps32);  // NaN bounds keep the unit
+}
+
 __device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpad, int64_t n, int KP,
                                           int a, int b, int lb, int jw, float eps32, int formula,
                                           bool unsafe) {
@@ -585,27 +624,14 @@ __device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpa
   const int64_t nb = min((int64_t)TILE, n - (int64_t)b * TILE);
   if (jw * 32 >= nb || lb * 32 * KP >= na) return false;
   if (a == b && jw < lb * KP) return false;
-  if (unsafe || !blk || (a == b && jw < (lb + 1) * KP)) return true;
-  const int BS = 2 * dpad + 1;
-  const int64_t nblk = (n + 31) / 32;
-  const float* cb = blk + ((int64_t)b * WPR + jw) * BS;
-  const int64_t l0 = (int64_t)a * WPR + (int64_t)lb * KP;
-  const int kl = (int)min((int64_t)KP, nblk - l0);
-  const double u = 1.0 / 16777216.0;
-  double L = 0.0, wn = (double)cb[2 * dpad];
-  for (int k = 0; k < kl; ++k) wn = fmax(wn, (double)blk[(l0 + k) * BS + 2 * dpad]);
-  for (int q = 0; q < dpad; ++q) {
-    float lo = INFINITY, hi = -INFINITY;
-    for (int k = 0; k < kl; ++k) {
-      lo = fminf(lo, blk[(l0 + k) * BS + q]);
-      hi = fmaxf(hi, blk[(l0 + k) * BS + dpad + q]);
-    }
-    const double g = fmax(0.0, fmax((double)cb[q] - (double)hi, (double)lo - (double)cb[dpad + q]));
-    L += g * g;
+  if (unsafe || !blk || KP != 4 || (a == b && jw < (lb + 1) * KP)) return true;
+  switch (dpad) {
+    case 1: return box_keep<1>(blk, n, a, b, lb, jw, eps32, formula);
+    case 2: return box_keep<2>(blk, n, a, b, lb, jw, eps32, formula);
+    case 3: return box_keep<3>(blk, n, a, b, lb, jw, eps32, formula);
+    case 4: return box_keep<4>(blk, n, a, b, lb, jw, eps32, formula);
+    default: return true;
   }
-  double bound = L * (1.0 - 4.0 * 3.0 * dpad * u) * (1.0 - 1e-12);
-  if (formula == DS_FORMULA_ALGEBRAIC) bound -= 4.0 * (2.0 * dpad + 3.0) * u * wn * 2.0 * 1.001;
-  return !(bound > (double)eps32);  // NaN bounds keep the unit
 }
 
 // Column masks of two lane blocks (2p, 2p + 1) of item (a, b): lanes 0-15 test the 16
@@ -624,61 +650,64 @@ __device__ __forceinline__ uint32_t pair_masks(const float* __restrict__ blk, in
 // bound the union kernels hold in shared memory (MAX_UPT), as for KP <= 2 unsplit.
 __device__ __forceinline__ int unit_cols(int KP) { return KP == 4 ? 4 : 16; }
 
-// pass 1: row units per kept item (warp per item); items past the kept count get 0
-__global__ void unit_count_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
-                                  float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
-                                  const uint32_t* __restrict__ items,
-                                  const unsigned long long* __restrict__ kept, int64_t all_items,
-                                  int32_t* __restrict__ ucnt) {
+// The row-unit list of this launch's shard, one kernel: warp per kept item (items are
+// dealt to the shards cyclically, q = rank + k * world, which spreads the dense and
+// the sparse regions evenly), masks by pair_masks, split into pieces, one atomic per
+// item reserves its list run. The order of the runs is arbitrary; item_units[q]
+// records {first unit, units} for the directory.
+__global__ void __launch_bounds__(256) unit_list_kernel(
+    const float* __restrict__ blk, int dpad, int64_t n, int KP, float eps32, int formula,
+    const uint32_t* __restrict__ unsafe_flag, const uint32_t* __restrict__ items,
+    const unsigned long long* __restrict__ kept, int rank, int world, uint2* __restrict__ list,
+    unsigned long long cap, unsigned long long* __restrict__ unit_count,
+    uint2* __restrict__ item_units) {
+  constexpr int W = 8;  // warps per CTA; one list reservation per CTA and round
+  __shared__ int wcnt[W];
+  __shared__ unsigned long long wpos[W];
   const int64_t K = (int64_t)*kept;
   const bool unsafe = *unsafe_flag != 0;
   const int LB = TILE / (32 * KP);
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = K + tid; q < all_items; q += nth) ucnt[q] = 0;
-  const int lane = threadIdx.x & 31;
-  for (int64_t q = tid >> 5; q < K; q += nth >> 5) {
-    const uint32_t ab = items[q];
-    const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
+  const int uc = unit_cols(KP);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t mine = K > rank ? (K - rank + world - 1) / world : 0;
+  for (int64_t t0 = (int64_t)blockIdx.x * W; t0 < mine; t0 += (int64_t)gridDim.x * W) {
+    const int64_t t = t0 + warp;
+    const int64_t q = rank + t * world;
+    uint32_t ab = 0u;
+    uint32_t bal[8];
     int c = 0;
-    for (int p = 0; p < LB / 2; ++p) {
-      const uint32_t bal = pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane);
-      const int uc = unit_cols(KP);
-      c += (__popc(bal & 0xffffu) + uc - 1) / uc + (__popc(bal >> 16) + uc - 1) / uc;
+    if (t < mine) {  // warp-uniform
+      ab = items[q];
+      const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        bal[p] = p < LB / 2 ? pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane) : 0u;
+        c += (__popc(bal[p] & 0xffffu) + uc - 1) / uc + (__popc(bal[p] >> 16) + uc - 1) / uc;
+      }
     }
-    if (lane == 0) ucnt[q] = c;
-  }
-}
-
-// pass 3: scatter {a << 16 | b, lb << 16 | mask} at the scanned offsets (item order)
-__global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int64_t n, int KP,
-                                    float eps32, int formula,
-                                    const uint32_t* __restrict__ unsafe_flag,
-                                    const uint32_t* __restrict__ items,
-                                    const unsigned long long* __restrict__ kept,
-                                    const int32_t* __restrict__ off, const int32_t* __restrict__ total,
-                                    uint2* __restrict__ list, unsigned long long cap,
-                                    unsigned long long* __restrict__ count) {
-  const int64_t K = (int64_t)*kept;
-  const bool unsafe = *unsafe_flag != 0;
-  const int LB = TILE / (32 * KP);
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  if (tid == 0) *count = (unsigned long long)*total;
-  const int lane = threadIdx.x & 31;
-  for (int64_t q = tid >> 5; q < K; q += nth >> 5) {
-    const uint32_t ab = items[q];
-    const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
-    unsigned long long pos = (unsigned long long)off[q];
-    for (int p = 0; p < LB / 2; ++p) {
-      const uint32_t bal = pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane);
-      if (lane == 0) {
+    if (lane == 0) wcnt[warp] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < W; ++w) tot += wcnt[w];
+      unsigned long long base = tot ? atomicAdd(unit_count, (unsigned long long)tot) : 0ull;
+      for (int w = 0; w < W; ++w) {
+        wpos[w] = base;
+        base += (unsigned long long)wcnt[w];
+      }
+    }
+    __syncthreads();
+    if (t < mine && lane == 0) {
+      unsigned long long pos = wpos[warp];
+      item_units[q] = make_uint2((uint32_t)pos, (uint32_t)c | ((uint32_t)(pos >> 32) << 16));
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          uint32_t m = h ? bal >> 16 : bal & 0xffffu;
+          uint32_t m = h ? bal[p] >> 16 : bal[p] & 0xffffu;
           while (m) {  // pieces of at most unit_cols(KP) column blocks
             uint32_t piece = 0u;
-            for (int k = 0; k < unit_cols(KP) && m; ++k) {
+            for (int k = 0; k < uc && m; ++k) {
               piece |= m & (0u - m);
               m &= m - 1u;
             }
@@ -687,41 +716,39 @@ __global__ void unit_scatter_kernel(const float* __restrict__ blk, int dpad, int
           }
         }
       }
-      pos = __shfl_sync(0xffffffffu, pos, 0);
     }
+    __syncthreads();  // wcnt / wpos are rewritten by the next round
   }
 }
 
 // ---- directory of tile pairs with words (for the union kernels) ------------------
-// Per item: its row units [lo, hi) (clipped to this launch's shard) own chunk entries
-// [lo * WPR, hi * WPR); the item gets a directory entry if any of them holds words.
+// Per item: its row units [lo, hi) (culled: item_units of this shard's items; dense:
+// the triangle order, clipped to the shard) own chunk entries [lo * WPR, hi * WPR);
+// the item gets a directory entry if any of them holds words.
 template <int KP>
-__global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32_t* __restrict__ item_off,
+__global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2* __restrict__ item_units,
                                 const unsigned long long* __restrict__ kept, uint4* __restrict__ dir,
                                 unsigned long long* __restrict__ dir_count) {
   constexpr int LB = TILE / (32 * KP);
-  long long U = A.dense_units;
-  int64_t K = all_items;
-  if (A.unit_list) {
-    const unsigned long long c = *A.unit_count;
-    U = (long long)(c < A.units_cap ? c : A.units_cap);
-    K = (int64_t)*kept;
-  }
-  const long long r_lo = U * A.shard_rank / A.shard_world;
-  const long long r_hi = U * (A.shard_rank + 1) / A.shard_world;
+  long long r_lo, r_hi;
+  unit_range(A, r_lo, r_hi);
+  const int64_t K = A.unit_list ? (int64_t)*kept : all_items;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < K; q += nwarps) {
     long long lo, hi;
     if (A.unit_list) {
-      lo = item_off[q];
-      hi = q + 1 < K ? (long long)item_off[q + 1] : U;
+      if (q % A.shard_world != A.shard_rank) continue;
+      const uint2 iu = item_units[q];
+      lo = (long long)iu.x | ((long long)(iu.y >> 16) << 32);
+      hi = lo + (long long)(iu.y & 0xffffu);
+      if (hi > r_hi) hi = r_hi;  // list overflow: the host re-runs
     } else {
       lo = q * LB;
       hi = lo + LB;
+      lo = lo > r_lo ? lo : r_lo;
+      hi = hi < r_hi ? hi : r_hi;
     }
-    lo = lo > r_lo ? lo : r_lo;
-    hi = hi < r_hi ? hi : r_hi;
     if (lo >= hi) continue;
     const long long c_lo = lo * WPR, c_hi = hi * WPR;
     uint32_t words = 0;
@@ -745,24 +772,61 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const int32
 }
 
 // ---- prep: narrow to float32 (RN), squared norms, padded records ------------------
-__global__ void prep_kernel(const double* __restrict__ coords, int64_t n, int d, int dpad, int S,
-                            float* __restrict__ rec, uint32_t* unsafe_flag) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double* src = coords + i * d;
-  float* dst = rec + i * S;
-  float p = 0.f;
+// Also reduces the bounding box of the first min(d, 4) coordinates for the spatial
+// sort (bbox != nullptr): grid-stride threads keep running min/max, then a warp and a
+// block reduction and one atomic per block and dimension.
+__global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ coords, int64_t n,
+                                                   int d, int dpad, int S, float* __restrict__ rec,
+                                                   uint32_t* unsafe_flag,
+                                                   unsigned int* __restrict__ bbox) {
+  float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
-  for (int c = 0; c < dpad; ++c) {
-    const float v = c < d ? __double2float_rn(src[c]) : 0.f;  // kernels.py:148-150
-    dst[c] = v;
-    const float sq = __fmul_rn(v, v);
-    p = (c == 0) ? sq : __fadd_rn(p, sq);  // kernels.py:388-391, left to right
-    bad |= !(fabsf(v) <= SAFE_ABS);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* src = coords + i * d;
+    float* dst = rec + i * S;
+    float p = 0.f;
+    for (int c = 0; c < dpad; ++c) {
+      const float v = c < d ? __double2float_rn(src[c]) : 0.f;  // kernels.py:148-150
+      dst[c] = v;
+      if (c < 4) {  // NaN coordinates drop out of fminf / fmaxf
+        mn[c] = fminf(mn[c], v);
+        mx[c] = fmaxf(mx[c], v);
+      }
+      const float sq = __fmul_rn(v, v);
+      p = (c == 0) ? sq : __fadd_rn(p, sq);  // kernels.py:388-391, left to right
+      bad |= !(fabsf(v) <= SAFE_ABS);
+    }
+    dst[dpad] = p;
+    for (int c = dpad + 1; c < S; ++c) dst[c] = 0.f;
   }
-  dst[dpad] = p;
-  for (int c = dpad + 1; c < S; ++c) dst[c] = 0.f;
-  if (bad) atomicOr(unsafe_flag, 1u);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(unsafe_flag, 1u);
+  if (!bbox) return;
+  __shared__ unsigned int smn[4], smx[4];
+  if (threadIdx.x < 4) {
+    smn[threadIdx.x] = 0xffffffffu;
+    smx[threadIdx.x] = 0u;
+  }
+  __syncthreads();
+  const int kd = d < 4 ? d : 4;
+  for (int k = 0; k < kd; ++k) {
+    float a = mn[k], b = mx[k];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      a = fminf(a, __shfl_xor_sync(0xffffffffu, a, off));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&smn[k], ord_bits(a));
+      atomicMax(&smx[k], ord_bits(b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kd) {
+    atomicMin(&bbox[threadIdx.x], smn[threadIdx.x]);
+    atomicMax(&bbox[4 + threadIdx.x], smx[threadIdx.x]);
+  }
 }
 
 // ---- tile culling ------------------------------------------------------------------
@@ -948,12 +1012,20 @@ cudaError_t launch_d(const UnitArgs& a, int formula, int sm_count, cudaStream_t 
 int padded_dim(int d) { return pad_dim(d); }
 
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
-                        cudaStream_t s) {
+                        unsigned int* bbox, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int threads = 256;
-  const int64_t blocks = (n + threads - 1) / threads;
-  prep_kernel<<<(unsigned)blocks, threads, 0, s>>>(coords, n, d, dp, S, rec, unsafe_flag);
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  if (bbox) {
+    cudaError_t e = cudaMemsetAsync(bbox, 0xff, 4 * sizeof(unsigned int), s);  // lo = max
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(bbox + 4, 0, 4 * sizeof(unsigned int), s);  // hi = min
+    if (e != cudaSuccess) return e;
+  }
+  prep_kernel<<<(unsigned)blocks, threads, 0, s>>>(coords, n, d, dp, S, rec, unsafe_flag, bbox);
   return cudaGetLastError();
 }
 
@@ -1001,27 +1073,21 @@ cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_co
 
 cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, int formula,
                              const uint32_t* unsafe_flag, const uint32_t* item_list,
-                             const unsigned long long* kept, int64_t all_items, int32_t* ucnt,
-                             int32_t* partials, int32_t* total32, uint2* unit_list,
-                             unsigned long long units_cap, unsigned long long* unit_count,
-                             cudaStream_t s) {
+                             const unsigned long long* kept, int64_t all_items, int rank, int world,
+                             uint2* unit_list, unsigned long long units_cap,
+                             unsigned long long* unit_count, uint2* item_units, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int KP = unit_kp(d);
   const float* box = dp <= 4 ? blk : nullptr;  // block boxes only pay off in low dimension
-  int64_t blocks = (all_items * 32 + 255) / 256;
+  int64_t blocks = (all_items / world * 32 + 255) / 256 + 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  unit_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
-                                                     item_list, kept, all_items, ucnt);
-  cudaError_t e = launch_exclusive_scan(ucnt, all_items, partials, total32, s);
-  if (e != cudaSuccess) return e;
-  unit_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
-                                                       item_list, kept, ucnt, total32, unit_list,
-                                                       units_cap, unit_count);
+  unit_list_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
+                                                    item_list, kept, rank, world, unit_list,
+                                                    units_cap, unit_count, item_units);
   return cudaGetLastError();
 }
 
-cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const int32_t* item_off,
+cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
                             unsigned long long* dir_count, cudaStream_t s) {
   int64_t blocks = (all_items * 32 + 255) / 256;
@@ -1029,13 +1095,13 @@ cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const i
   if (blocks < 1) blocks = 1;
   switch (unit_kp(d)) {
     case 4:
-      unit_dir_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+      unit_dir_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
       break;
     case 2:
-      unit_dir_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+      unit_dir_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
       break;
     default:
-      unit_dir_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_off, kept, dir, dir_count);
+      unit_dir_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
   }
   return cudaGetLastError();
 }
