@@ -351,16 +351,17 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
     const long long lo = r_lo + (long long)x * B;
     return lo < r_hi ? lo : r_hi;
   };
+  // the first two batches of warp gw are gw and nw + gw; later ones come from the counter
+  // (offset by 2 nw), its first fetch issued here and consumed two batches later
+  const unsigned int gw = blockIdx.x * G::WARPS + warp;
   unsigned int pend = 0;
-  if (lane == 0) pend = atomicAdd(ctr, 1u);
-  long long gpos = batch_lo(__shfl_sync(0xffffffffu, pend, 0));  // next unit of the batch
+  if (lane == 0) pend = atomicAdd(ctr, 1u) + 2u * (unsigned int)nw;
+  long long gpos = batch_lo(gw);  // next unit of the batch
   long long cb_lo = gpos;
   long long cb_hi = gpos + B < r_hi ? gpos + B : r_hi;
   uint2 cent = load_entries(cb_lo);
-  if (lane == 0) pend = atomicAdd(ctr, 1u);
-  long long nb_lo = batch_lo(__shfl_sync(0xffffffffu, pend, 0));
+  long long nb_lo = batch_lo(gw + (unsigned int)nw);
   uint2 nent = load_entries(nb_lo);
-  if (lane == 0) pend = atomicAdd(ctr, 1u);
 
   // ---- step generator: (unit, column block) in order ----
   uint32_t grem = 0u;  // column blocks of unit gu not yet handed out
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
         cent = nent;
         nb_lo = batch_lo(__shfl_sync(0xffffffffu, pend, 0));
         nent = load_entries(nb_lo);
-        if (lane == 0) pend = atomicAdd(ctr, 1u);
+        if (lane == 0) pend = atomicAdd(ctr, 1u) + 2u * (unsigned int)nw;
       }
       const long long u = gpos++;
       uint32_t m;
@@ -527,16 +528,16 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
           w[k] &= diag_keep((llb * 32 + lane) * KP + k - cur.jw * 32);
       }
       // append the non-zero words into the warp's reserved run
-      int nz = 0;
+      // word order: lane-major, then k; offsets from one ballot per k (no shuffle chain)
+      const uint32_t lt = (1u << lane) - 1u;
+      int excl = 0;
+      total = 0;
 #pragma unroll
-      for (int k = 0; k < KP; ++k) nz += w[k] != 0u;
-      int incl = nz;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += y;
+      for (int k = 0; k < KP; ++k) {
+        const uint32_t m = __ballot_sync(0xffffffffu, w[k] != 0u);
+        excl += __popc(m & lt);
+        total += __popc(m);
       }
-      total = __shfl_sync(0xffffffffu, incl, 31);
       if (wpos + (unsigned long long)total > wend) {  // reserve WORD_RUN more slots
         unsigned long long r = 0;
         if (lane == 0) r = atomicAdd(A.words_count, (unsigned long long)WORD_RUN);
@@ -545,7 +546,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
       }
       base = wpos;
       wpos += (unsigned long long)total;
-      unsigned long long pos = base + (unsigned long long)(incl - nz);
+      unsigned long long pos = base + (unsigned long long)excl;
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         if (w[k]) {
