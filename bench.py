@@ -313,9 +313,12 @@ def run_b200(args):
     ops = algorithmic_ops_per_pair(d, formula)
     tile_s = statistics.mean(tile_ms) / 1e3
     achieved = pairs * ops / tile_s / 1e12
-    # kernels per step: prep, 2x eps-tile (one exits at once), core flags, 2 union rounds,
-    # 7 finalize kernels; sharded runs add the forest merge and run core flags twice
-    launches_per_step = (12 + 2 * (last[3] - 1)) if world == 1 else 14
+    # kernels per step (1 GPU, culled schedule; the ncu launch list in profiles/): prep,
+    # morton, 4 CUB radix-sort kernels, permute, tile bounds, cull flags, scan, cull
+    # scatter, block bounds, unit list, 2x eps-unit (one exits at once), unit dir, core
+    # init, diag index, union diag, union links, roots, flags, scan, label = 24; a
+    # word-overflow re-run repeats the pipeline; sharded runs add the forest merge
+    launches_per_step = 24 * last[3] if world == 1 else 26
 
     line = {
         "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",
@@ -341,7 +344,7 @@ def run_b200(args):
                 "parts_ms": ({k: statistics.mean(getattr(p, k) or 0.0 for p in e2e_parts)
                               for k in ("h2d_ms", "fused_ms", "merge_ms", "d2h_ms", "total_ms")}
                              if world == 1 else None)},
-        "roofline": {"bound": "fp32", "kernel": "eps_tile_kernel", "achieved": achieved,
+        "roofline": {"bound": "fp32", "kernel": "eps_unit_kernel", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": tile_traffic(args.config),
                      "traffic_source": "dram__bytes_read+write per launch, profiles/r01_tile_traffic.json",

@@ -563,7 +563,7 @@ extern "C" {
 int ds_abi_version(void) { return DS_ABI_VERSION; }
 
 const char* ds_build_info(void) {
-  return "densescan_b200 sm_100a; eps-tile kernel TILE=512, TMA bulk staging, sign-bit packing; "
+  return "densescan_b200 sm_100a; eps-unit kernel TILE=512, warp units + cp.async staging, exact culling; "
          "union-find merge; built with nvcc " __DATE__;
 }
 

@@ -129,13 +129,8 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
 //     shared-memory union-find (CAS on the larger root);
 //   * every core point gets parent = its local root (the smallest index of its
 //     local component) — each tile is owned by one CTA, so no global atomics.
-// Round 2, one CTA per off-diagonal chunk (tiles a < b): each point's current
-// ancestor is one coalesced load; the dominant ancestor of each tile (the
-// round-1 giant component in dense regions) is found with a shared histogram.
-// A core-core bit whose tile-b end hangs under tile b's dominant ancestor is
-// covered by one global link per chunk; the other bits link their two
-// ancestors directly (rare). Border minima (lowest ORIGINAL core index,
-// merge.py:116-130) are reduced per chunk in shared memory, then once per point.
+// Round 2 (union_links_kernel, below) walks the off-diagonal units of the eps-tile
+// launch, one warp per unit.
 // A directory entry names one tile pair with words and its range of unit chunks;
 // the words of a tile pair are the concatenation of its units' chunks. ItemWords
 // holds the prefix sums of the chunk lengths in shared memory so that a CTA can

@@ -6,33 +6,23 @@
 // rounding, the distance matrix is never stored, and the result leaves the
 // kernel as bit-packed 32-bit adjacency words plus neighbour counts.
 //
-// Work decomposition. Points are cut into tiles of TILE=512. The relation is
-// exactly symmetric (both formulas are bitwise symmetric in (i, j), see
-// DESIGN.md §2), so only tile pairs (a, b) with a <= b are evaluated: one
-// "item" = one tile pair = 262,144 pair evaluations. A persistent grid pulls
-// items from an atomic counter. Per item:
-//   * tile b (the broadcast side) is staged into shared memory with a TMA
-//     bulk copy (cp.async.bulk, mbarrier completion), double-buffered so the
-//     next item's copy overlaps this item's arithmetic;
-//   * tile a (the lane side) lives in registers: each thread owns KPT points
-//     and keeps 2*c (algebraic) or c (direct) plus the norm T;
-//   * every thread walks the 512 staged points; for each pair it computes
-//     d2 in exact reference order: every operation a separately rounded
-//     f32 op (never contracted into an FMA; tests/test_sass_gate.py checks
-//     the SASS). The FP32 pipe is the bound, so the arithmetic is issued as
-//     packed f32x2 where the reference order allows it — products of two
-//     dimensions in one FMUL2, T + P and the final subtraction of two lane
-//     points in one FADD2 — which executes exactly the 2d+1 (algebraic) or
-//     3d-1 (direct) FP32 lane-ops per pair and nothing else on that pipe;
-//   * the compare is split between an FSETP on the ALU pipe and the sign bit
-//     of fl(eps32 - d2) (see pack_bits) to balance the two pipes; 32 results
-//     pack into one 32-bit word per lane point;
-//   * words go to shared memory; the lane-side counts are popcounts of the
-//     words, the broadcast-side counts a bit-sliced (carry-save) vertical
-//     popcount of the same words; the non-zero words are appended to HBM for
-//     stage 3 after a block-wide prefix scan, as one contiguous "chunk" per
-//     tile pair: 8-byte records {word, row << 4 | column word} plus a chunk
-//     entry {a, b, base, count}.
+// Work decomposition. Points (in spatial order, ds_sort.cu) are cut into tiles of
+// TILE=512. The relation is exactly symmetric (both formulas are bitwise symmetric
+// in (i, j)), so only tile pairs (a, b) with a <= b are evaluated.
+// Inside a tile pair the work unit of one warp is (a lane block of 32*KP points of
+// tile a, held in registers) x (up to 4-16 column blocks of 32 points of tile b,
+// streamed through a per-warp double buffer with cp.async). Warps run independently:
+// no block-level barrier, dynamic batches of units (see eps_unit_kernel). Per staged
+// point every lane computes d2 for its KP points in the exact reference order, every
+// operation a separately rounded f32 op (never contracted into an FMA;
+// tests/test_abi.py checks the SASS) — the FP32 pipe is the bound, so products of two
+// dimensions go through one FMUL2 and T + P / the final subtraction of two lane
+// points through one FADD2, which executes exactly the 2d+1 (algebraic) or 3d-1
+// (direct) FP32 lane-ops per pair. Predicates become 32-bit words (FSETP or the sign
+// bit of fl(eps32 - d2), see pack_bits); lane-side counts are popcounts of the words,
+// column-side counts a bit-sliced vertical popcount; the non-zero words are appended
+// to HBM for stage 3 with their local row and column block, one chunk entry per
+// (unit, column block).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -300,10 +290,11 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // The eps-tile kernel. Warps work independently (no block-level synchronisation):
-//   * row units come in batches of B consecutive units from a global atomic counter
-//     (about four batches per warp); the next batch's index and its list entries (one
-//     per lane, coalesced) are fetched one batch ahead, so neither the atomic nor the
-//     list load is on the critical path;
+//   * units come in batches of B consecutive units (about 16 batches per warp): the
+//     first two batches of a warp are static, later ones come from a global atomic
+//     counter; each batch's index and its list entries (one per lane, coalesced) are
+//     fetched one batch ahead, so neither the atomic nor the list load is on the
+//     critical path;
 //   * the unit's lane block is held in registers; the masked column blocks are copied
 //     into the warp's double buffer with cp.async (one 16-byte copy per lane and
 //     record quarter), issued one column block ahead, across unit boundaries;
