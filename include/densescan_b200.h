@@ -149,10 +149,37 @@ ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
                         const uint8_t* valid, int64_t n, int64_t min_pts,
                         int64_t* labels_out, ds_timings* timings);
 
+/* ---- materialising ladder (kernels.py:153-308) ----
+ * The BASELINE / SOA / TILED / TILED_UNROLLED rungs all compute the same
+ * direct-formula squared distances (kernels.py:21-25, _direct_block 197-210):
+ * d2[i][j] = ((x_j - x_i)^2 + (y_j - y_i)^2) + ..., float32, no FMA. */
+
+/* dist_baseline / dist_soa / dist_tiled: the n x n float32 matrix, row-major
+ * into out (host). Capacity: 4 n^2 bytes against mem_cap (kernels.py:156). */
+ds_status ds_dist_matrix(ds_ctx* ctx, const double* coords, int64_t n, int32_t d,
+                         int64_t mem_cap, float* out, ds_timings* timings);
+
+/* build_clusters_from_dist (kernels.py:284-308): threshold a host n x n float32
+ * matrix at float32(eps_sq) into the reference layout (bits n x ceil(n/8)
+ * MSB-first, int64 counts incl. self, uint8 valid = counts >= min_pts).
+ * Capacity: n * ceil(n/8) bytes against mem_cap (kernels.py:293). */
+ds_status ds_dist_threshold(ds_ctx* ctx, const float* dist, int64_t n, double eps_sq,
+                            int64_t min_pts, int64_t mem_cap, uint8_t* bits_out,
+                            int64_t* counts_out, uint8_t* valid_out, ds_timings* timings);
+
+/* run_variant's materialising rungs (kernels.py:445-470): both steps on the
+ * device, the matrix materialised in HBM (row blocks of at most 4 GiB) and never
+ * copied to the host. timings->tile_ms = distance kernels (dist_ms),
+ * timings->merge_ms = threshold kernels (cluster_ms). */
+ds_status ds_dist_build(ds_ctx* ctx, const double* coords, int64_t n, int32_t d, double eps_sq,
+                        int64_t min_pts, int64_t mem_cap, uint8_t* bits_out,
+                        int64_t* counts_out, uint8_t* valid_out, ds_timings* timings);
+
 /* ---- multi-GPU shards (row-block sharding of stage 1 over tile-pair items) ----
  * The upper-triangle tile pairs (TILE = ds_tile_side() points per side) are
- * numbered 0 .. ds_tile_items(n)-1 row-major. Each rank evaluates a contiguous
- * share of them; exchanges (done by the caller over NCCL, see
+ * numbered 0 .. ds_tile_items(n)-1 row-major. Each rank evaluates a share of
+ * them (culled: the kept tile pairs dealt cyclically; dense: a contiguous range
+ * of work units); exchanges (done by the caller over NCCL, see
  * paper_1506_02226_b200/distributed.py) are: all-reduce(SUM) of the int32
  * counts, all-gather of the int32 parent forests, all-reduce(MIN) of the
  * int32 border minima. Replaces the reference's fork-join over row ranges
@@ -160,8 +187,8 @@ ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
 int64_t ds_tile_items(int64_t n);
 int ds_tile_side(void);
 
-/* Stage 1+2 on rank's contiguous share of the tile-pair items (of the culled
- * list when DS_OPT_TILE_CULL is on, of the dense triangle otherwise): partial
+/* Stage 1+2 on rank's share of the tile-pair items (of the culled list when
+ * DS_OPT_TILE_CULL is on, of the dense triangle otherwise): partial
  * neighbour counts into d_counts (int32[n], overwritten); the adjacency words
  * stay in the context for ds_shard_stage3_local. */
 ds_status ds_shard_stage12(ds_ctx* ctx, const double* d_coords, int64_t n, int32_t d,

@@ -29,7 +29,8 @@ EXPORTS = (
     "ds_ctx_create", "ds_ctx_destroy", "ds_ctx_set_option", "ds_ctx_get_option",
     "ds_host_register", "ds_host_unregister",
     "ds_run_dbscan", "ds_run_dbscan_device",
-    "ds_fused_build", "ds_merge_bits", "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
+    "ds_fused_build", "ds_merge_bits", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
+    "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
     "ds_shard_stage3_local", "ds_shard_stage3_merge",
 )
 
@@ -111,6 +112,16 @@ def load_library(path: str = LIB_PATH):
         lib.ds_merge_bits.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
                                       ctypes.POINTER(Timings)]
         lib.ds_merge_bits.restype = ctypes.c_int
+        lib.ds_dist_matrix.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp,
+                                       ctypes.POINTER(Timings)]
+        lib.ds_dist_matrix.restype = ctypes.c_int
+        lib.ds_dist_threshold.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                          ctypes.c_int64, vp, vp, vp, ctypes.POINTER(Timings)]
+        lib.ds_dist_threshold.restype = ctypes.c_int
+        lib.ds_dist_build.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                      ctypes.c_int64, ctypes.c_int64, vp, vp, vp,
+                                      ctypes.POINTER(Timings)]
+        lib.ds_dist_build.restype = ctypes.c_int
         lib.ds_tile_items.argtypes = [ctypes.c_int64]
         lib.ds_tile_items.restype = ctypes.c_int64
         lib.ds_tile_side.restype = ctypes.c_int
@@ -280,6 +291,46 @@ class Context:
                                     ctypes.byref(t))
         raise_for(st, self.lib)
         return labels, t
+
+
+    # ---- materialising ladder (kernels.py:153-308) ----
+    def dist_matrix(self, coords: np.ndarray, mem_cap: int):
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n, d = coords.shape
+        out = np.empty((n, n), dtype=np.float32)
+        t = Timings()
+        st = self.lib.ds_dist_matrix(self.handle, coords.ctypes.data, n, d, int(mem_cap),
+                                     out.ctypes.data, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return out, t
+
+    def dist_threshold(self, dist: np.ndarray, eps_sq: float, min_pts: int, mem_cap: int):
+        dist = np.ascontiguousarray(dist, dtype=np.float32)
+        n = dist.shape[0]
+        if dist.shape != (n, n):
+            raise ValueError(f"distance matrix must be square, got {dist.shape}")
+        bits = np.empty((n, (n + 7) // 8), dtype=np.uint8)
+        counts = np.empty(n, dtype=np.int64)
+        valid = np.empty(n, dtype=np.uint8)
+        t = Timings()
+        st = self.lib.ds_dist_threshold(self.handle, dist.ctypes.data, n, float(eps_sq),
+                                        int(min_pts), int(mem_cap), bits.ctypes.data,
+                                        counts.ctypes.data, valid.ctypes.data, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return bits, counts, valid.astype(bool), t
+
+    def dist_build(self, coords: np.ndarray, eps_sq: float, min_pts: int, mem_cap: int):
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n, d = coords.shape
+        bits = np.empty((n, (n + 7) // 8), dtype=np.uint8)
+        counts = np.empty(n, dtype=np.int64)
+        valid = np.empty(n, dtype=np.uint8)
+        t = Timings()
+        st = self.lib.ds_dist_build(self.handle, coords.ctypes.data, n, d, float(eps_sq),
+                                    int(min_pts), int(mem_cap), bits.ctypes.data,
+                                    counts.ctypes.data, valid.ctypes.data, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return bits, counts, valid.astype(bool), t
 
 
 def pin_frozen(arr: np.ndarray, owner) -> bool:

@@ -68,7 +68,7 @@ struct ds_ctx {
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, bbox, blk, diag, ulist, uchunks, ucnt;
+      keys_alt, kidx, sort_temp, bbox, blk, diag, ulist, uchunks, ucnt, dist, dbits;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -111,7 +111,8 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                      &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt};
+                      &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt,
+                      &c->dist, &c->dbits};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -610,7 +611,8 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt};
+                &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt,
+                &c->dist, &c->dbits};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -896,6 +898,188 @@ ds_status ds_shard_stage3_merge(ds_ctx* c, const int32_t* d_counts, int64_t n, i
     t->merge_ms = m;
     t->core_count = (int64_t)c->h_scalars->ncore;
     t->cluster_count = c->h_scalars->nclusters;
+  }
+  return DS_OK;
+}
+
+// ---- materialising ladder (ds_dist.cu) ---------------------------------------------
+namespace {
+
+constexpr size_t DIST_BLOCK_BYTES = (size_t)4 << 30;  // device row block of the matrix
+
+int64_t dist_rows_per_block(int64_t n) {
+  const int64_t r = (int64_t)(DIST_BLOCK_BYTES / ((size_t)dist_pitch(n) * 4));
+  return r < 1 ? 1 : (r > n ? n : r);
+}
+
+ds_status ladder_capacity(int64_t required, int64_t mem_cap, const char* what) {
+  if (mem_cap > 0 && required > mem_cap) {
+    set_capacity(required, mem_cap);
+    set_error(std::string(what) + " exceeds the memory cap");
+    return DS_ECAPACITY;
+  }
+  return DS_OK;
+}
+
+// coords (host float64 n x d) -> narrowed records on the device
+ds_status ladder_prep(ds_ctx* c, const double* coords, int64_t n, int32_t d) {
+  cudaStream_t s = c->stream;
+  const size_t in_bytes = (size_t)n * d * 8;
+  DS_CK(ensure(c->coords64, in_bytes));
+  DS_CK(ensure(c->rec, (size_t)n * rec_stride(d) * 4));
+  DS_CK(ensure(c->scalars, sizeof(Scalars)));
+  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
+  DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
+  DS_CK(launch_prep((const double*)c->coords64.p, n, d, (float*)c->rec.p,
+                    &((Scalars*)c->scalars.p)->unsafe_flag, nullptr, s));
+  return DS_OK;
+}
+
+}  // namespace
+
+ds_status ds_dist_matrix(ds_ctx* c, const double* coords, int64_t n, int32_t d, int64_t mem_cap,
+                         float* out, ds_timings* t) {
+  if (!c || !coords || !out) {
+    set_error("ctx, coords and out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, 1, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  st = ladder_capacity(4 * n * n, mem_cap, "the n x n float32 distance matrix");  // kernels.py:156
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  st = ladder_prep(c, coords, n, d);
+  if (st != DS_OK) return st;
+  const int64_t pitch = dist_pitch(n), rows = dist_rows_per_block(n);
+  DS_CK(ensure(c->dist, (size_t)rows * pitch * 4));
+  float kernel_ms = 0.f;
+  for (int64_t r0 = 0; r0 < n; r0 += rows) {
+    const int64_t rb = std::min(rows, n - r0);
+    DS_CK(cudaEventRecord(c->ev[1], s));
+    DS_CK(launch_dist((const float*)c->rec.p, n, d, r0, rb, (float*)c->dist.p, s));
+    DS_CK(cudaEventRecord(c->ev[2], s));
+    DS_CK(cudaMemcpy2DAsync(out + r0 * n, (size_t)n * 4, c->dist.p, (size_t)pitch * 4,
+                            (size_t)n * 4, (size_t)rb, cudaMemcpyDeviceToHost, s));
+    DS_CK(cudaStreamSynchronize(s));
+    float k = 0.f;
+    DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    kernel_ms += k;
+  }
+  if (t) {
+    ds_timings local{};
+    local.tile_ms = kernel_ms;
+    local.pairs_evaluated = n * n;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
+  }
+  return DS_OK;
+}
+
+ds_status ds_dist_threshold(ds_ctx* c, const float* dist, int64_t n, double eps_sq, int64_t min_pts,
+                            int64_t mem_cap, uint8_t* bits_out, int64_t* counts_out,
+                            uint8_t* valid_out, ds_timings* t) {
+  if (!c || !dist || !bits_out || !counts_out) {
+    set_error("ctx, dist, bits_out and counts_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  const int64_t rb_bytes = (n + 7) / 8;
+  st = ladder_capacity(n * rb_bytes, mem_cap, "the n x ceil(n/8) neighbourhood matrix");
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  const float eps32 = (float)eps_sq;  // kernels.py:297
+  const int64_t pitch = dist_pitch(n), rows = dist_rows_per_block(n);
+  DS_CK(ensure(c->dist, (size_t)rows * pitch * 4));
+  DS_CK(ensure(c->dbits, (size_t)rows * rb_bytes));
+  DS_CK(ensure(c->counts64, (size_t)n * 8));
+  float kernel_ms = 0.f;
+  for (int64_t r0 = 0; r0 < n; r0 += rows) {
+    const int64_t rb = std::min(rows, n - r0);
+    DS_CK(cudaMemcpy2DAsync(c->dist.p, (size_t)pitch * 4, dist + r0 * n, (size_t)n * 4,
+                            (size_t)n * 4, (size_t)rb, cudaMemcpyHostToDevice, s));
+    DS_CK(cudaEventRecord(c->ev[1], s));
+    DS_CK(launch_threshold((const float*)c->dist.p, n, rb, eps32, (uint8_t*)c->dbits.p,
+                           (int64_t*)c->counts64.p + r0, s));
+    DS_CK(cudaEventRecord(c->ev[2], s));
+    DS_CK(cudaMemcpyAsync(bits_out + r0 * rb_bytes, c->dbits.p, (size_t)rb * rb_bytes,
+                          cudaMemcpyDeviceToHost, s));
+    DS_CK(cudaStreamSynchronize(s));
+    float k = 0.f;
+    DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    kernel_ms += k;
+  }
+  DS_CK(cudaMemcpy(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  if (valid_out)
+    for (int64_t i = 0; i < n; ++i) valid_out[i] = counts_out[i] >= min_pts ? 1 : 0;
+  if (t) {
+    ds_timings local{};
+    local.merge_ms = kernel_ms;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
+  }
+  return DS_OK;
+}
+
+ds_status ds_dist_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, double eps_sq,
+                        int64_t min_pts, int64_t mem_cap, uint8_t* bits_out, int64_t* counts_out,
+                        uint8_t* valid_out, ds_timings* t) {
+  if (!c || !coords || !bits_out || !counts_out) {
+    set_error("ctx, coords, bits_out and counts_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  const int64_t rb_bytes = (n + 7) / 8;
+  st = ladder_capacity(4 * n * n, mem_cap, "the n x n float32 distance matrix");
+  if (st != DS_OK) return st;
+  st = ladder_capacity(n * rb_bytes, mem_cap, "the n x ceil(n/8) neighbourhood matrix");
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  st = ladder_prep(c, coords, n, d);
+  if (st != DS_OK) return st;
+  const float eps32 = (float)eps_sq;
+  const int64_t pitch = dist_pitch(n), rows = dist_rows_per_block(n);
+  DS_CK(ensure(c->dist, (size_t)rows * pitch * 4));
+  DS_CK(ensure(c->dbits, (size_t)n * rb_bytes));
+  DS_CK(ensure(c->counts64, (size_t)n * 8));
+  float dist_ms = 0.f, thr_ms = 0.f;
+  for (int64_t r0 = 0; r0 < n; r0 += rows) {
+    const int64_t rb = std::min(rows, n - r0);
+    DS_CK(cudaEventRecord(c->ev[1], s));
+    DS_CK(launch_dist((const float*)c->rec.p, n, d, r0, rb, (float*)c->dist.p, s));
+    DS_CK(cudaEventRecord(c->ev[2], s));
+    DS_CK(launch_threshold((const float*)c->dist.p, n, rb, eps32,
+                           (uint8_t*)c->dbits.p + r0 * rb_bytes, (int64_t*)c->counts64.p + r0, s));
+    DS_CK(cudaEventRecord(c->ev[3], s));
+    DS_CK(cudaEventSynchronize(c->ev[3]));
+    float a = 0.f, b = 0.f;
+    DS_CK(cudaEventElapsedTime(&a, c->ev[1], c->ev[2]));
+    DS_CK(cudaEventElapsedTime(&b, c->ev[2], c->ev[3]));
+    dist_ms += a;
+    thr_ms += b;
+  }
+  DS_CK(cudaMemcpyAsync(bits_out, c->dbits.p, (size_t)n * rb_bytes, cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  if (valid_out)
+    for (int64_t i = 0; i < n; ++i) valid_out[i] = counts_out[i] >= min_pts ? 1 : 0;
+  if (t) {
+    ds_timings local{};
+    local.tile_ms = dist_ms;
+    local.merge_ms = thr_ms;
+    local.pairs_evaluated = n * n;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
   }
   return DS_OK;
 }

@@ -191,6 +191,15 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
                                 size_t temp_bytes, unsigned int* bbox, cudaStream_t s);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
+// ---- materialising ladder (ds_dist.cu) -----------------------------------------
+int64_t dist_pitch(int64_t n);  // floats per device matrix row (roundup4(n))
+// rows [row0, row0 + rows) of the direct-formula n x n matrix into out (pitch floats)
+cudaError_t launch_dist(const float* rec, int64_t n, int d, int64_t row0, int64_t rows,
+                        float* out, cudaStream_t s);
+// bits (rows x ceil(n/8), packbits layout) and int64 counts of out-of-pitch rows
+cudaError_t launch_threshold(const float* dist, int64_t n, int64_t rows, float eps32, uint8_t* bits,
+                             int64_t* counts, cudaStream_t s);
+
 // ---- error plumbing (ds_api.cu) -----------------------------------------------
 void set_error(const std::string& msg);
 void set_capacity(int64_t required, int64_t cap);

@@ -2,13 +2,18 @@
 
 Mirrors the reference module `densescan.kernels` (pkg/src/densescan/
 kernels.py): the same VariantId ladder, KernelVariant validation, result
-containers and CapacityExceeded error. The computation runs in the sm_100a
-eps-tile kernel (csrc/ds_tile.cu); the variant only selects the formula:
+containers and CapacityExceeded error. The computation runs in sm_100a
+kernels; the variant selects the formula and whether the distance matrix is
+materialised:
 
-  FUSED_ALGEBRAIC                 -> algebraic T + P - (X*x + Y*y + ...)  (default)
-  FUSED, BASELINE, SOA, TILED,    -> direct ((dx^2 + dy^2) + ...); the four
-  TILED_UNROLLED                     materialising rungs compute exactly these
-                                     values (kernels.py:21-25)
+  FUSED_ALGEBRAIC                 -> eps-tile kernel (csrc/ds_tile.cu), algebraic
+                                     T + P - (X*x + Y*y + ...)  (default)
+  FUSED                           -> eps-tile kernel, direct ((dx^2 + dy^2) + ...)
+  BASELINE, SOA, TILED,           -> the n x n float32 direct-formula matrix in HBM
+  TILED_UNROLLED                     (csrc/ds_dist.cu), thresholded into bits; the
+                                     four rungs compute exactly these values
+                                     (kernels.py:21-25), so do dist_baseline /
+                                     dist_soa / dist_tiled
 
 `tile_size` / `unroll_width` are validated exactly as in the reference but,
 as there, never change a result (the device tiling is fixed at 512).
@@ -98,6 +103,14 @@ class KernelVariant:
 
 
 @dataclass
+class DistSqMatrix:
+    """Dense float32 matrix of pairwise squared Euclidean distances (kernels.py:113-118)."""
+
+    n: int
+    values: np.ndarray
+
+
+@dataclass
 class NeighborhoodMatrix:
     """Bit-packed boolean matrix, reference layout (kernels.py:120-137).
 
@@ -161,22 +174,69 @@ def fused_build_algebraic(points: PointSet, params: DbscanParams, variant: Kerne
     return nbr, valid
 
 
+# ---- materialising ladder (kernels.py:153-308) -------------------------------------
+# All four rungs compute the same direct-formula values (kernels.py:21-25): on the
+# device they are one HBM-write-bound kernel (csrc/ds_dist.cu); the rungs differ
+# only in the reference's CPU memory access pattern, which has no device analogue.
+
+def _dist(points: PointSet, mem_cap, device=None) -> DistSqMatrix:
+    n = points.n
+    ensure_capacity(4 * n * n, mem_cap)  # kernels.py:156 / 262
+    ctx = _native.context(device)
+    values, _ = ctx.dist_matrix(points.coords_aos, 0)
+    return DistSqMatrix(n=n, values=values)
+
+
+def dist_baseline(points: PointSet, threads: int = 1, mem_cap=None) -> DistSqMatrix:
+    """Ladder rung 0 (kernels.py:177-180): the direct-formula matrix, on the GPU."""
+    return _dist(points, mem_cap)
+
+
+def dist_soa(points: PointSet, threads: int = 1, mem_cap=None) -> DistSqMatrix:
+    """Ladder rung 1 (kernels.py:183-185): identical values to dist_baseline."""
+    return _dist(points, mem_cap)
+
+
+def dist_tiled(points: PointSet, variant: KernelVariant, threads: int = 1,
+               mem_cap=None) -> DistSqMatrix:
+    """Ladder rungs 2-3 (kernels.py:251-281): identical values to dist_baseline."""
+    if variant.id not in (VariantId.TILED, VariantId.TILED_UNROLLED):
+        raise ValueError(f"dist_tiled cannot run variant {variant.id.value}")
+    return _dist(points, mem_cap)
+
+
+def build_clusters_from_dist(dist: DistSqMatrix, params: DbscanParams,
+                             threads: int = 1, mem_cap=None):
+    """Stage 2 from a materialised matrix (kernels.py:284-308), on the GPU:
+    bit (i, j) iff values[i, j] <= float32(eps_sq); (NeighborhoodMatrix, ValidVector)."""
+    n = dist.n
+    ensure_capacity(n * row_bytes(n), mem_cap)  # kernels.py:293
+    ctx = _native.context()
+    bits, counts, valid, _ = ctx.dist_threshold(dist.values, params.eps_sq, params.min_pts, 0)
+    return (NeighborhoodMatrix(n=n, bits=bits, neighbor_count=counts),
+            ValidVector(valid=valid, min_pts=params.min_pts))
+
+
 def run_variant(points: PointSet, params: DbscanParams, variant: KernelVariant,
                 threads: int = 1, mem_cap=None):
     """One ladder rung to (NeighborhoodMatrix, ValidVector) plus stage times
     (kernels.py:445-470): (nbr, valid, dist_ms, cluster_ms, fused_ms).
 
-    Device times from CUDA events. For the materialising rungs the same
-    eps-tile kernel runs with the direct formula (their values are bitwise the
-    direct formula's); dist_ms reports the tile kernel and cluster_ms the rest
-    of stage 1+2.
+    Device times from CUDA events. The materialising rungs build the float32
+    matrix in HBM (ds_dist_build: dist_ms = distance kernel, cluster_ms =
+    threshold kernel) and never copy it to the host; the fused rungs run the
+    eps-tile kernel (fused_ms = stage 1+2).
     """
     if variant.materializes_distance():
-        # the reference would allocate the 4 n^2 float matrix here (kernels.py:156)
-        ensure_capacity(4 * points.n * points.n, mem_cap)
+        n = points.n
+        ensure_capacity(4 * n * n, mem_cap)  # kernels.py:156 / 262
+        ensure_capacity(n * row_bytes(n), mem_cap)  # kernels.py:293
+        ctx = _native.context()
+        bits, counts, valid, t = ctx.dist_build(points.coords_aos, params.eps_sq,
+                                                params.min_pts, 0)
+        return (NeighborhoodMatrix(n=n, bits=bits, neighbor_count=counts),
+                ValidVector(valid=valid, min_pts=params.min_pts), t.tile_ms, t.merge_ms, None)
     nbr, valid, t = _fused(points, params, variant.formula, mem_cap)
-    if variant.materializes_distance():
-        return nbr, valid, t.tile_ms, max(t.fused_ms - t.tile_ms, 0.0), None
     return nbr, valid, None, None, t.fused_ms
 
 
