@@ -59,6 +59,15 @@ struct Scalars {
   int32_t units32;
 };
 
+// The per-call zero region: one memset clears the scalars, the spatial-sort bounding
+// box, the diagonal directory index and the label scan's look-back state.
+constexpr size_t ZR_ALIGN = 256;
+inline size_t zr_round(size_t b) { return (b + ZR_ALIGN - 1) / ZR_ALIGN * ZR_ALIGN; }
+inline size_t zr_bbox() { return zr_round(sizeof(Scalars)); }
+inline size_t zr_diag() { return zr_bbox() + ZR_ALIGN; }
+inline size_t zr_scan(int64_t n) { return zr_diag() + zr_round((size_t)n_tiles(n) * 4); }
+inline size_t zr_bytes(int64_t n) { return zr_scan(n) + (size_t)scan_partials_len(n) * 4; }
+
 }  // namespace
 
 struct ds_ctx {
@@ -176,9 +185,10 @@ MergeWs merge_ws(ds_ctx* c, int64_t n) {
   w.root = (int32_t*)c->root.p;
   w.flag = (int32_t*)c->flag.p;
   w.partials = (int32_t*)c->partials.p;
+  w.scan_state = (int32_t*)((char*)c->scalars.p + zr_scan(n));  // zeroed per call
   w.nclusters = &sc->nclusters;
   w.ncore = &sc->ncore;
-  w.diag_idx = (int32_t*)c->diag.p;
+  w.diag_idx = (int32_t*)((char*)c->scalars.p + zr_diag());
   if (c->sorted) {
     w.perm = (const int32_t*)c->perm.p;
     w.inv = (const int32_t*)c->inv.p;
@@ -198,9 +208,8 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->root, N * 4));
   DS_CK(ensure(c->flag, N * 4));
   DS_CK(ensure(c->partials, (size_t)scan_partials_len(n) * 4));
-  DS_CK(ensure(c->scalars, sizeof(Scalars)));
+  DS_CK(ensure(c->scalars, zr_bytes(n)));
   DS_CK(ensure(c->chunks, (size_t)n_items(n_tiles(n)) * 16));  // tile-pair directory
-  DS_CK(ensure(c->diag, (size_t)n_tiles(n) * 4));
   return DS_OK;
 }
 
@@ -224,9 +233,11 @@ struct Plan {
 // waits for the device: the adjacency-word buffer is sized from what earlier calls
 // needed, and an overflow (detected by check_words after the caller's single sync)
 // triggers one re-run with the exact size.
+// core_min_pts >= 1: the directory launch also initialises the core flags and the
+// union-find (single GPU, where the counts are complete after stage 1).
 ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                           int formula, int64_t mem_cap, cudaStream_t s, Plan& pl, int rank = 0,
-                          int world = 1) {
+                          int world = 1, int64_t core_min_pts = 0) {
   ds_status st = alloc_common(c, n, d);
   if (st != DS_OK) return st;
   if (world < 1 || rank < 0 || rank >= world) {
@@ -279,14 +290,25 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   Scalars* sc = (Scalars*)c->scalars.p;
   const float eps32 = (float)eps_sq;  // float32(float64 eps^2), RN (kernels.py:355/385)
 
-  DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
-  DS_CK(cudaMemsetAsync(c->cnt.p, 0, (size_t)n * 4, s));
+  DS_CK(cudaMemsetAsync(c->scalars.p, 0, zr_bytes(n), s));  // the zero region (cnt: prep)
   const bool do_sort = c->sort && T > 1;
-  if (do_sort) DS_CK(ensure(c->bbox, 64));
-  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag,
-                    do_sort ? (unsigned int*)c->bbox.p : nullptr, s));
+  unsigned int* bbox = (unsigned int*)((char*)c->scalars.p + zr_bbox());
+  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, do_sort ? bbox : nullptr,
+                    (int32_t*)c->cnt.p, s));
   const float* rec = (const float*)c->rec.p;
   c->sorted = false;
+  const int dp = padded_dim(d);
+  SortBounds bnd;  // with culling on, the sort's permute pass also reduces the boxes
+  if (pl.cull) {
+    DS_CK(ensure(c->tbox, (size_t)T * (2 * dp + 1) * 4));
+    DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * dp + 1) * 4));
+    if (do_sort) {
+      bnd.lo = (float*)c->tbox.p;
+      bnd.hi = bnd.lo + (size_t)T * dp;
+      bnd.maxnorm = bnd.lo + (size_t)T * 2 * dp;
+      bnd.blk = dp <= 4 ? (float*)c->blk.p : nullptr;  // block boxes only pay off at d <= 4
+    }
+  }
   if (do_sort) {  // Morton order: compact tiles (ds_sort.cu)
     const size_t N = (size_t)n;
     DS_CK(ensure(c->rec_sorted, N * rec_stride(d) * 4));
@@ -299,20 +321,19 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     DS_CK(launch_spatial_sort(rec, n, d, (float*)c->rec_sorted.p, (int32_t*)c->perm.p,
                               (int32_t*)c->inv.p, (unsigned long long*)c->keys.p,
                               (unsigned long long*)c->keys_alt.p, (int32_t*)c->kidx.p,
-                              c->sort_temp.p, c->sort_temp.bytes, (unsigned int*)c->bbox.p, s));
+                              c->sort_temp.p, c->sort_temp.bytes, bbox, bnd,
+                              s));
     rec = (const float*)c->rec_sorted.p;
     c->sorted = true;
   }
   if (pl.cull) {
-    const int dp = padded_dim(d);
-    DS_CK(ensure(c->tbox, (size_t)T * (2 * dp + 1) * 4));
     DS_CK(ensure(c->items, (size_t)pl.all_items * 4));
     DS_CK(ensure(c->iflags, (size_t)pl.all_items * 4));
     DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(pl.all_items) * 4));
     float* lo = (float*)c->tbox.p;
     DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo, lo + (size_t)T * dp,
                       lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p,
-                      &sc->kept32, (uint32_t*)c->items.p, &sc->kept, s));
+                      &sc->kept32, (uint32_t*)c->items.p, &sc->kept, bnd.lo != nullptr, s));
   }
   UnitArgs a;
   a.rec = rec;
@@ -334,9 +355,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.work_ctr = &sc->work_ctr;
   a.unit_list = nullptr;
   if (pl.cull) {
-    const int dp = padded_dim(d);
-    DS_CK(ensure(c->blk, (size_t)((n + 31) / 32) * (2 * dp + 1) * 4));
-    DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
+    if (!bnd.lo && dp <= 4) DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
     DS_CK(ensure(c->ucnt, (size_t)pl.all_items * 8));  // item_units
     DS_CK(ensure(c->ulist, (size_t)pl.units_cap * 8));
     c->units_cap = pl.units_cap;
@@ -353,8 +372,22 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
   DS_CK(record(c, c->ev[2], s));
+  CoreInit ci;
+  if (core_min_pts >= 1) {
+    const MergeWs w = merge_ws(c, n);
+    ci.cnt = w.cnt;
+    ci.n = n;
+    ci.min_pts = core_min_pts;
+    ci.core = w.core;
+    ci.corew = w.corew;
+    ci.parent = w.parent;
+    ci.bmin = w.bmin;
+    ci.cmin = w.cmin;
+    ci.ncore = w.ncore;
+  }
   DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const uint2*)c->ucnt.p : nullptr,
-                        &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count, s));
+                        &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count,
+                        (int32_t*)((char*)c->scalars.p + zr_diag()), ci, s));
   return DS_OK;
 }
 
@@ -421,11 +454,11 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   c->capturing = captured;
   auto rec = [&](cudaEvent_t e) { return record(c, e, s); };
   DS_CK(rec(c->ev[0]));
-  ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl);
+  ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl, 0, 1, min_pts);
   if (st != DS_OK) return st;
   MergeWs w = merge_ws(c, n);
+  w.scan_zeroed = true;
   Scalars* sc = (Scalars*)c->scalars.p;
-  DS_CK(launch_core_init(w, min_pts, s));
   DS_CK(rec(c->ev[3]));
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, (const uint4*)c->chunks.p,
                             &sc->nonempty_count, s));
@@ -931,7 +964,7 @@ ds_status ladder_prep(ds_ctx* c, const double* coords, int64_t n, int32_t d) {
   DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
   DS_CK(launch_prep((const double*)c->coords64.p, n, d, (float*)c->rec.p,
-                    &((Scalars*)c->scalars.p)->unsafe_flag, nullptr, s));
+                    &((Scalars*)c->scalars.p)->unsafe_flag, nullptr, nullptr, s));
   return DS_OK;
 }
 

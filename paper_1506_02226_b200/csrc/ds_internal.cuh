@@ -83,6 +83,30 @@ struct UnitArgs {
   unsigned long long* work_ctr;         // batch counter (zeroed before the launch)
 };
 
+// ---- programmatic dependent launch ------------------------------------------------
+// Pipeline kernels are launched with programmatic stream serialization: a kernel may
+// be scheduled while its predecessor in the stream drains (hiding the launch and
+// CTA ramp of ~20 small dependent kernels per call); each such kernel executes
+// griddep_wait() first, which returns once the predecessor grid has completed and
+// its memory is visible (a no-op for an ordinary launch).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ---- item <-> tile pair: items enumerate the upper triangle a <= b in row order ----
 __device__ __forceinline__ int64_t row_offset(int64_t a, int64_t T) {
   return a * T - a * (a - 1) / 2;
@@ -119,10 +143,12 @@ __device__ __forceinline__ unsigned int ord_bits(float f) {
 }
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
-// bbox (nullable): 8 uints {ord lo[4], ord hi[4]} of the first min(d, 4) dimensions,
-// reset here and reduced by the kernel (the spatial sort's grid)
+// bbox (nullable): 8 uints {~ord lo[4], ord hi[4]} of the first min(d, 4) dimensions
+// (the spatial sort's grid).
+// bbox words must be zero on entry (lo is stored as ~ord_bits, hi as ord_bits, so
+// both reduce with atomicMax); cnt (nullable): zeroed here for stage 1's counts
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
-                        unsigned int* bbox, cudaStream_t s);
+                        unsigned int* bbox, int32_t* cnt, cudaStream_t s);
 cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
                                 cudaStream_t s);
 // culled schedule: the row-unit list of this shard (kept items q = rank + k * world),
@@ -133,16 +159,32 @@ cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, in
                              uint2* unit_list, unsigned long long units_cap,
                              unsigned long long* unit_count, uint2* item_units, cudaStream_t s);
 // per tile pair with words: {a << 16 | b, first unit lo, units, first unit hi} (atomic append)
+// core_init's job (core flags, core words, union-find init), optionally fused into the
+// directory launch (single GPU: the counts are complete after the eps-tile kernel)
+struct CoreInit {
+  const int32_t* cnt = nullptr;  // nullptr: skip
+  int64_t n = 0, min_pts = 0;
+  uint8_t* core = nullptr;
+  uint32_t* corew = nullptr;
+  int32_t* parent = nullptr;
+  int32_t* bmin = nullptr;
+  int32_t* cmin = nullptr;
+  unsigned long long* ncore = nullptr;
+};
+// also fills diag_idx[T] (1 + directory index of each diagonal tile pair; 0 = none,
+// the array must be zero on entry)
 cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
-                            unsigned long long* dir_count, cudaStream_t s);
+                            unsigned long long* dir_count, int32_t* diag_idx, const CoreInit& ci,
+                            cudaStream_t s);
 // 32-point block boxes [block][lo(dpad), hi(dpad), maxnorm] for sub-tile culling
 cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s);
 // tile bounding boxes + list of tile pairs that are not provably empty
+// bounds_ready: lo / hi / maxnorm were filled by the spatial sort (SortBounds)
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
                         int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
-                        unsigned long long* count, cudaStream_t s);
+                        unsigned long long* count, bool bounds_ready, cudaStream_t s);
 // exclusive prefix sum of int32 data in place (3 kernels); *total = sum
 cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
                                   cudaStream_t s);
@@ -159,7 +201,9 @@ struct MergeWs {
   int32_t* cmin;
   int32_t* root;
   int32_t* flag;          // flags, then exclusive scan (cluster ids)
-  int32_t* partials;      // scan block partials
+  int32_t* partials;      // scan workspace (scan_partials_len ints)
+  int32_t* scan_state = nullptr;  // label-scan look-back state in the per-call zero region
+  bool scan_zeroed = false;       // scan_state was zeroed by the call's zero-region memset
   int32_t* nclusters;     // device scalar
   unsigned long long* ncore;
   int32_t* diag_idx = nullptr;    // dir index of each diagonal tile pair (-1: none)
@@ -185,10 +229,18 @@ cudaError_t launch_permute_i32(const int32_t* src, int64_t n, const int32_t* per
                                int32_t* dst, cudaStream_t s);
 // ---- spatial order (ds_sort.cu) -----------------------------------------------
 size_t sort_temp_bytes(int64_t n);
+// culling bounds computed while permuting (lo == nullptr: plain permute)
+struct SortBounds {
+  float* lo = nullptr;       // T x dpad tile boxes
+  float* hi = nullptr;
+  float* maxnorm = nullptr;  // T max squared norms
+  float* blk = nullptr;      // 32-point block boxes (nullptr: skip)
+};
 cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
                                 int32_t* perm, int32_t* inv, unsigned long long* keys,
                                 unsigned long long* keys_alt, int32_t* idx, void* temp,
-                                size_t temp_bytes, unsigned int* bbox, cudaStream_t s);
+                                size_t temp_bytes, unsigned int* bbox, const SortBounds& bnd,
+                                cudaStream_t s);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
 // ---- materialising ladder (ds_dist.cu) -----------------------------------------

@@ -249,23 +249,13 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 }
 
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
-__global__ void diag_index_kernel(const uint4* __restrict__ dir,
-                                  const unsigned long long* __restrict__ ndir,
-                                  int32_t* __restrict__ diag_idx) {
-  const unsigned long long total = *ndir;
-  for (unsigned long long c = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; c < total;
-       c += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t ab = dir[c].x;
-    if ((ab >> 16) == (ab & 0xffffu)) diag_idx[ab >> 16] = (int32_t)c;
-  }
-}
-
 __global__ void __launch_bounds__(512) union_diag_kernel(
     const uint4* __restrict__ dir, const uint2* __restrict__ uchunks,
     const int32_t* __restrict__ diag_idx, int64_t ntiles,
     const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
     const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
+  griddep_wait();
   constexpr int THREADS = 512;
   constexpr int RB = TILE / (THREADS / WPR);  // rows per block: 16
   extern __shared__ uint32_t dsm[];
@@ -283,7 +273,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   const int w = tid % WPR, cblk = tid / WPR;
   const int64_t nw = (n + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int c = diag_idx[tile];
+    const int c = diag_idx[tile] - 1;  // 0 = no diagonal chunk
     if (c < 0) continue;  // uniform per CTA
     const DirInfo ci = decode_dir(dir[c]);
     load_item_words(ci, uchunks, words_cap, iw);
@@ -461,6 +451,7 @@ constexpr int LINK_WARPS = 8;
 __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
     const UnitArgs A, int LB, const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
+  griddep_wait();
   __shared__ int rows_sh[LINK_WARPS][TILE / WPR * 4];  // up to 128 rows per lane block
   __shared__ int cols_sh[LINK_WARPS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -601,6 +592,7 @@ __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __
                              const int32_t* __restrict__ bmin, int64_t n,
                              const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
                              int32_t* __restrict__ root, int32_t* cmin) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int r = -1, o = NONE;
   if (i < n) {
@@ -618,16 +610,6 @@ __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __
   const unsigned grp = __match_any_sync(0xffffffffu, r);
   const int m = (int)__reduce_min_sync(grp, (unsigned)o);  // o >= 0
   if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicMin(&cmin[r], m);
-}
-
-// flag[o] = 1 iff original index o is the first appearance of its cluster
-__global__ void flags_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
-                             int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ flag) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int r = root[i];
-  const int o = perm ? perm[i] : (int)i;
-  flag[o] = (r >= 0 && cmin[r] == o) ? 1 : 0;
 }
 
 // block-wide exclusive scan of one int per thread; also returns the block total
@@ -666,10 +648,30 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
 // over the predecessors' published {flag, value} words until it meets an inclusive
 // prefix, and publishes its own. state[] and the ticket are zeroed before the launch.
 constexpr unsigned long long SC_AGG = 1ull << 62, SC_PRE = 2ull << 62;
-__global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(int32_t* data, int64_t n,
+
+// scan input: the array itself
+struct ScanInPlace {
+  const int32_t* data;
+  __device__ __forceinline__ int operator()(int64_t i) const { return data[i]; }
+};
+// scan input for canonical ids: 1 iff original index o is the first appearance
+// (lowest ORIGINAL member) of its cluster (core.py:116-132)
+struct ScanFirstAppearance {
+  const int32_t* root;  // sorted order
+  const int32_t* cmin;
+  const int32_t* inv;   // original -> sorted (nullptr: identity)
+  __device__ __forceinline__ int operator()(int64_t o) const {
+    const int r = root[inv ? inv[o] : o];
+    return (r >= 0 && cmin[r] == (int)o) ? 1 : 0;
+  }
+};
+
+template <class In>
+__global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* data, int64_t n,
                                                                unsigned int* ticket,
                                                                unsigned long long* state,
                                                                int32_t* total) {
+  griddep_wait();
   __shared__ unsigned int tile_sh;
   __shared__ int prefix_sh;
   if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
@@ -680,7 +682,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(int32_t* data, in
   int sum = 0;
 #pragma unroll
   for (int k = 0; k < SCAN_PER; ++k) {
-    v[k] = base + k < n ? data[base + k] : 0;
+    v[k] = base + k < n ? in(base + k) : 0;
     sum += v[k];
   }
   int agg;
@@ -717,6 +719,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(int32_t* data, in
 __global__ void label_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
                              const int32_t* __restrict__ id, int64_t n,
                              const int32_t* __restrict__ perm, int64_t* __restrict__ labels) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int r = root[i];
@@ -811,17 +814,15 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
     diag_cfg = true;
   }
   const int64_t ntiles = (w.n + TILE - 1) / TILE;
-  cudaError_t e = cudaMemsetAsync(w.diag_idx, 0xff, (size_t)ntiles * 4, s);
-  if (e != cudaSuccess) return e;
-  diag_index_kernel<<<sms, 256, 0, s>>>(dir, ndir, w.diag_idx);
+  // diag_idx was filled by the directory launch (launch_unit_dir)
   // one CTA per tile (one wave: up to 4 resident per SM)
   const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
-  union_diag_kernel<<<(unsigned)grid, 512, diag_smem, s>>>(dir, uchunks, w.diag_idx, ntiles,
-                                                          words, words_cap, w.n, w.corew,
-                                                          w.parent, w.bmin, w.perm);
-  union_links_kernel<<<sms * 8, LINK_WARPS * 32, 0, s>>>(units, lane_blocks, w.corew, w.parent,
-                                                         w.bmin, w.perm);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(union_diag_kernel, dim3((unsigned)grid), dim3(512), diag_smem, s, dir,
+                             uchunks, (const int32_t*)w.diag_idx, ntiles, words, words_cap, w.n,
+                             (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(union_links_kernel, dim3(sms * 8), dim3(LINK_WARPS * 32), 0, s, units,
+                    lane_blocks, (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
 }
 
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
@@ -837,12 +838,23 @@ cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
   const int t = 256;
   const unsigned b = blocks_for(w.n, t);
-  roots_kernel<<<b, t, 0, s>>>(w.core, w.parent, w.bmin, w.n, w.perm, w.inv, w.root, w.cmin);
-  flags_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.n, w.perm, w.flag);
-  cudaError_t e = launch_exclusive_scan(w.flag, w.n, w.partials, w.nclusters, s);
+  // canonical ids: exclusive scan of the first-appearance flags, in original order; its
+  // look-back state is zeroed first so that roots -> scan -> label chain directly
+  const int64_t tiles = (w.n + SCAN_BLK - 1) / SCAN_BLK;
+  int32_t* state = w.scan_zeroed ? w.scan_state : w.partials;
+  cudaError_t e = w.scan_zeroed ? cudaSuccess
+                                : cudaMemsetAsync(state, 0, (size_t)(tiles + 1) * 8, s);
   if (e != cudaSuccess) return e;
-  label_kernel<<<b, t, 0, s>>>(w.root, w.cmin, w.flag, w.n, w.perm, labels);
-  return cudaGetLastError();
+  e = launch_pdl(roots_kernel, dim3(b), dim3(t), 0, s, (const uint8_t*)w.core,
+                 (const int32_t*)w.parent, (const int32_t*)w.bmin, w.n, w.perm, w.inv, w.root, w.cmin);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(scan_lookback_kernel<ScanFirstAppearance>, dim3((unsigned)tiles), dim3(SCAN_T), 0, s,
+                 ScanFirstAppearance{w.root, w.cmin, w.inv}, w.flag, w.n,
+                 reinterpret_cast<unsigned int*>(state),
+                 reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(label_kernel, dim3(b), dim3(t), 0, s, (const int32_t*)w.root,
+                    (const int32_t*)w.cmin, (const int32_t*)w.flag, w.n, w.perm, labels);
 }
 
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R,
@@ -879,7 +891,7 @@ cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, i
   cudaError_t e = cudaMemsetAsync(partials, 0, (size_t)(tiles + 1) * 8, s);
   if (e != cudaSuccess) return e;
   scan_lookback_kernel<<<(unsigned)tiles, SCAN_T, 0, s>>>(
-      data, n, reinterpret_cast<unsigned int*>(partials),
+      ScanInPlace{data}, data, n, reinterpret_cast<unsigned int*>(partials),
       reinterpret_cast<unsigned long long*>(partials) + 1, total);
   return cudaGetLastError();
 }

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ds_internal.cuh"
 
 namespace ds {
@@ -308,6 +310,7 @@ __device__ __forceinline__ void cp_async_wait() {
 //     blocks without a single bit (most of a dense schedule) skip both.
 template <int D, int F, bool SAFE>
 __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
+  griddep_wait();
   using G = Geo<D>;
   constexpr int KP = G::KP;
   constexpr int S = G::S;
@@ -653,6 +656,7 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
     const unsigned long long* __restrict__ kept, int rank, int world, uint2* __restrict__ list,
     unsigned long long cap, unsigned long long* __restrict__ unit_count,
     uint2* __restrict__ item_units) {
+  griddep_wait();
   constexpr int W = 8;  // warps per CTA; one list reservation per CTA and round
   __shared__ int wcnt[W];
   __shared__ unsigned long long wpos[W];
@@ -717,10 +721,16 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
 // Per item: its row units [lo, hi) (culled: item_units of this shard's items; dense:
 // the triangle order, clipped to the shard) own chunk entries [lo * WPR, hi * WPR);
 // the item gets a directory entry if any of them holds words.
+// Diagonal tile pairs also record their directory index (diag_idx[a], -1 preset)
+// for union_diag_kernel. With ci.cnt set, the same launch also does core_init's job
+// (ds_merge.cu): core flags, core words, union-find and border-minimum init, one
+// warp per 32 points after the items.
 template <int KP>
 __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2* __restrict__ item_units,
                                 const unsigned long long* __restrict__ kept, uint4* __restrict__ dir,
-                                unsigned long long* __restrict__ dir_count) {
+                                unsigned long long* __restrict__ dir_count,
+                                int32_t* __restrict__ diag_idx, const CoreInit ci) {
+  griddep_wait();
   constexpr int LB = TILE / (32 * KP);
   long long r_lo, r_hi;
   unit_range(A, r_lo, r_hi);
@@ -756,9 +766,28 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2
       } else {
         decode_item(q, A.T, a, b);
       }
-      const unsigned long long ci = atomicAdd(dir_count, 1ull);
-      dir[ci] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)c_lo, (uint32_t)(c_hi - c_lo),
-                           (uint32_t)((unsigned long long)c_lo >> 32));
+      const unsigned long long e = atomicAdd(dir_count, 1ull);
+      dir[e] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)c_lo, (uint32_t)(c_hi - c_lo),
+                          (uint32_t)((unsigned long long)c_lo >> 32));
+      if (a == b) diag_idx[a] = (int32_t)e + 1;
+    }
+  }
+  if (ci.cnt) {  // core_init (kernels.py:335): warp per 32 points
+    const int64_t nb = (ci.n + 31) / 32;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nb; w += nwarps) {
+      const int64_t i = w * 32 + lane;
+      const bool c = i < ci.n && (int64_t)ci.cnt[i] >= ci.min_pts;
+      const uint32_t ballot = __ballot_sync(0xffffffffu, c);
+      if (i < ci.n) {
+        ci.core[i] = c ? 1 : 0;
+        ci.parent[i] = (int32_t)i;
+        ci.bmin[i] = NONE;
+        ci.cmin[i] = NONE;
+      }
+      if (lane == 0) {
+        ci.corew[w] = __brev(ballot);  // bit 31 - t <-> point 32w + t
+        if (ballot) atomicAdd(ci.ncore, (unsigned long long)__popc(ballot));
+      }
     }
   }
 }
@@ -770,7 +799,9 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2
 __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ coords, int64_t n,
                                                    int d, int dpad, int S, float* __restrict__ rec,
                                                    uint32_t* unsafe_flag,
-                                                   unsigned int* __restrict__ bbox) {
+                                                   unsigned int* __restrict__ bbox,
+                                                   int32_t* __restrict__ cnt) {
+  griddep_wait();
   float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
@@ -792,12 +823,13 @@ __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ co
     }
     dst[dpad] = p;
     for (int c = dpad + 1; c < S; ++c) dst[c] = 0.f;
+    if (cnt) cnt[i] = 0;
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(unsafe_flag, 1u);
   if (!bbox) return;
-  __shared__ unsigned int smn[4], smx[4];
+  __shared__ unsigned int smn[4], smx[4];  // smn holds ~ord(min): both reduce with max
   if (threadIdx.x < 4) {
-    smn[threadIdx.x] = 0xffffffffu;
+    smn[threadIdx.x] = 0u;
     smx[threadIdx.x] = 0u;
   }
   __syncthreads();
@@ -810,13 +842,13 @@ __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ co
       b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, off));
     }
     if ((threadIdx.x & 31) == 0) {
-      atomicMin(&smn[k], ord_bits(a));
+      atomicMax(&smn[k], ~ord_bits(a));
       atomicMax(&smx[k], ord_bits(b));
     }
   }
   __syncthreads();
   if (threadIdx.x < kd) {
-    atomicMin(&bbox[threadIdx.x], smn[threadIdx.x]);
+    atomicMax(&bbox[threadIdx.x], smn[threadIdx.x]);
     atomicMax(&bbox[4 + threadIdx.x], smx[threadIdx.x]);
   }
 }
@@ -956,6 +988,77 @@ __global__ void cull_scatter_kernel(const float* __restrict__ lo, const float* _
   }
 }
 
+// Row-wise culling for T <= CULL_ROWS_MAX tiles (two launches instead of flags + scan
+// + scatter): pass 1 counts the kept pairs of each tile row a (CTA per row); pass 2
+// sums the counts of the rows before a (every CTA itself: O(T) reads, L2-resident)
+// and writes row a's kept pairs in order with a block scan. Same list, same order.
+constexpr int64_t CULL_ROWS_MAX = 8192;
+constexpr int CULL_T = 256;
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();  // red may still be read by a previous call
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  int t = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(CULL_T) cull_rows_kernel(
+    const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
+    int dpad, int64_t T, float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
+    int32_t* __restrict__ rowcnt) {
+  griddep_wait();
+  __shared__ int red[CULL_T / 32];
+  const bool unsafe = *unsafe_flag != 0;
+  for (int64_t a = blockIdx.x; a < T; a += gridDim.x) {
+    int c = 0;
+    for (int64_t b = a + threadIdx.x; b < T; b += blockDim.x)
+      c += keep_item(lo, hi, maxnorm, dpad, (int)a, (int)b, eps32, formula, unsafe) ? 1 : 0;
+    const int t = block_sum(c, red);
+    if (threadIdx.x == 0) rowcnt[a] = t;
+  }
+}
+
+__global__ void __launch_bounds__(CULL_T) cull_write_kernel(
+    const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
+    int dpad, int64_t T, float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
+    const int32_t* __restrict__ rowcnt, uint32_t* __restrict__ list, int32_t* __restrict__ total_kept,
+    unsigned long long* __restrict__ count) {
+  griddep_wait();
+  __shared__ int red[CULL_T / 32];
+  __shared__ int wsum[CULL_T / 32];
+  const bool unsafe = *unsafe_flag != 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t a = blockIdx.x; a < T; a += gridDim.x) {
+    int p = 0;
+    for (int64_t r = threadIdx.x; r < a; r += blockDim.x) p += rowcnt[r];
+    int pos = block_sum(p, red);  // kept pairs of the rows before a
+    for (int64_t b0 = a; b0 < T; b0 += blockDim.x) {
+      const int64_t b = b0 + threadIdx.x;
+      const bool k = b < T && keep_item(lo, hi, maxnorm, dpad, (int)a, (int)b, eps32, formula, unsafe);
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      __syncthreads();  // wsum of the previous chunk is consumed
+      if (lane == 0) wsum[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, all = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        before += w < wid ? wsum[w] : 0;
+        all += wsum[w];
+      }
+      if (k) list[pos + before + __popc(bal & ((1u << lane) - 1u))] = ((uint32_t)a << 16) | (uint32_t)b;
+      pos += all;
+    }
+    if (a == T - 1 && threadIdx.x == 0) {
+      *total_kept = pos;
+      *count = (unsigned long long)pos;
+    }
+  }
+}
+
 int pad_dim(int d) {
   if (d <= 4) return d;
   if (d <= 8) return 8;
@@ -979,8 +1082,7 @@ cudaError_t launch_one(const UnitArgs& a, int sm_count, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
     configured = true;
   }
-  kern<<<(unsigned)(sm_count * per_sm), G::THREADS, G::SMEM, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)(sm_count * per_sm)), dim3(G::THREADS), G::SMEM, s, a);
 }
 
 // Both instantiations are launched back to back; each reads the device flag set by
@@ -1004,31 +1106,35 @@ cudaError_t launch_d(const UnitArgs& a, int formula, int sm_count, cudaStream_t 
 int padded_dim(int d) { return pad_dim(d); }
 
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
-                        unsigned int* bbox, cudaStream_t s) {
+                        unsigned int* bbox, int32_t* cnt, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int threads = 256;
   int64_t blocks = (n + threads - 1) / threads;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  if (bbox) {
-    cudaError_t e = cudaMemsetAsync(bbox, 0xff, 4 * sizeof(unsigned int), s);  // lo = max
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(bbox + 4, 0, 4 * sizeof(unsigned int), s);  // hi = min
-    if (e != cudaSuccess) return e;
-  }
-  prep_kernel<<<(unsigned)blocks, threads, 0, s>>>(coords, n, d, dp, S, rec, unsafe_flag, bbox);
-  return cudaGetLastError();
+  return launch_pdl(prep_kernel, dim3((unsigned)blocks), dim3(threads), 0, s, coords, n, d, dp, S,
+                    rec, unsafe_flag, bbox, cnt);
 }
 
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
                         int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
-                        unsigned long long* count, cudaStream_t s) {
+                        unsigned long long* count, bool bounds_ready, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int64_t T = (n + TILE - 1) / TILE;
-  tile_bounds_kernel<<<(unsigned)T, 256, 0, s>>>(rec, n, dp, S, lo, hi, maxnorm);
+  if (!bounds_ready) tile_bounds_kernel<<<(unsigned)T, 256, 0, s>>>(rec, n, dp, S, lo, hi, maxnorm);
+  if (T <= CULL_ROWS_MAX) {  // rowcnt lives in the flags buffer (T <= T(T+1)/2 ints)
+    const unsigned g = (unsigned)std::min<int64_t>(T, 148 * 8);
+    cudaError_t e = launch_pdl(cull_rows_kernel, dim3(g), dim3(CULL_T), 0, s, (const float*)lo,
+                               (const float*)hi, (const float*)maxnorm, dp, T, eps32, formula,
+                               unsafe_flag, flags);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(cull_write_kernel, dim3(g), dim3(CULL_T), 0, s, (const float*)lo,
+                      (const float*)hi, (const float*)maxnorm, dp, T, eps32, formula, unsafe_flag,
+                      (const int32_t*)flags, list, total_kept, count);
+  }
   const int64_t total = T * (T + 1) / 2;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
@@ -1073,27 +1179,29 @@ cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, in
   const float* box = dp <= 4 ? blk : nullptr;  // block boxes only pay off in low dimension
   int64_t blocks = (all_items / world * 32 + 255) / 256 + 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  unit_list_kernel<<<(unsigned)blocks, 256, 0, s>>>(box, dp, n, KP, eps32, formula, unsafe_flag,
-                                                    item_list, kept, rank, world, unit_list,
-                                                    units_cap, unit_count, item_units);
-  return cudaGetLastError();
+  return launch_pdl(unit_list_kernel, dim3((unsigned)blocks), dim3(256), 0, s, box, dp, n, KP, eps32,
+                    formula, unsafe_flag, item_list, kept, rank, world, unit_list, units_cap,
+                    unit_count, item_units);
 }
 
 cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
-                            unsigned long long* dir_count, cudaStream_t s) {
+                            unsigned long long* dir_count, int32_t* diag_idx, const CoreInit& ci,
+                            cudaStream_t s) {
   int64_t blocks = (all_items * 32 + 255) / 256;
+  if (ci.cnt) blocks = std::max<int64_t>(blocks, (ci.n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   switch (unit_kp(d)) {
     case 4:
-      unit_dir_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
-      break;
+      return launch_pdl(unit_dir_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
+                        item_units, kept, dir, dir_count, diag_idx, ci);
     case 2:
-      unit_dir_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
-      break;
+      return launch_pdl(unit_dir_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
+                        item_units, kept, dir, dir_count, diag_idx, ci);
     default:
-      unit_dir_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(a, all_items, item_units, kept, dir, dir_count);
+      return launch_pdl(unit_dir_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
+                        item_units, kept, dir, dir_count, diag_idx, ci);
   }
   return cudaGetLastError();
 }
