@@ -463,8 +463,10 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
   unit_range(A, r_lo, r_hi);
   const long long nw = (long long)gridDim.x * LINK_WARPS;
   int last_a = -1, last_b = -1;  // this lane's last linked pair of roots
-  for (long long u = r_lo + (long long)blockIdx.x * LINK_WARPS + warp; u < r_hi; u += nw) {
-    int a, b, lb;
+  // loads are issued a step ahead where the data does not depend on them: the next
+  // unit's list entry and chunk entries during the current unit, and per column block
+  // the core word, the 32 parents and the first 32 words together
+  auto unit_entry = [&](long long u, int& a, int& b, int& lb) {
     if (A.unit_list) {
       const uint2 e = __ldg(A.unit_list + u);
       a = (int)(e.x >> 16);
@@ -474,9 +476,22 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
       decode_item(u / LB, A.T, a, b);
       lb = (int)(u % LB);
     }
+  };
+  long long u = r_lo + (long long)blockIdx.x * LINK_WARPS + warp;
+  int na = 0, nb = 0, nlb = 0;
+  uint2 nce = make_uint2(0u, 0u);
+  if (u < r_hi) {
+    unit_entry(u, na, nb, nlb);
+    if (lane < WPR) nce = A.uchunks[u * WPR + lane];
+  }
+  for (; u < r_hi; u += nw) {
+    const int a = na, b = nb, lb = nlb;
+    const uint2 ce = nce;
+    if (u + nw < r_hi) {  // prefetch the next unit
+      unit_entry(u + nw, na, nb, nlb);
+      nce = lane < WPR ? A.uchunks[(u + nw) * WPR + lane] : make_uint2(0u, 0u);
+    }
     if (a == b) continue;  // round 1
-    uint2 ce = make_uint2(0u, 0u);
-    if (lane < WPR) ce = A.uchunks[u * WPR + lane];
     const uint32_t cnt = ce.y & 0xffffu;
     const unsigned long long base = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
     const bool ok = cnt != 0u && base + cnt <= A.words_cap;  // overflowed run: the host re-runs
@@ -486,8 +501,9 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
     const int r0 = a * TILE + lb * KPL;
     for (int k = lane; k < KPL; k += 32) {
       const int g = r0 + k;
+      const int pg = g < n ? parent[g] : -1;
       const bool c = g < n && ((corew[g >> 5] >> (31 - (g & 31))) & 1u);
-      rows[k] = c ? parent[g] : -1;
+      rows[k] = c ? pg : -1;
     }
     while (todo) {
       const int jw = __ffs(todo) - 1;
@@ -495,9 +511,11 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
       const uint32_t wcnt = __shfl_sync(0xffffffffu, cnt, jw);
       const unsigned long long wbase = __shfl_sync(0xffffffffu, base, jw);
       const int c0 = b * TILE + jw * 32;
+      const uint2 rec0 = lane < wcnt ? A.words[wbase + lane] : make_uint2(0u, 0u);
+      const int praw = c0 + lane < n ? parent[c0 + lane] : -1;
       const uint32_t cw = corew[(b * TILE >> 5) + jw];
       const bool cc = (cw >> (31 - lane)) & 1u;
-      const int pv = cc ? parent[c0 + lane] : -1;
+      const int pv = cc ? praw : -1;
       cols[lane] = pv;
       const unsigned same = __match_any_sync(0xffffffffu, pv);
       const unsigned corel = __brev(cw);  // bit l <-> lane l
@@ -507,7 +525,7 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
       const int ub = (corel && (corel & ~grp0) == 0u) ? __shfl_sync(0xffffffffu, pv, first) : -1;
       __syncwarp();
       for (uint32_t k = lane; k < wcnt; k += 32) {
-        const uint2 rec = A.words[wbase + k];
+        const uint2 rec = k < 32 ? rec0 : A.words[wbase + k];
         const uint32_t x = rec.x;
         const int ul = (int)(rec.y >> 4);
         const int au = rows[ul - lb * KPL];
@@ -821,7 +839,14 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
                              uchunks, (const int32_t*)w.diag_idx, ntiles, words, words_cap, w.n,
                              (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
   if (e != cudaSuccess) return e;
-  return launch_pdl(union_links_kernel, dim3(sms * 8), dim3(LINK_WARPS * 32), 0, s, units,
+  static int links_per_sm = 0;  // one resident wave: warps take units grid-stride
+  if (!links_per_sm) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&links_per_sm, union_links_kernel,
+                                                      LINK_WARPS * 32, 0) != cudaSuccess ||
+        links_per_sm < 1)
+      links_per_sm = 4;
+  }
+  return launch_pdl(union_links_kernel, dim3(sms * links_per_sm), dim3(LINK_WARPS * 32), 0, s, units,
                     lane_blocks, (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
 }
 
