@@ -268,7 +268,6 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   __shared__ uint32_t adj[32];
   __shared__ int wroots[WPR], wpre[WPR], slot_root[32];
   __shared__ int ntrees_sh;
-  __shared__ ItemWords iw;
   const int tid = threadIdx.x;
   const int w = tid % WPR, cblk = tid / WPR;
   const int64_t nw = (n + 31) / 32;
@@ -276,8 +275,6 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     const int c = diag_idx[tile] - 1;  // 0 = no diagonal chunk
     if (c < 0) continue;  // uniform per CTA
     const DirInfo ci = decode_dir(dir[c]);
-    load_item_words(ci, uchunks, words_cap, iw);
-    if (!iw.ok) continue;  // uniform per CTA
     const int base = ci.a * TILE;
     if (tid < WPR) {
       const int64_t gw = (int64_t)ci.a * WPR + tid;
@@ -290,27 +287,34 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
       hist[v] = 0;
     }
     __syncthreads();
-    // scatter the chunk into the dense matrix (core rows, core columns only);
-    // non-core rows give their own border candidate directly
-    for (int k = tid; k < iw.total; k += THREADS) {
-      const uint2 rec = item_word(iw, words, (uint32_t)k);
-      const int u = (int)(rec.y >> 4);
-      const int ww = (int)(rec.y & 15u);
-      const uint32_t cw = lcw[ww];
-      if ((lcw[u >> 5] >> (31 - (u & 31))) & 1u) {
-        R[ww * TILE + u] = rec.x & cw;
-        uint32_t bm = rec.x & ~cw;  // core u in range of non-core v (merge.py:116-130)
-        if (bm) {
-          const int gu = orig_of(perm, base + u);
-          while (bm) {
-            const int t = __clz(bm);
-            bm &= ~(0x80000000u >> t);
-            atomicMin(&lb[ww * 32 + t], gu);
+    // scatter the tile pair's words into the dense matrix (core rows, core columns
+    // only), one warp per chunk entry; non-core rows give their own border candidate
+    // directly. Entries of an overflowed run are skipped (the host re-runs).
+    for (int e = tid >> 5; e < ci.nunits; e += THREADS / 32) {
+      const uint2 ce = uchunks[ci.ulo + e];
+      const uint32_t cnt = ce.y & 0xffffu;
+      const unsigned long long wb = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
+      if (cnt == 0u || wb + cnt > words_cap) continue;  // warp-uniform
+      for (uint32_t k = tid & 31; k < cnt; k += 32) {
+        const uint2 rec = words[wb + k];
+        const int u = (int)(rec.y >> 4);
+        const int ww = (int)(rec.y & 15u);
+        const uint32_t cw = lcw[ww];
+        if ((lcw[u >> 5] >> (31 - (u & 31))) & 1u) {
+          R[ww * TILE + u] = rec.x & cw;
+          uint32_t bm = rec.x & ~cw;  // core u in range of non-core v (merge.py:116-130)
+          if (bm) {
+            const int gu = orig_of(perm, base + u);
+            while (bm) {
+              const int t = __clz(bm);
+              bm &= ~(0x80000000u >> t);
+              atomicMin(&lb[ww * 32 + t], gu);
+            }
           }
+        } else {
+          const uint32_t cm = rec.x & cw;
+          if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
         }
-      } else {
-        const uint32_t cm = rec.x & cw;
-        if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
       }
     }
     __syncthreads();

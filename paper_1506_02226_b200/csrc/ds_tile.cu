@@ -165,7 +165,9 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
 // overflow) compares every lane point.
 // Measured on B200 (tools/tile_bench.py): d <= 4 runs best with 3 of 4 lane points
 // compared (the FP32 pipe is the tighter one there), wider records with all lane
-// points on the sign-bit path (the cross-product chain leaves the ALU idle).
+// points on the sign-bit path (the cross-product chain leaves the ALU idle). A
+// compare costs FSETP + SEL + half an IADD3 (ptxas lowers set.* and predicated
+// lop3 to the same), the sign bit one FP op + one funnel shift.
 template <int KP, bool SAFE, int D>
 struct Pack {
   static constexpr int KC = !SAFE ? KP : (D <= 4 ? (3 * KP) / 4 : 0);
@@ -201,8 +203,15 @@ struct Geo {
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int STAGE = 32 * S;                       // floats per staged block
   static constexpr size_t SMEM = (size_t)WARPS * 2 * STAGE * 4;
-  static constexpr int UNROLL = D <= 4 ? 32 : 8;
-  static constexpr int MINB = (D <= 8 || D == 32) ? 4 : 3;  // 16 or 12 resident warps per SM
+#ifndef DS_UNROLL_WIDE
+#define DS_UNROLL_WIDE 8
+#endif
+#ifndef DS_MINB16
+#define DS_MINB16 3
+#endif
+  static constexpr int UNROLL = D <= 4 ? 32 : DS_UNROLL_WIDE;
+  // resident CTAs (x 4 warps) per SM: 16-D holds 4 lane points x 17 floats per lane
+  static constexpr int MINB = (D <= 8 || D == 32) ? 4 : (D == 16 ? DS_MINB16 : 3);
 };
 
 // Column-side counts of one unit: the number of set bits of every column over the

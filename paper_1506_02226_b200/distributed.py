@@ -9,8 +9,10 @@ NCCL for the exchanges):
   * the upper-triangle tile pairs (items, TILE = 512 points per side,
     numbered row-major by ds_tile_items) — after bounding-box culling, the
     list of tile pairs that can hold an in-range pair, built identically on
-    every rank — are split into contiguous equal ranges, one per rank; items
-    cost the same, so ranks are balanced;
+    every rank (deterministic sort and scan) — are dealt to the ranks
+    cyclically (kept pair q goes to rank q mod world, which spreads dense and
+    sparse regions evenly); with culling off, the work units of the dense
+    triangle are split into contiguous equal ranges (shard_range);
   * stage 1+2 on the rank's items gives partial neighbour counts and the
     rank's adjacency words (ds_shard_stage12);
   * exchange 1: all_reduce(SUM) of the int32 counts -> identical core flags;
