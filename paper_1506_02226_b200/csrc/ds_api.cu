@@ -82,6 +82,8 @@ struct ds_ctx {
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
   cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr;  // kept alive: its memcpy nodes are re-pointed per launch
+  cudaGraphNode_t gn_h2d = nullptr, gn_labels = nullptr, gn_counts = nullptr;
   unsigned long long gkey[12] = {};
   unsigned long long seen_key[12] = {};
   bool capturing = false;  // events become external graph nodes while recording
@@ -448,11 +450,34 @@ void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* 
 }
 
 // Device part of the pipeline: stage 1+2, core flags, merge, labels (+ counts).
+// Host buffers of ds_run_dbscan: the coordinates copied in and the labels / counts
+// copied out are part of the enqueued (and graph-recorded) work.
+struct HostIO {
+  const double* coords = nullptr;
+  size_t in_bytes = 0;
+  int64_t* labels = nullptr;
+  int64_t* counts = nullptr;
+};
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                          int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
-                         int64_t* d_counts64, cudaStream_t s, Plan& pl, bool captured) {
+                         int64_t* d_counts64, cudaStream_t s, Plan& pl, bool captured,
+                         const HostIO* io) {
   c->capturing = captured;
   auto rec = [&](cudaEvent_t e) { return record(c, e, s); };
+  if (io && io->coords) {
+    DS_CK(rec(c->ev[5]));
+    DS_CK(cudaMemcpyAsync((void*)d_coords, io->coords, io->in_bytes, cudaMemcpyHostToDevice, s));
+  }
   DS_CK(rec(c->ev[0]));
   ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl, 0, 1, min_pts);
   if (st != DS_OK) return st;
@@ -465,8 +490,31 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
   DS_CK(rec(c->ev[4]));
+  if (io && io->labels)
+    DS_CK(cudaMemcpyAsync(io->labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  if (io && io->counts && d_counts64)
+    DS_CK(cudaMemcpyAsync(io->counts, d_counts64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  DS_CK(rec(c->ev[7]));
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   c->capturing = false;
   return DS_OK;
+}
+
+// memcpy node of `g` whose host end is `host` (source or destination), or nullptr
+cudaGraphNode_t find_copy_node(cudaGraph_t g, const void* host) {
+  if (!host) return nullptr;
+  size_t count = 0;
+  if (cudaGraphGetNodes(g, nullptr, &count) != cudaSuccess || count == 0) return nullptr;
+  std::vector<cudaGraphNode_t> nodes(count);
+  if (cudaGraphGetNodes(g, nodes.data(), &count) != cudaSuccess) return nullptr;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeMemcpy) continue;
+    cudaMemcpy3DParms pr{};
+    if (cudaGraphMemcpyNodeGetParams(nd, &pr) != cudaSuccess) continue;
+    if (pr.srcPtr.ptr == host || pr.dstPtr.ptr == host) return nd;
+  }
+  return nullptr;
 }
 
 // The whole pipeline, enqueued without host round trips; the optional host
@@ -476,9 +524,13 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
 // cost); an adjacency-word overflow invalidates the graph.
 ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                    int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
-                   int64_t* d_counts64, cudaStream_t s, ds_timings* t, int64_t* h_labels = nullptr,
-                   int64_t* h_counts = nullptr) {
+                   int64_t* d_counts64, cudaStream_t s, ds_timings* t, const HostIO* io = nullptr) {
   Plan pl;
+  // host copies are recorded into the graph (and re-pointed per launch) when every
+  // host buffer is page-locked; pageable buffers run the pipeline eagerly
+  const bool io_graphable =
+      !io || ((!io->coords || host_pinned(io->coords)) && (!io->labels || host_pinned(io->labels)) &&
+              (!io->counts || host_pinned(io->counts)));
   for (int attempt = 1;; ++attempt) {
     unsigned long long key[12];
     uint64_t eps_bits;
@@ -496,8 +548,20 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[9] = (unsigned long long)mem_cap;
     key[10] = (unsigned long long)c->device;
     key[11] = c->units_cap;
-    const bool graph_hit = c->use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
+    key[1] |= (unsigned long long)(io && io->coords) << 41 | (unsigned long long)(io && io->labels) << 42 |
+              (unsigned long long)(io && io->counts) << 43;
+    const bool use_graph = c->use_graph && io_graphable;
+    const bool graph_hit = use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
     if (graph_hit) {
+      if (io && io->coords && c->gn_h2d)
+        DS_CK(cudaGraphExecMemcpyNodeSetParams1D(c->gexec, c->gn_h2d, (void*)d_coords, io->coords,
+                                                 io->in_bytes, cudaMemcpyHostToDevice));
+      if (io && io->labels && c->gn_labels)
+        DS_CK(cudaGraphExecMemcpyNodeSetParams1D(c->gexec, c->gn_labels, io->labels, d_labels,
+                                                 (size_t)n * 8, cudaMemcpyDeviceToHost));
+      if (io && io->counts && c->gn_counts)
+        DS_CK(cudaGraphExecMemcpyNodeSetParams1D(c->gexec, c->gn_counts, io->counts, d_counts64,
+                                                 (size_t)n * 8, cudaMemcpyDeviceToHost));
       DS_CK(cudaGraphLaunch(c->gexec, s));
       // plan fields the timings need (no device work)
       pl.T = n_tiles(n);
@@ -508,11 +572,15 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       pl.dense_units = pl.all_items * lane_blocks(d);
       pl.units_cap = pl.cull ? c->units_cap : (unsigned long long)pl.dense_units;
       pl.base = base_bytes(n, d) + (size_t)pl.units_cap * unit_bytes(pl.cull);
-    } else if (c->use_graph && std::memcmp(key, c->seen_key, sizeof key) == 0) {
+    } else if (use_graph && std::memcmp(key, c->seen_key, sizeof key) == 0) {
       // second call with this key: record the device pipeline and replay it
       if (c->gexec) {
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
+      }
+      if (c->graph) {
+        cudaGraphDestroy(c->graph);
+        c->graph = nullptr;
       }
       const unsigned long long gen0 = g_alloc_generation;
       // the legacy default stream cannot be captured: record on the context's own
@@ -522,7 +590,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
                              : s;
       DS_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       ds_status st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap,
-                                    d_labels, d_counts64, cap, pl, true);
+                                    d_labels, d_counts64, cap, pl, true, io);
       c->capturing = false;
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(cap, &graph);
@@ -534,17 +602,20 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       if (gen0 != g_alloc_generation) {  // a buffer moved while recording: run eagerly
         cudaGraphDestroy(graph);
         st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap, d_labels,
-                            d_counts64, s, pl, false);
+                            d_counts64, s, pl, false, io);
         if (st != DS_OK) return st;
       } else {
         DS_CK(cudaGraphInstantiate(&c->gexec, graph, 0));
-        cudaGraphDestroy(graph);
+        c->graph = graph;
+        c->gn_h2d = io ? find_copy_node(graph, io->coords) : nullptr;
+        c->gn_labels = io ? find_copy_node(graph, io->labels) : nullptr;
+        c->gn_counts = io ? find_copy_node(graph, io->counts) : nullptr;
         std::memcpy(c->gkey, key, sizeof key);
         DS_CK(cudaGraphLaunch(c->gexec, s));
       }
     } else {
       ds_status st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap,
-                                    d_labels, d_counts64, s, pl, false);
+                                    d_labels, d_counts64, s, pl, false, io);
       if (st != DS_OK) return st;
       // key after this call's allocations: the next identical call records the graph
       key[7] = c->words_cap;
@@ -552,13 +623,6 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       key[11] = c->units_cap;
       std::memcpy(c->seen_key, key, sizeof key);
     }
-    if (h_labels)
-      DS_CK(cudaMemcpyAsync(h_labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-    if (h_counts && d_counts64)
-      DS_CK(cudaMemcpyAsync(h_counts, d_counts64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-    DS_CK(cudaEventRecord(c->ev[7], s));
-    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost,
-                          s));
     DS_CK(cudaStreamSynchronize(s));
     bool retry = false;
     ds_status st = check_words(c, pl, mem_cap, &retry);
@@ -653,6 +717,7 @@ void ds_ctx_destroy(ds_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->h_scalars) cudaFreeHost(c->h_scalars);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
   delete c;
 }
 
@@ -692,11 +757,14 @@ ds_status ds_run_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, d
   DS_CK(ensure(c->labels, (size_t)n * 8));
   if (counts_out) DS_CK(ensure(c->counts64, (size_t)n * 8));
   cudaStream_t s = c->stream;
-  DS_CK(cudaEventRecord(c->ev[5], s));
-  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
+  HostIO io;
+  io.coords = coords;
+  io.in_bytes = in_bytes;
+  io.labels = labels_out;
+  io.counts = counts_out;
   st = pipeline(c, (const double*)c->coords64.p, n, d, eps_sq, min_pts, formula, mem_cap,
                 (int64_t*)c->labels.p, counts_out ? (int64_t*)c->counts64.p : nullptr, s, &local,
-                labels_out, counts_out);
+                &io);
   if (st != DS_OK) return st;
   float h2d = 0;
   DS_CK(cudaEventElapsedTime(&h2d, c->ev[5], c->ev[0]));
