@@ -314,11 +314,11 @@ def run_b200(args):
     tile_s = statistics.mean(tile_ms) / 1e3
     achieved = pairs * ops / tile_s / 1e12
     # kernels per step (1 GPU, culled schedule; the ncu launch list in profiles/): prep,
-    # morton, 4 CUB radix-sort kernels, permute, tile bounds, cull flags, scan, cull
-    # scatter, block bounds, unit list, 2x eps-unit (one exits at once), unit dir, core
-    # init, diag index, union diag, union links, roots, flags, scan, label = 24; a
-    # word-overflow re-run repeats the pipeline; sharded runs add the forest merge
-    launches_per_step = 24 * last[3] if world == 1 else 26
+    # morton, 4 CUB radix-sort kernels, permute+bounds, 2 cull-row kernels, unit list,
+    # eps-unit, unit dir (+ core init), union diag, union links, roots, label scan,
+    # label = 17; a word-overflow re-run repeats the pipeline; sharded runs add the
+    # forest merge and a separate core init
+    launches_per_step = 17 * last[3] if world == 1 else 19
 
     line = {
         "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",

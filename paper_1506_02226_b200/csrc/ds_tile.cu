@@ -318,15 +318,12 @@ __device__ __forceinline__ void cp_async_wait() {
 //     atomic per WORD_RUN slots) and the chunk entry records where they went. Column
 //     blocks without a single bit (most of a dense schedule) skip both.
 template <int D, int F, bool SAFE>
-__global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
-  griddep_wait();
+__device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   using G = Geo<D>;
   constexpr int KP = G::KP;
   constexpr int S = G::S;
   constexpr int KC = Pack<KP, SAFE, D>::KC;
   constexpr int LB = TILE / (32 * KP);
-
-  if ((*A.unsafe_flag != 0) == SAFE) return;  // the other instantiation owns this input
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -344,8 +341,11 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
   // ---- batches of row units: [lo, hi) + list entries (lane i: entry lo + i) ----
   // about 16 batches per warp; batch indices come from a 32-bit atomic counter
   const long long nw = (long long)gridDim.x * G::WARPS;
+#ifndef DS_BATCH_MIN
+#define DS_BATCH_MIN 1
+#endif
   long long B = (r_hi - r_lo) / (nw * 16);
-  B = B < 1 ? 1 : (B > 32 ? 32 : B);
+  B = B < DS_BATCH_MIN ? DS_BATCH_MIN : (B > 32 ? 32 : B);
   unsigned int* const ctr = reinterpret_cast<unsigned int*>(A.work_ctr);
   auto load_entries = [&](long long lo) -> uint2 {
     return (list && lo + lane < r_hi && lane < B) ? __ldg(list + lo + lane) : make_uint2(0u, 0u);
@@ -570,6 +570,16 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
   flush();
   if (lane == 0 && steps_done)
     atomicAdd(A.pairs_done, steps_done * 32ull * 32ull * (unsigned long long)KP);
+}
+
+// One launch serves both number ranges: the prep kernel's device flag selects the
+// body (no host round trip); SAFE=false compares every predicate (inputs whose
+// squares could overflow).
+template <int D, int F>
+__global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
+  griddep_wait();
+  if (*A.unsafe_flag != 0) eps_unit_body<D, F, false>(A);
+  else eps_unit_body<D, F, true>(A);
 }
 
 // ---- culled schedule: row-unit list ----------------------------------------------------
@@ -1076,10 +1086,10 @@ int pad_dim(int d) {
   return 64;
 }
 
-template <int D, int F, bool SAFE>
-cudaError_t launch_one(const UnitArgs& a, int sm_count, cudaStream_t s) {
+template <int D, int F>
+cudaError_t launch_df(const UnitArgs& a, int sm_count, cudaStream_t s) {
   using G = Geo<D>;
-  auto kern = eps_unit_kernel<D, F, SAFE>;
+  auto kern = eps_unit_kernel<D, F>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
@@ -1092,16 +1102,6 @@ cudaError_t launch_one(const UnitArgs& a, int sm_count, cudaStream_t s) {
     configured = true;
   }
   return launch_pdl(kern, dim3((unsigned)(sm_count * per_sm)), dim3(G::THREADS), G::SMEM, s, a);
-}
-
-// Both instantiations are launched back to back; each reads the device flag set by
-// the prep kernel and the one that does not own the input exits immediately, so
-// the host never waits for the range check.
-template <int D, int F>
-cudaError_t launch_df(const UnitArgs& a, int sm_count, cudaStream_t s) {
-  cudaError_t e = launch_one<D, F, true>(a, sm_count, s);
-  if (e != cudaSuccess) return e;
-  return launch_one<D, F, false>(a, sm_count, s);
 }
 
 template <int D>

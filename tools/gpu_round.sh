@@ -14,9 +14,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-cpu --no-dense > gpurun_out/ncu_launch.log 2>&1
 # second call of tools/prof_unit.py (the graph-recorded one) for each kernel
 DS_DENSE=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:eps_unit_kernel.*bool\)1' -s 1 -c 1 -o gpurun_out/prof_tile_c2_${TAG} python tools/prof_unit.py > gpurun_out/ncu_tile.log 2>&1
+  -k 'regex:eps_unit_kernel' -s 1 -c 1 -o gpurun_out/prof_tile_c2_${TAG} python tools/prof_unit.py > gpurun_out/ncu_tile.log 2>&1
 DS_CONFIG=C4 DS_DENSE=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:eps_unit_kernel.*bool\)1' -s 1 -c 1 -o gpurun_out/prof_tile_c4_${TAG} python tools/prof_unit.py > gpurun_out/ncu_tile_c4.log 2>&1
+  -k 'regex:eps_unit_kernel' -s 1 -c 1 -o gpurun_out/prof_tile_c4_${TAG} python tools/prof_unit.py > gpurun_out/ncu_tile_c4.log 2>&1
 DS_DENSE=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k 'regex:union_|scan_lookback|unit_list|roots' -s 6 -c 6 -o gpurun_out/prof_merge_${TAG} python tools/prof_unit.py > gpurun_out/ncu_merge.log 2>&1
 echo done
