@@ -98,6 +98,6 @@ def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
     for body in tile:
         name = body.split("\n")[0]
         assert not re.search(r"\bFFMA2?\b", body), name
-    k2 = [f for f in tile if "eps_unit_kernelILi2ELi1ELb1E" in f.split("\n")[0]]
+    k2 = [f for f in tile if "eps_unit_kernelILi2ELi1EE" in f.split("\n")[0]]
     assert k2 and "FMUL2" in k2[0] and "FADD2" in k2[0]
     assert "LDGSTS" in k2[0]
