@@ -11,7 +11,7 @@
 //
 // Keys: up to 4 leading dimensions quantised to a 2^(b/k)-per-dimension grid over
 // the global bounding box (reduced by the prep kernel), b = 16 bits (two radix passes)
-// for 1-2-D inputs up to 2^18 points, 20 up to 2^22 and 24 bits otherwise — far finer than a 512-point tile. The sort is CUB's stable LSD radix sort on
+// for 1-2-D inputs up to 2^18 points and 24 bits otherwise — far finer than a 512-point tile. The sort is CUB's stable LSD radix sort on
 // (32-bit key, original index), so the permutation is deterministic and identical on
 // every rank.
 #include <cuda_runtime.h>
@@ -25,13 +25,12 @@ namespace ds {
 namespace {
 
 // total key bits: 16 (two radix passes, a 256 x 256 grid) for 1-2-D inputs up to
-// 2^18 points, 20 up to 2^22, 24 (three passes) otherwise
-// Measured on B200 (key-bit sweep, round 1): a few points per grid cell keeps the 32-point block boxes
-// tight; coarser keys double the evaluated pairs at C2, finer ones cost a third pass.
-inline int key_bits(int64_t n, int kd) {
-  if (kd > 2) return 24;
-  return n <= (1 << 18) ? 16 : (n <= (1 << 22) ? 20 : 24);
-}
+// 2^18 points, 24 (three passes) otherwise
+// Measured on B200 (key-bit sweep, round 1): about one point per grid cell keeps the
+// 32-point block boxes tight — 12-bit keys nearly double the pairs evaluated at C2,
+// 16 bits are best up to ~2^18 points (two radix passes), 24 above (C3 -3 %, C5 -12 %
+// pairs vs 16/20 bits).
+inline int key_bits(int64_t n, int kd) { return (kd <= 2 && n <= (1 << 18)) ? 16 : 24; }
 
 __device__ __forceinline__ float unord(unsigned int u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
