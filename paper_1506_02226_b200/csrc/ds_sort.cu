@@ -11,9 +11,9 @@
 //
 // Keys: up to 4 leading dimensions quantised to a 2^(b/k)-per-dimension grid over
 // the global bounding box (reduced by the prep kernel), b = 16 bits (two radix passes)
-// for 1-2-D inputs up to 2^18 points and 24 bits otherwise — far finer than a 512-point tile. The sort is CUB's stable LSD radix sort on
-// (32-bit key, original index), so the permutation is deterministic and identical on
-// every rank.
+// for 1-2-D inputs up to 2^18 points and 24 bits otherwise — far finer than a
+// 512-point tile. The sort is CUB's stable LSD radix sort on (32-bit key, original
+// index), so the permutation is deterministic and identical on every rank.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
