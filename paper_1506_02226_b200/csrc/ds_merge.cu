@@ -503,11 +503,30 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
     if (!todo) continue;
     // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not core)
     const int r0 = a * TILE + lb * KPL;
+    int rfirst = -1;  // this lane's first core row root
+    bool rsame = true;  // all of this lane's core rows share it
+    bool rnoncore = false;  // this lane has a non-core row
     for (int k = lane; k < KPL; k += 32) {
       const int g = r0 + k;
       const int pg = g < n ? parent[g] : -1;
       const bool c = g < n && ((corew[g >> 5] >> (31 - (g & 31))) & 1u);
       rows[k] = c ? pg : -1;
+      rnoncore |= g < n && !c;
+      if (c) {
+        if (rfirst < 0) rfirst = pg;
+        else rsame &= pg == rfirst;
+      }
+    }
+    const bool rows_allcore = !__any_sync(0xffffffffu, rnoncore);
+    // urow: the single root of all core rows of the lane block (the common case inside
+    // a cluster), -1 if they differ or there are none
+    int urow = -1;
+    {
+      const unsigned has = __ballot_sync(0xffffffffu, rfirst >= 0);
+      if (has) {
+        const int r = __shfl_sync(0xffffffffu, rfirst, __ffs(has) - 1);
+        if (__all_sync(0xffffffffu, rsame && (rfirst < 0 || rfirst == r))) urow = r;
+      }
     }
     while (todo) {
       const int jw = __ffs(todo) - 1;
@@ -528,7 +547,18 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
       const unsigned grp0 = __shfl_sync(0xffffffffu, same, first);
       const int ub = (corel && (corel & ~grp0) == 0u) ? __shfl_sync(0xffffffffu, pv, first) : -1;
       __syncwarp();
-      for (uint32_t k = lane; k < wcnt; k += 32) {
+      // uniform rows x uniform columns: the whole column block is at most one link
+      // (urow, ub), made once by lane 0 if any core-core bit is set
+      const bool one_link = urow >= 0 && ub >= 0;
+      bool cc_any = false;
+      // all rows and all (valid) columns core: every word is a core-core word and no
+      // border candidates exist, so the block is exactly the link — its words need not
+      // be read
+      const int nvalid = n - c0 < 32 ? n - c0 : 32;
+      const uint32_t vmask = nvalid >= 32 ? 0xffffffffu : ~(0xffffffffu >> nvalid);
+      const bool skip_words = one_link && rows_allcore && cw == vmask;
+      if (skip_words) cc_any = wcnt > 0;
+      for (uint32_t k = skip_words ? wcnt : lane; k < wcnt; k += 32) {
         const uint2 rec = k < 32 ? rec0 : A.words[wbase + k];
         const uint32_t x = rec.x;
         const int ul = (int)(rec.y >> 4);
@@ -536,7 +566,9 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
         const uint32_t cm = x & cw;
         if (au >= 0) {
           if (cm) {
-            if (ub >= 0) {
+            if (one_link) {
+              cc_any = true;
+            } else if (ub >= 0) {
               if (au != ub && !(au == last_a && ub == last_b)) {
                 link_root(parent, find_plain(parent, au), ub);
                 last_a = au;
@@ -568,6 +600,12 @@ __global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
         } else if (cm) {
           atomicMin(&bmin[a * TILE + ul], min_orig(perm, c0, cm));
         }
+      }
+      if (one_link && __any_sync(0xffffffffu, cc_any) && lane == 0 && urow != ub &&
+          !(urow == last_a && ub == last_b)) {
+        link_root(parent, find_plain(parent, urow), ub);
+        last_a = urow;
+        last_b = ub;
       }
       __syncwarp();  // cols is rewritten by the next column block
     }
