@@ -757,9 +757,11 @@ ds_status ds_run_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, d
   DS_CK(ensure(c->labels, (size_t)n * 8));
   if (counts_out) DS_CK(ensure(c->counts64, (size_t)n * 8));
   cudaStream_t s = c->stream;
+  // the coordinates go in before the graph launch, so the copy overlaps the launch;
+  // the label / count copies out are part of the recorded pipeline
+  DS_CK(cudaEventRecord(c->ev[5], s));
+  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
   HostIO io;
-  io.coords = coords;
-  io.in_bytes = in_bytes;
   io.labels = labels_out;
   io.counts = counts_out;
   st = pipeline(c, (const double*)c->coords64.p, n, d, eps_sq, min_pts, formula, mem_cap,
