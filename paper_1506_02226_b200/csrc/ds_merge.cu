@@ -339,6 +339,31 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
       }
     }
     __syncthreads();
+    // Fast path: a core point without a smaller core neighbour is a local minimum. If
+    // the tile has at most one, every core point reaches it by following smaller
+    // neighbours, so the tile is one component rooted there (the common dense case):
+    // no pointer jumping, no tree merge.
+    {
+      const bool core0 = (lcw[tid >> 5] >> (31 - (tid & 31))) & 1u;
+      const bool root0 = core0 && lp[tid] == tid;
+      const uint32_t rb0 = __ballot_sync(0xffffffffu, root0);
+      if ((tid & 31) == 0) wroots[tid >> 5] = __popc(rb0);
+      if (root0) slot_root[0] = tid;  // read only when it is the single root
+      __syncthreads();
+      int nroots = 0;
+#pragma unroll
+      for (int q = 0; q < THREADS / 32; ++q) nroots += wroots[q];
+      if (nroots <= 1) {  // uniform per CTA
+        const int64_t g = (int64_t)base + tid;
+        if (g < n) {
+          if (nroots == 1 && core0 && tid != slot_root[0]) parent[g] = base + slot_root[0];
+          if (lb[tid] != NONE) atomicMin(&bmin[g], lb[tid]);
+        }
+        __syncthreads();  // smem is reused by the next tile
+        continue;
+      }
+      __syncthreads();  // wroots / slot_root are rewritten below
+    }
     // pointer jumping over the min-neighbour forest (9 halvings cover 512 nodes)
 #pragma unroll 1
     for (int r = 0; r < 9; ++r) {
