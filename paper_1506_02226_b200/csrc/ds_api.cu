@@ -56,7 +56,6 @@ struct Scalars {
   int32_t kept32;
   uint32_t unsafe_flag;
   int32_t nclusters;
-  int32_t units32;
 };
 
 // The per-call zero region: one memset clears the scalars, the spatial-sort bounding
@@ -77,7 +76,7 @@ struct ds_ctx {
   cudaEvent_t ev[8] = {};
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, bbox, blk, diag, ulist, uchunks, ucnt, dist, dbits;
+      keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -122,7 +121,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->counts64, &c->words, &c->chunks, &c->scalars, &c->dense,
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                      &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt,
+                      &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
                       &c->dist, &c->dbits};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
@@ -708,7 +707,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->counts64, &c->words,  &c->chunks, &c->scalars, &c->dense,
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
-                &c->sort_temp, &c->bbox, &c->blk, &c->diag, &c->ulist, &c->uchunks, &c->ucnt,
+                &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
                 &c->dist, &c->dbits};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
