@@ -222,8 +222,7 @@ def run_b200(args):
                 "stage3_merge": tm.stage3_merge_ms, "tile": tm.tile_ms}, 1
         t = ctx.run_dbscan_device(coords_dev.data_ptr(), n, d, params.eps_sq, params.min_pts,
                                   formula, mem_cap, labels_dev.data_ptr(), stream.cuda_stream)
-        extra = {"words_emitted": t.words_emitted, "tiles_nonempty": t.tiles_nonempty,
-                 "tiles_total": t.tiles_total}
+        extra = {"words_emitted": t.words_emitted, "tiles_kept": t.tiles_total}
         return t.tile_ms, t.pairs_evaluated, {"fused": t.fused_ms, "merge": t.merge_ms,
                                                "tile": t.tile_ms, **extra}, t.tile_launches
 
@@ -315,10 +314,10 @@ def run_b200(args):
     achieved = pairs * ops / tile_s / 1e12
     # kernels per step (1 GPU, culled schedule; the ncu launch list in profiles/): prep,
     # morton, 4 CUB radix-sort kernels, permute+bounds, 2 cull-row kernels, unit list,
-    # eps-unit, unit dir (+ core init), union diag, union links, roots, label scan,
-    # label = 17; a word-overflow re-run repeats the pipeline; sharded runs add the
-    # forest merge and a separate core init
-    launches_per_step = 17 * last[3] if world == 1 else 19
+    # eps-unit, union diag (+ core init), union links, roots, label scan, label = 16; a
+    # word-overflow re-run repeats the pipeline; sharded runs add the forest merge and
+    # a separate core init
+    launches_per_step = 16 * last[3] if world == 1 else 18
 
     line = {
         "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",

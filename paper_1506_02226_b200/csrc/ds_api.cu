@@ -64,7 +64,7 @@ constexpr size_t ZR_ALIGN = 256;
 inline size_t zr_round(size_t b) { return (b + ZR_ALIGN - 1) / ZR_ALIGN * ZR_ALIGN; }
 inline size_t zr_bbox() { return zr_round(sizeof(Scalars)); }
 inline size_t zr_diag() { return zr_bbox() + ZR_ALIGN; }
-inline size_t zr_scan(int64_t n) { return zr_diag() + zr_round((size_t)n_tiles(n) * 4); }
+inline size_t zr_scan(int64_t n) { return zr_diag() + zr_round((size_t)n_tiles(n) * 8); }
 inline size_t zr_bytes(int64_t n) { return zr_scan(n) + (size_t)scan_partials_len(n) * 4; }
 
 }  // namespace
@@ -173,6 +173,9 @@ size_t base_bytes(int64_t n, int d) {
          + (size_t)scan_partials_len(n) * 4 + sizeof(Scalars) + N * 8;  // labels
 }
 
+// the diagonal tile pairs' unit ranges (zero region; written by the unit list)
+uint2* diag_range(ds_ctx* c) { return (uint2*)((char*)c->scalars.p + zr_diag()); }
+
 MergeWs merge_ws(ds_ctx* c, int64_t n) {
   MergeWs w;
   Scalars* sc = (Scalars*)c->scalars.p;
@@ -189,12 +192,26 @@ MergeWs merge_ws(ds_ctx* c, int64_t n) {
   w.scan_state = (int32_t*)((char*)c->scalars.p + zr_scan(n));  // zeroed per call
   w.nclusters = &sc->nclusters;
   w.ncore = &sc->ncore;
-  w.diag_idx = (int32_t*)((char*)c->scalars.p + zr_diag());
   if (c->sorted) {
     w.perm = (const int32_t*)c->perm.p;
     w.inv = (const int32_t*)c->inv.p;
   }
   return w;
+}
+
+// core_init's job for the diagonal union pass (single GPU)
+CoreInit core_init_args(const MergeWs& w, int64_t min_pts) {
+  CoreInit ci;
+  ci.cnt = w.cnt;
+  ci.n = w.n;
+  ci.min_pts = min_pts;
+  ci.core = w.core;
+  ci.corew = w.corew;
+  ci.parent = w.parent;
+  ci.bmin = w.bmin;
+  ci.cmin = w.cmin;
+  ci.ncore = w.ncore;
+  return ci;
 }
 
 ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
@@ -234,11 +251,11 @@ struct Plan {
 // waits for the device: the adjacency-word buffer is sized from what earlier calls
 // needed, and an overflow (detected by check_words after the caller's single sync)
 // triggers one re-run with the exact size.
-// core_min_pts >= 1: the directory launch also initialises the core flags and the
-// union-find (single GPU, where the counts are complete after stage 1).
+// want_dir: also build the directory of tile pairs with words (the reference-layout
+// export reads it; stage 3 walks the units directly).
 ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                           int formula, int64_t mem_cap, cudaStream_t s, Plan& pl, int rank = 0,
-                          int world = 1, int64_t core_min_pts = 0) {
+                          int world = 1, bool want_dir = false) {
   ds_status st = alloc_common(c, n, d);
   if (st != DS_OK) return st;
   if (world < 1 || rank < 0 || rank >= world) {
@@ -363,7 +380,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     DS_CK(launch_unit_list((const float*)c->blk.p, n, d, eps32, formula, &sc->unsafe_flag,
                            (const uint32_t*)c->items.p, &sc->kept, pl.all_items, rank, world,
                            (uint2*)c->ulist.p, pl.units_cap, &sc->unit_count, (uint2*)c->ucnt.p,
-                           s));
+                           diag_range(c), s));
     a.unit_list = (const uint2*)c->ulist.p;
   }
   DS_CK(ensure(c->uchunks, (size_t)pl.units_cap * WPR * 8));
@@ -373,22 +390,9 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
   DS_CK(record(c, c->ev[2], s));
-  CoreInit ci;
-  if (core_min_pts >= 1) {
-    const MergeWs w = merge_ws(c, n);
-    ci.cnt = w.cnt;
-    ci.n = n;
-    ci.min_pts = core_min_pts;
-    ci.core = w.core;
-    ci.corew = w.corew;
-    ci.parent = w.parent;
-    ci.bmin = w.bmin;
-    ci.cmin = w.cmin;
-    ci.ncore = w.ncore;
-  }
-  DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const uint2*)c->ucnt.p : nullptr,
-                        &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count,
-                        (int32_t*)((char*)c->scalars.p + zr_diag()), ci, s));
+  if (want_dir)
+    DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const uint2*)c->ucnt.p : nullptr,
+                          &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count, s));
   return DS_OK;
 }
 
@@ -478,14 +482,12 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
     DS_CK(cudaMemcpyAsync((void*)d_coords, io->coords, io->in_bytes, cudaMemcpyHostToDevice, s));
   }
   DS_CK(rec(c->ev[0]));
-  ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl, 0, 1, min_pts);
+  ds_status st = stage12_enqueue(c, d_coords, n, d, eps_sq, formula, mem_cap, s, pl);
   if (st != DS_OK) return st;
   MergeWs w = merge_ws(c, n);
   w.scan_zeroed = true;
-  Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(rec(c->ev[3]));
-  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, (const uint4*)c->chunks.p,
-                            &sc->nonempty_count, s));
+  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
   DS_CK(rec(c->ev[4]));
@@ -795,7 +797,8 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
   Plan pl;
   for (int attempt = 1;; ++attempt) {
     DS_CK(cudaEventRecord(c->ev[0], s));
-    st = stage12_enqueue(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, pl);
+    st = stage12_enqueue(c, (const double*)c->coords64.p, n, d, eps_sq, formula, mem_cap, s, pl, 0,
+                         1, bits_out != nullptr);
     if (st != DS_OK) return st;
     const int32_t* perm = c->sorted ? (const int32_t*)c->perm.p : nullptr;
     DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, perm, (int64_t*)c->counts64.p, s));
@@ -954,8 +957,7 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
   DS_CK(launch_core_init(w, min_pts, s));
-  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, (const uint4*)c->chunks.p,
-                            &sc->nonempty_count, s));
+  DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), CoreInit{}, s));
   DS_CK(cudaMemcpyAsync(d_parent, c->parent.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   DS_CK(cudaMemcpyAsync(d_bmin, c->bmin.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   DS_CK(cudaEventRecord(c->ev[4], s));

@@ -152,15 +152,18 @@ cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint
 cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
                                 cudaStream_t s);
 // culled schedule: the row-unit list of this shard (kept items q = rank + k * world),
-// pieces of unit_cols column blocks; item_units[q] = {first unit, units}
+// pieces of unit_cols column blocks; item_units[q] = {first unit, units}; for a
+// diagonal pair (a, a) also diag_range[a] = {first unit lo, first unit hi << 16 |
+// units} (must be zero on entry)
 cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, int formula,
                              const uint32_t* unsafe_flag, const uint32_t* item_list,
                              const unsigned long long* kept, int64_t all_items, int rank, int world,
                              uint2* unit_list, unsigned long long units_cap,
-                             unsigned long long* unit_count, uint2* item_units, cudaStream_t s);
+                             unsigned long long* unit_count, uint2* item_units, uint2* diag_range,
+                             cudaStream_t s);
 // per tile pair with words: {a << 16 | b, first unit lo, units, first unit hi} (atomic append)
-// core_init's job (core flags, core words, union-find init), optionally fused into the
-// directory launch (single GPU: the counts are complete after the eps-tile kernel)
+// core_init's job (core flags, core words, union-find init), fused into the diagonal
+// union pass on one GPU (the counts are complete after the eps-tile kernel)
 struct CoreInit {
   const int32_t* cnt = nullptr;  // nullptr: skip
   int64_t n = 0, min_pts = 0;
@@ -171,12 +174,10 @@ struct CoreInit {
   int32_t* cmin = nullptr;
   unsigned long long* ncore = nullptr;
 };
-// also fills diag_idx[T] (1 + directory index of each diagonal tile pair; 0 = none,
-// the array must be zero on entry)
+// tile pairs with words (the reference-layout export walks them)
 cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
-                            unsigned long long* dir_count, int32_t* diag_idx, const CoreInit& ci,
-                            cudaStream_t s);
+                            unsigned long long* dir_count, cudaStream_t s);
 // 32-point block boxes [block][lo(dpad), hi(dpad), maxnorm] for sub-tile culling
 cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s);
 // tile bounding boxes + list of tile pairs that are not provably empty
@@ -206,16 +207,18 @@ struct MergeWs {
   bool scan_zeroed = false;       // scan_state was zeroed by the call's zero-region memset
   int32_t* nclusters;     // device scalar
   unsigned long long* ncore;
-  int32_t* diag_idx = nullptr;    // dir index of each diagonal tile pair (-1: none)
   const int32_t* perm = nullptr;  // sorted -> original index (nullptr: identity)
   const int32_t* inv = nullptr;   // original -> sorted index
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);
-// stage 3 over the stage-1 output: diagonal tile pairs from the directory (dir), the
-// off-diagonal ones walked per row unit of `units` (the eps-tile launch's arguments)
+// stage 3 over the stage-1 output, walked per row unit of `units` (the eps-tile
+// launch's arguments): diagonal tile pairs by tile (their units: diag_range for the
+// culled list, the triangle order otherwise), off-diagonal ones by unit. With ci.cnt
+// set, the diagonal pass also initialises the core flags and the union-find of its
+// tile (core_init's job; the counts must be complete).
 cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lane_blocks,
-                                const uint4* dir, const unsigned long long* ndir, cudaStream_t s);
+                                const uint2* diag_range, const CoreInit& ci, cudaStream_t s);
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);

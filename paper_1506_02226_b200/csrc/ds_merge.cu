@@ -250,10 +250,8 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
 __global__ void __launch_bounds__(512) union_diag_kernel(
-    const uint4* __restrict__ dir, const uint2* __restrict__ uchunks,
-    const int32_t* __restrict__ diag_idx, int64_t ntiles,
-    const uint2* __restrict__ words, unsigned long long words_cap, int64_t n,
-    const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
+    const UnitArgs A, int LB, const uint2* __restrict__ diag_range, const CoreInit ci,
+    const uint32_t* __restrict__ corew_in, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
   griddep_wait();
   constexpr int THREADS = 512;
@@ -270,16 +268,55 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   __shared__ int ntrees_sh;
   const int tid = threadIdx.x;
   const int w = tid % WPR, cblk = tid / WPR;
+  const int64_t n = A.n;
+  const int64_t ntiles = A.T;
   const int64_t nw = (n + 31) / 32;
+  const uint2* __restrict__ uchunks = A.uchunks;
+  const uint2* __restrict__ words = A.words;
+  const unsigned long long words_cap = A.words_cap;
+  long long r_lo, r_hi;
+  unit_range(A, r_lo, r_hi);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int c = diag_idx[tile] - 1;  // 0 = no diagonal chunk
-    if (c < 0) continue;  // uniform per CTA
-    const DirInfo ci = decode_dir(dir[c]);
-    const int base = ci.a * TILE;
-    if (tid < WPR) {
-      const int64_t gw = (int64_t)ci.a * WPR + tid;
-      lcw[tid] = gw < nw ? corew[gw] : 0u;
+    const int base = (int)tile * TILE;
+    if (ci.cnt) {  // core_init for the tile's points (kernels.py:335); one word per warp
+      const int64_t i = base + tid;
+      const bool c = i < n && (int64_t)ci.cnt[i] >= ci.min_pts;
+      const uint32_t ballot = __ballot_sync(0xffffffffu, c);
+      if (i < n) {
+        ci.core[i] = c ? 1 : 0;
+        parent[i] = (int32_t)i;
+        bmin[i] = NONE;
+        ci.cmin[i] = NONE;
+      }
+      if ((tid & 31) == 0) {
+        const int64_t gw = (int64_t)tile * WPR + (tid >> 5);
+        if (gw < nw) ci.corew[gw] = __brev(ballot);  // bit 31 - t <-> point 32w + t
+        lcw[tid >> 5] = __brev(ballot);
+        if (ballot) atomicAdd(ci.ncore, (unsigned long long)__popc(ballot));
+      }
+    } else if (tid < WPR) {
+      const int64_t gw = (int64_t)tile * WPR + tid;
+      lcw[tid] = gw < nw ? corew_in[gw] : 0u;
     }
+    // the diagonal pair's chunk entries: its units (culled list: diag_range; dense: the
+    // triangle order, clipped to this launch's shard) own entries [u * WPR, ...)
+    long long u_lo = 0, u_hi = 0;
+    if (A.unit_list) {
+      const uint2 dr = diag_range[tile];
+      u_lo = (long long)dr.x | ((long long)(dr.y >> 16) << 32);
+      u_hi = u_lo + (long long)(dr.y & 0xffffu);
+      if (u_hi > r_hi) u_hi = r_hi;  // list overflow: the host re-runs
+    } else {
+      const long long q = row_offset(tile, ntiles);
+      u_lo = q * LB > r_lo ? q * LB : r_lo;
+      u_hi = (q + 1) * LB < r_hi ? (q + 1) * LB : r_hi;
+    }
+    if (u_lo >= u_hi) {  // no words on this launch: only the core init (uniform per CTA)
+      __syncthreads();
+      continue;
+    }
+    const long long e_lo = u_lo * WPR;
+    const int nentries = (int)((u_hi - u_lo) * WPR);
     for (int k = tid; k < WPR * TILE; k += THREADS) R[k] = 0u;
     for (int v = tid; v < TILE; v += THREADS) {
       lp[v] = v;
@@ -290,8 +327,8 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     // scatter the tile pair's words into the dense matrix (core rows, core columns
     // only), one warp per chunk entry; non-core rows give their own border candidate
     // directly. Entries of an overflowed run are skipped (the host re-runs).
-    for (int e = tid >> 5; e < ci.nunits; e += THREADS / 32) {
-      const uint2 ce = uchunks[ci.ulo + e];
+    for (int e = tid >> 5; e < nentries; e += THREADS / 32) {
+      const uint2 ce = uchunks[e_lo + e];
       const uint32_t cnt = ce.y & 0xffffu;
       const unsigned long long wb = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
       if (cnt == 0u || wb + cnt > words_cap) continue;  // warp-uniform
@@ -883,14 +920,11 @@ cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s) 
 }
 
 cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lane_blocks,
-                                const uint4* dir, const unsigned long long* ndir, cudaStream_t s) {
-  const uint2* words = units.words;
-  const unsigned long long words_cap = units.words_cap;
-  const uint2* uchunks = units.uchunks;
+                                const uint2* diag_range, const CoreInit& ci, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // round 1: one chunk per tile (few, dense) -> wide CTAs; round 2: many chunks
+  // round 1: one CTA per tile (wide, dense in shared memory); round 2: a warp per unit
   const size_t diag_smem = (size_t)(WPR * TILE + 512) * 4 + (size_t)3 * TILE * 4;
   static bool diag_cfg = false;
   if (!diag_cfg) {
@@ -899,12 +933,10 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
     diag_cfg = true;
   }
   const int64_t ntiles = (w.n + TILE - 1) / TILE;
-  // diag_idx was filled by the directory launch (launch_unit_dir)
-  // one CTA per tile (one wave: up to 4 resident per SM)
   const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
-  cudaError_t e = launch_pdl(union_diag_kernel, dim3((unsigned)grid), dim3(512), diag_smem, s, dir,
-                             uchunks, (const int32_t*)w.diag_idx, ntiles, words, words_cap, w.n,
-                             (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
+  cudaError_t e = launch_pdl(union_diag_kernel, dim3((unsigned)grid), dim3(512), diag_smem, s, units,
+                             lane_blocks, diag_range, ci, (const uint32_t*)w.corew, w.parent,
+                             w.bmin, w.perm);
   if (e != cudaSuccess) return e;
   static int links_per_sm = 0;  // one resident wave: warps take units grid-stride
   if (!links_per_sm) {

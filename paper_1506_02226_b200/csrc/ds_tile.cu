@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
     const uint32_t* __restrict__ unsafe_flag, const uint32_t* __restrict__ items,
     const unsigned long long* __restrict__ kept, int rank, int world, uint2* __restrict__ list,
     unsigned long long cap, unsigned long long* __restrict__ unit_count,
-    uint2* __restrict__ item_units) {
+    uint2* __restrict__ item_units, uint2* __restrict__ diag_range) {
   griddep_wait();
   constexpr int W = 8;  // warps per CTA; one list reservation per CTA and round
   __shared__ int wcnt[W];
@@ -714,7 +714,9 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
     __syncthreads();
     if (t < mine && lane == 0) {
       unsigned long long pos = wpos[warp];
-      item_units[q] = make_uint2((uint32_t)pos, (uint32_t)c | ((uint32_t)(pos >> 32) << 16));
+      const uint2 iu = make_uint2((uint32_t)pos, (uint32_t)c | ((uint32_t)(pos >> 32) << 16));
+      item_units[q] = iu;
+      if ((ab >> 16) == (ab & 0xffffu)) diag_range[ab >> 16] = iu;  // for union_diag
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
 #pragma unroll
@@ -740,15 +742,10 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
 // Per item: its row units [lo, hi) (culled: item_units of this shard's items; dense:
 // the triangle order, clipped to the shard) own chunk entries [lo * WPR, hi * WPR);
 // the item gets a directory entry if any of them holds words.
-// Diagonal tile pairs also record their directory index (diag_idx[a], -1 preset)
-// for union_diag_kernel. With ci.cnt set, the same launch also does core_init's job
-// (ds_merge.cu): core flags, core words, union-find and border-minimum init, one
-// warp per 32 points after the items.
 template <int KP>
 __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2* __restrict__ item_units,
                                 const unsigned long long* __restrict__ kept, uint4* __restrict__ dir,
-                                unsigned long long* __restrict__ dir_count,
-                                int32_t* __restrict__ diag_idx, const CoreInit ci) {
+                                unsigned long long* __restrict__ dir_count) {
   griddep_wait();
   constexpr int LB = TILE / (32 * KP);
   long long r_lo, r_hi;
@@ -788,25 +785,6 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2
       const unsigned long long e = atomicAdd(dir_count, 1ull);
       dir[e] = make_uint4(((uint32_t)a << 16) | (uint32_t)b, (uint32_t)c_lo, (uint32_t)(c_hi - c_lo),
                           (uint32_t)((unsigned long long)c_lo >> 32));
-      if (a == b) diag_idx[a] = (int32_t)e + 1;
-    }
-  }
-  if (ci.cnt) {  // core_init (kernels.py:335): warp per 32 points
-    const int64_t nb = (ci.n + 31) / 32;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nb; w += nwarps) {
-      const int64_t i = w * 32 + lane;
-      const bool c = i < ci.n && (int64_t)ci.cnt[i] >= ci.min_pts;
-      const uint32_t ballot = __ballot_sync(0xffffffffu, c);
-      if (i < ci.n) {
-        ci.core[i] = c ? 1 : 0;
-        ci.parent[i] = (int32_t)i;
-        ci.bmin[i] = NONE;
-        ci.cmin[i] = NONE;
-      }
-      if (lane == 0) {
-        ci.corew[w] = __brev(ballot);  // bit 31 - t <-> point 32w + t
-        if (ballot) atomicAdd(ci.ncore, (unsigned long long)__popc(ballot));
-      }
     }
   }
 }
@@ -1182,7 +1160,8 @@ cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, in
                              const uint32_t* unsafe_flag, const uint32_t* item_list,
                              const unsigned long long* kept, int64_t all_items, int rank, int world,
                              uint2* unit_list, unsigned long long units_cap,
-                             unsigned long long* unit_count, uint2* item_units, cudaStream_t s) {
+                             unsigned long long* unit_count, uint2* item_units, uint2* diag_range,
+                             cudaStream_t s) {
   const int dp = pad_dim(d);
   const int KP = unit_kp(d);
   const float* box = dp <= 4 ? blk : nullptr;  // block boxes only pay off in low dimension
@@ -1190,27 +1169,25 @@ cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, in
   if (blocks > 148 * 16) blocks = 148 * 16;
   return launch_pdl(unit_list_kernel, dim3((unsigned)blocks), dim3(256), 0, s, box, dp, n, KP, eps32,
                     formula, unsafe_flag, item_list, kept, rank, world, unit_list, units_cap,
-                    unit_count, item_units);
+                    unit_count, item_units, diag_range);
 }
 
 cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const uint2* item_units,
                             const unsigned long long* kept, uint4* dir,
-                            unsigned long long* dir_count, int32_t* diag_idx, const CoreInit& ci,
-                            cudaStream_t s) {
+                            unsigned long long* dir_count, cudaStream_t s) {
   int64_t blocks = (all_items * 32 + 255) / 256;
-  if (ci.cnt) blocks = std::max<int64_t>(blocks, (ci.n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   switch (unit_kp(d)) {
     case 4:
       return launch_pdl(unit_dir_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
-                        item_units, kept, dir, dir_count, diag_idx, ci);
+                        item_units, kept, dir, dir_count);
     case 2:
       return launch_pdl(unit_dir_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
-                        item_units, kept, dir, dir_count, diag_idx, ci);
+                        item_units, kept, dir, dir_count);
     default:
       return launch_pdl(unit_dir_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, s, a, all_items,
-                        item_units, kept, dir, dir_count, diag_idx, ci);
+                        item_units, kept, dir, dir_count);
   }
   return cudaGetLastError();
 }

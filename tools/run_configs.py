@@ -55,7 +55,7 @@ def main():
             "d2h_ms": statistics.median(r.d2h_ms for r in runs),
             "pairs_evaluated": runs[-1].pairs_evaluated,
             "n2": pts.n * pts.n,
-            "tiles_total": runs[-1].tiles_total, "tiles_nonempty": runs[-1].tiles_nonempty,
+            "tiles_kept": runs[-1].tiles_total,
             "words": runs[-1].words_emitted, "clusters": labeling.cluster_count(),
             "noise": labeling.noise_count(), "cores": runs[-1].core_count,
         }
