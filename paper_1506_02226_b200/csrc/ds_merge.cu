@@ -766,9 +766,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
 }
 
 // Single-pass exclusive scan (decoupled look-back): tiles of SCAN_BLK elements are
-// taken in ticket order; each tile publishes its aggregate, then thread 0 walks back
-// over the predecessors' published {flag, value} words until it meets an inclusive
-// prefix, and publishes its own. state[] and the ticket are zeroed before the launch.
+// taken in ticket order; each tile publishes its aggregate, then warp 0 reads the
+// predecessors' published {flag, value} words 32 at a time until it meets an
+// inclusive prefix, and publishes its own. state[] and the ticket are zeroed before
+// the launch.
 constexpr unsigned long long SC_AGG = 1ull << 62, SC_PRE = 2ull << 62;
 
 // scan input: the array itself
@@ -809,25 +810,39 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* d
   }
   int agg;
   const int excl = block_exclusive_scan(sum, agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: publish the aggregate, look back 32 tiles at a time
+    const int lane = threadIdx.x;
     volatile unsigned long long* st = state;
     int prefix = 0;
     if (tile == 0) {
-      st[0] = SC_PRE | (unsigned int)agg;
+      if (lane == 0) st[0] = SC_PRE | (unsigned int)agg;
     } else {
-      st[tile] = SC_AGG | (unsigned int)agg;
-      for (int64_t j = (int64_t)tile - 1; j >= 0;) {
-        const unsigned long long w = st[j];
-        if (!(w >> 62)) continue;  // predecessor not published yet
-        prefix += (int)(unsigned int)w;
-        if ((w >> 62) == 2) break;
-        --j;
+      if (lane == 0) st[tile] = SC_AGG | (unsigned int)agg;
+      int64_t hi = (int64_t)tile - 1;  // predecessors hi, hi-1, ... still to add
+      for (;;) {
+        const int64_t j = hi - lane;
+        const unsigned long long w = j >= 0 ? st[j] : (2ull << 62);  // before tile 0: prefix 0
+        const unsigned flag = (unsigned)(w >> 62);
+        const unsigned pre = __ballot_sync(0xffffffffu, flag == 2u);
+        const int stop = pre ? __ffs(pre) - 1 : 31;  // nearest inclusive prefix in reach
+        const unsigned need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+        if (__ballot_sync(0xffffffffu, flag == 0u) & need) continue;  // not published yet
+        int v = lane <= stop ? (int)(unsigned int)w : 0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        prefix += v;
+        if (pre) break;
+        hi -= 32;
       }
-      __threadfence();
-      st[tile] = SC_PRE | (unsigned int)(prefix + agg);
+      if (lane == 0) {
+        __threadfence();
+        st[tile] = SC_PRE | (unsigned int)(prefix + agg);
+      }
     }
-    prefix_sh = prefix;
-    if ((int64_t)(tile + 1) * SCAN_BLK >= n) *total = prefix + agg;  // last tile
+    if (lane == 0) {
+      prefix_sh = prefix;
+      if ((int64_t)(tile + 1) * SCAN_BLK >= n) *total = prefix + agg;  // last tile
+    }
   }
   __syncthreads();
   int run = prefix_sh + excl;
