@@ -327,8 +327,12 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     // scatter the tile pair's words into the dense matrix (core rows, core columns
     // only), one warp per chunk entry; non-core rows give their own border candidate
     // directly. Entries of an overflowed run are skipped (the host re-runs).
-    for (int e = tid >> 5; e < nentries; e += THREADS / 32) {
-      const uint2 ce = uchunks[e_lo + e];
+    // the warp's chunk entries e = warp + 16 i are loaded together (lane i holds entry i)
+    const int nmine = nentries > (tid >> 5) ? (nentries - (tid >> 5) + THREADS / 32 - 1) / (THREADS / 32) : 0;
+    const uint2 mine = (tid & 31) < nmine ? uchunks[e_lo + (tid >> 5) + (THREADS / 32) * (tid & 31)]
+                                          : make_uint2(0u, 0u);
+    for (int i = 0; i < nmine; ++i) {  // nmine <= 32: 16 warps, <= 256 entries per tile pair
+      const uint2 ce = make_uint2(__shfl_sync(0xffffffffu, mine.x, i), __shfl_sync(0xffffffffu, mine.y, i));
       const uint32_t cnt = ce.y & 0xffffu;
       const unsigned long long wb = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
       if (cnt == 0u || wb + cnt > words_cap) continue;  // warp-uniform
