@@ -377,3 +377,17 @@ def test_graph_replay_with_new_data(ds, oracle):
     labels, _, _ = ctx.run_dbscan(sets[2], params.eps_sq, 5, 1, 0)
     ctx.set_cuda_graph(True)
     assert np.array_equal(labels, oracle.dbscan(sets[2], params.eps_sq, 5, 1)[0])
+
+
+def test_public_api_graph_replay_repoints_host_buffers(ds, oracle):
+    """run_dbscan through the public API: page-locked PointSet coordinates and label
+    buffers, so from the second call on the label copy is a recorded graph node that
+    is re-pointed at every call's fresh buffer; alternate data sets of one shape."""
+    params = ds.validate_params(0.2, 5)
+    sets = [ds.generate_blobs(7000, 4, 0.3, 0.1, s, 2) for s in (11, 12, 13)]
+    conf = ds.default_config()
+    for rnd in range(3):
+        for pts in sets:
+            labeling, _ = ds.run_dbscan(pts, params, conf)
+            want, _ = oracle.dbscan(pts.coords_aos, params.eps_sq, 5, 1)
+            assert np.array_equal(labeling.labels, want), rnd
