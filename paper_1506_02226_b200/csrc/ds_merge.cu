@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
 // Links go through the global lock-free union-find (link_root: CAS hooks the larger
 // root under the smaller), so the result does not depend on the order.
 constexpr int LINK_WARPS = 8;
-__global__ void __launch_bounds__(LINK_WARPS * 32) union_links_kernel(
+__global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
     const UnitArgs A, int LB, const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
   griddep_wait();
