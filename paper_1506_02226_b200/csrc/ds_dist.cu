@@ -7,9 +7,9 @@
 //   dist_kernel       out[i][j] = ((x_j - x_i)^2 + (y_j - y_i)^2) + (z_j - z_i)^2 ...
 //                     in float32, every op separately rounded (no FMA), the d-dim form
 //                     extended left to right. HBM-write bound: 4 bytes per pair; each
-//                     thread owns 4 consecutive columns (one float4 store per row) and
-//                     walks DIST_ROWS rows, so the column records are read once per
-//                     DIST_ROWS rows.
+//                     thread owns 4 consecutive columns (one float4 store per row; one
+//                     column above 16-D) and walks DIST_ROWS rows, so the column
+//                     records are read once per DIST_ROWS rows.
 //   threshold_kernel  bits (numpy packbits layout: MSB-first bytes, ceil(n/8) per row)
 //                     of d <= eps32 (NaN -> 0, like numpy) and int64 row counts.
 //                     HBM-read bound: 4 bytes per pair.
@@ -25,15 +25,23 @@ namespace {
 constexpr int DIST_THREADS = 256;
 constexpr int DIST_ROWS = 16;
 
+// CPT columns per thread: 4 (one float4 store per row) up to 16-D; wider records keep
+// one column per thread so the column records stay in registers
+template <int D>
+struct DistGeo {
+  static constexpr int CPT = D <= 16 ? 4 : 1;
+};
+
 template <int D>
 __global__ void __launch_bounds__(DIST_THREADS) dist_kernel(const float* __restrict__ rec, int S,
                                                             int64_t n, int64_t row0, int64_t rows,
                                                             int64_t pitch, float* __restrict__ out) {
-  const int64_t j0 = ((int64_t)blockIdx.x * DIST_THREADS + threadIdx.x) * 4;
+  constexpr int CPT = DistGeo<D>::CPT;
+  const int64_t j0 = ((int64_t)blockIdx.x * DIST_THREADS + threadIdx.x) * CPT;
   if (j0 >= n) return;
-  float cj[4][D];
+  float cj[CPT][D];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < CPT; ++t) {
     const int64_t j = j0 + t < n ? j0 + t : n - 1;
 #pragma unroll
     for (int q = 0; q < D; ++q) cj[t][q] = __ldg(rec + j * S + q);
@@ -46,9 +54,9 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_kernel(const float* __restr
     float ci[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) ci[q] = __ldg(rec + i * S + q);
-    float v[4];
+    float v[CPT];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < CPT; ++t) {
       float dx = __fsub_rn(cj[t][0], ci[0]);  // column minus row (kernels.py:205)
       float acc = __fmul_rn(dx, dx);
 #pragma unroll
@@ -59,8 +67,10 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_kernel(const float* __restr
       v[t] = acc;
     }
     float* dst = out + il * pitch + j0;
-    if (j0 + 3 < pitch) {
-      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+    if constexpr (CPT == 4) {
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);  // j0 + 3 < pitch
+    } else {
+      dst[0] = v[0];
     }
   }
 }
@@ -107,7 +117,8 @@ __global__ void __launch_bounds__(256) threshold_kernel(const float* __restrict_
 template <int D>
 cudaError_t launch_dist_d(const float* rec, int S, int64_t n, int64_t row0, int64_t rows,
                           int64_t pitch, float* out, cudaStream_t s) {
-  const dim3 grid((unsigned)((n + 4 * DIST_THREADS - 1) / (4 * DIST_THREADS)),
+  constexpr int CPT = DistGeo<D>::CPT;
+  const dim3 grid((unsigned)((n + CPT * DIST_THREADS - 1) / (CPT * DIST_THREADS)),
                   (unsigned)((rows + DIST_ROWS - 1) / DIST_ROWS));
   dist_kernel<D><<<grid, DIST_THREADS, 0, s>>>(rec, S, n, row0, rows, pitch, out);
   return cudaGetLastError();

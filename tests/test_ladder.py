@@ -107,7 +107,7 @@ def test_run_variant_materialising_rungs(ds, rung):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,d", [(1, 3), (7, 2), (1000, 3), (3001, 5), (513, 16)])
+@pytest.mark.parametrize("n,d", [(1, 3), (7, 2), (1000, 3), (3001, 5), (513, 16), (129, 24), (300, 40)])
 def test_dist_matrix_vs_oracle_random(ds, n, d, rng):
     from oracle import densescan_oracle as oracle
     pts = rng.normal(0, 3, (n, d)) + rng.uniform(-50, 50, d)
