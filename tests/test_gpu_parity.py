@@ -391,3 +391,47 @@ def test_public_api_graph_replay_repoints_host_buffers(ds, oracle):
             labeling, _ = ds.run_dbscan(pts, params, conf)
             want, _ = oracle.dbscan(pts.coords_aos, params.eps_sq, 5, 1)
             assert np.array_equal(labeling.labels, want), rnd
+
+
+def _degenerate_cases(rng):
+    """(name, coords, eps, min_pts): inputs that stress the spatial order, the
+    culling bounds and the merge rather than the formula."""
+    line = np.zeros((3000, 3))
+    line[:, 0] = np.arange(3000) * 0.5  # spacing == eps: every neighbour an exact tie
+    far = rng.normal(0, 1e-3, (6000, 3)) + np.array([1.5e4, -2.5e4, 7e3])
+    far[::7] += rng.normal(0, 0.05, (len(far[::7]), 3))
+    same = np.full((5000, 3), 3.25)
+    same_out = same.copy()
+    same_out[:4] = [[1e3, 0, 0], [-1e3, 5, 5], [0, 2e3, 0], [3.25, 3.25, 3.26]]
+    grid = np.array([[x, y, 0.0] for x in range(80) for y in range(80)], dtype=float) * 0.1
+    return [
+        ("identical", same, 1e-3, 10),
+        ("identical_outliers", same_out, 0.02, 10),
+        ("line_ties", line, 0.5, 3),
+        ("far_offset", far, 4e-3, 5),  # |x| ~ 2.5e4: the algebraic form cancels badly
+        ("grid_ties", grid, 0.1, 5),
+        ("all_noise", rng.uniform(0, 1, (4000, 3)), 0.05, 10_000),
+        ("one_cluster", rng.uniform(0, 1, (4000, 3)), 10.0, 2),
+    ]
+
+
+def test_degenerate_inputs_against_oracle(ds, rng):
+    """Identical points (zero-span bounding box, one Morton cell), exact ties on a line
+    and a grid, a tiny cluster far from the origin, MinPts above n and eps above the
+    diameter: labels and counts equal the C oracle's for both formulas, with the
+    default (sorted, culled) and the dense schedule."""
+    from oracle import c_oracle
+    ctx = ds._native.context()
+    for name, coords, eps, min_pts in _degenerate_cases(rng):
+        params = ds.validate_params(eps, min_pts)
+        for fname, formula in FORMULAS.items():
+            want, wc = c_oracle.dbscan(coords, params.eps_sq, min_pts, formula)
+            for prune in (True, False):
+                ctx.configure(prune, prune)
+                try:
+                    labels, counts, _ = ctx.run_dbscan(coords, params.eps_sq, min_pts, formula,
+                                                       0, want_counts=True)
+                finally:
+                    ctx.configure(True, True)
+                assert np.array_equal(counts, wc), (name, fname, prune)
+                assert np.array_equal(labels, want), (name, fname, prune)
