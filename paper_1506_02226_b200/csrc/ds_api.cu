@@ -3,6 +3,8 @@
 // run_dbscan (pkg/src/densescan/pipeline.py:70-92), fused_build[_algebraic]
 // (kernels.py:420-442) and merge_iterative (merge.py:133-166).
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include <algorithm>
@@ -97,7 +99,8 @@ struct ds_ctx {
 
 namespace {
 
-static unsigned long long g_alloc_generation = 0;  // bumped whenever a buffer moves
+// bumped whenever a buffer moves (any context, any thread): recorded graphs compare it
+static std::atomic<unsigned long long> g_alloc_generation{0};
 
 cudaError_t ensure(Buf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
@@ -545,7 +548,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[5] = (unsigned long long)(uintptr_t)d_labels;
     key[6] = (unsigned long long)(uintptr_t)d_counts64;
     key[7] = c->words_cap;
-    key[8] = g_alloc_generation;
+    key[8] = g_alloc_generation.load();
     key[9] = (unsigned long long)mem_cap;
     key[10] = (unsigned long long)c->device;
     key[11] = c->units_cap;
@@ -583,7 +586,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
         cudaGraphDestroy(c->graph);
         c->graph = nullptr;
       }
-      const unsigned long long gen0 = g_alloc_generation;
+      const unsigned long long gen0 = g_alloc_generation.load();
       // the legacy default stream cannot be captured: record on the context's own
       // stream (nothing executes while recording) and launch on the caller's
       cudaStream_t cap = (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread)
@@ -600,7 +603,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
         return st;
       }
       DS_CK(ce);
-      if (gen0 != g_alloc_generation) {  // a buffer moved while recording: run eagerly
+      if (gen0 != g_alloc_generation.load()) {  // a buffer moved while recording: run eagerly
         cudaGraphDestroy(graph);
         st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap, d_labels,
                             d_counts64, s, pl, false, io);
@@ -620,7 +623,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       if (st != DS_OK) return st;
       // key after this call's allocations: the next identical call records the graph
       key[7] = c->words_cap;
-      key[8] = g_alloc_generation;
+      key[8] = g_alloc_generation.load();
       key[11] = c->units_cap;
       std::memcpy(c->seen_key, key, sizeof key);
     }

@@ -33,6 +33,7 @@ constexpr int KPT = TILE / NT;        // lane points owned by one thread
 constexpr int WPR = TILE / 32;        // adjacency words per point per tile
 constexpr int BSTRIDE = TILE + 8;     // smem stride of one word column (bank padding)
 constexpr int MAX_D = 64;
+constexpr int DS_MAX_DEVICES = 64;    // per-device launch configuration caches
 constexpr int32_t NONE = 0x7fffffff;  // "no core" marker in bmin / cmin
 
 int padded_dim(int d);  // tile kernels are instantiated for d in {1,2,3,4,8,16,32,64}

@@ -16,6 +16,8 @@
 // All kernels here are HBM/L2 bound: they stream the adjacency words once and
 // touch O(n) int32 arrays that stay L2-resident (4n <= 8 MB at C5).
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include "ds_internal.cuh"
@@ -945,11 +947,17 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // round 1: one CTA per tile (wide, dense in shared memory); round 2: a warp per unit
   const size_t diag_smem = (size_t)(WPR * TILE + 512) * 4 + (size_t)3 * TILE * 4;
-  static bool diag_cfg = false;
-  if (!diag_cfg) {
+  // kernel attributes and occupancy are per device (idempotent if raced)
+  static std::atomic<int> links_per_sm_dev[DS_MAX_DEVICES] = {};
+  int links_per_sm = dev < DS_MAX_DEVICES ? links_per_sm_dev[dev].load() : 0;
+  if (links_per_sm == 0) {
     cudaFuncSetAttribute(union_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)diag_smem);
-    diag_cfg = true;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&links_per_sm, union_links_kernel,
+                                                      LINK_WARPS * 32, 0) != cudaSuccess ||
+        links_per_sm < 1)
+      links_per_sm = 4;
+    if (dev < DS_MAX_DEVICES) links_per_sm_dev[dev].store(links_per_sm);
   }
   const int64_t ntiles = (w.n + TILE - 1) / TILE;
   const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
@@ -957,13 +965,7 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
                              lane_blocks, diag_range, ci, (const uint32_t*)w.corew, w.parent,
                              w.bmin, w.perm);
   if (e != cudaSuccess) return e;
-  static int links_per_sm = 0;  // one resident wave: warps take units grid-stride
-  if (!links_per_sm) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&links_per_sm, union_links_kernel,
-                                                      LINK_WARPS * 32, 0) != cudaSuccess ||
-        links_per_sm < 1)
-      links_per_sm = 4;
-  }
+  // one resident wave of union_links: warps take units grid-stride
   return launch_pdl(union_links_kernel, dim3(sms * links_per_sm), dim3(LINK_WARPS * 32), 0, s, units,
                     lane_blocks, (const uint32_t*)w.corew, w.parent, w.bmin, w.perm);
 }

@@ -24,6 +24,8 @@
 // to HBM for stage 3 with their local row and column block, one chunk entry per
 // (unit, column block).
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include <algorithm>
@@ -1068,16 +1070,19 @@ template <int D, int F>
 cudaError_t launch_df(const UnitArgs& a, int sm_count, cudaStream_t s) {
   using G = Geo<D>;
   auto kern = eps_unit_kernel<D, F>;
-  static bool configured = false;
-  static int per_sm = 1;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+  // kernel attributes are per device: configure once per device (idempotent if raced)
+  static std::atomic<int> per_sm_dev[DS_MAX_DEVICES] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int per_sm = dev < DS_MAX_DEVICES ? per_sm_dev[dev].load() : 0;
+  if (per_sm == 0) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, G::SMEM);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
-    configured = true;
+    if (dev < DS_MAX_DEVICES) per_sm_dev[dev].store(per_sm);
   }
   return launch_pdl(kern, dim3((unsigned)(sm_count * per_sm)), dim3(G::THREADS), G::SMEM, s, a);
 }
