@@ -251,6 +251,12 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 }
 
 // Round 1. THREADS = 512: thread (w, c) owns column word w and row block c.
+// Row stride of union_diag's dense adjacency R (word column ww, row u at ww * DIAG_RS + u):
+// one word of padding puts the 16 word columns of a row in different banks, so the
+// row-block scans (thread = word column x row block) are conflict-free (a stride of
+// TILE made them 16-way conflicts)
+constexpr int DIAG_RS = TILE + 1;
+
 __global__ void __launch_bounds__(512) union_diag_kernel(
     const UnitArgs A, int LB, const uint2* __restrict__ diag_range, const CoreInit ci,
     const uint32_t* __restrict__ corew_in, int32_t* parent, int32_t* bmin,
@@ -259,8 +265,8 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
   constexpr int THREADS = 512;
   constexpr int RB = TILE / (THREADS / WPR);  // rows per block: 16
   extern __shared__ uint32_t dsm[];
-  uint32_t* R = dsm;                         // [WPR][TILE] core-masked adjacency words
-  uint32_t* M = R + WPR * TILE;              // [THREADS / WPR][WPR] row-block column masks
+  uint32_t* R = dsm;                         // [WPR][DIAG_RS] core-masked adjacency words
+  uint32_t* M = R + WPR * DIAG_RS;           // [THREADS / WPR][WPR] row-block column masks
   int* lp = reinterpret_cast<int*>(M + THREADS);
   int* lb = lp + TILE;
   int* hist = lb + TILE;
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     }
     const long long e_lo = u_lo * WPR;
     const int nentries = (int)((u_hi - u_lo) * WPR);
-    for (int k = tid; k < WPR * TILE; k += THREADS) R[k] = 0u;
+    for (int k = tid; k < WPR * DIAG_RS; k += THREADS) R[k] = 0u;
     for (int v = tid; v < TILE; v += THREADS) {
       lp[v] = v;
       lb[v] = NONE;
@@ -333,46 +339,58 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     const int nmine = nentries > (tid >> 5) ? (nentries - (tid >> 5) + THREADS / 32 - 1) / (THREADS / 32) : 0;
     const uint2 mine = (tid & 31) < nmine ? uchunks[e_lo + (tid >> 5) + (THREADS / 32) * (tid & 31)]
                                           : make_uint2(0u, 0u);
+    // An entry holds at most 32*KP <= 128 words: lane l takes words l + 32 q, q < 4,
+    // all loaded before any is scattered (one L2 round trip per entry instead of up to
+    // four dependent ones)
+    auto scatter = [&](const uint2 rec) {
+      const int u = (int)(rec.y >> 4);
+      const int ww = (int)(rec.y & 15u);
+      const uint32_t cw = lcw[ww];
+      if ((lcw[u >> 5] >> (31 - (u & 31))) & 1u) {
+        R[ww * DIAG_RS + u] = rec.x & cw;
+        uint32_t bm = rec.x & ~cw;  // core u in range of non-core v (merge.py:116-130)
+        if (bm) {
+          const int gu = orig_of(perm, base + u);
+          while (bm) {
+            const int t = __clz(bm);
+            bm &= ~(0x80000000u >> t);
+            atomicMin(&lb[ww * 32 + t], gu);
+          }
+        }
+      } else {
+        const uint32_t cm = rec.x & cw;
+        if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
+      }
+    };
     for (int i = 0; i < nmine; ++i) {  // nmine <= 32: 16 warps, <= 256 entries per tile pair
       const uint2 ce = make_uint2(__shfl_sync(0xffffffffu, mine.x, i), __shfl_sync(0xffffffffu, mine.y, i));
       const uint32_t cnt = ce.y & 0xffffu;
       const unsigned long long wb = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
       if (cnt == 0u || wb + cnt > words_cap) continue;  // warp-uniform
-      for (uint32_t k = tid & 31; k < cnt; k += 32) {
-        const uint2 rec = words[wb + k];
-        const int u = (int)(rec.y >> 4);
-        const int ww = (int)(rec.y & 15u);
-        const uint32_t cw = lcw[ww];
-        if ((lcw[u >> 5] >> (31 - (u & 31))) & 1u) {
-          R[ww * TILE + u] = rec.x & cw;
-          uint32_t bm = rec.x & ~cw;  // core u in range of non-core v (merge.py:116-130)
-          if (bm) {
-            const int gu = orig_of(perm, base + u);
-            while (bm) {
-              const int t = __clz(bm);
-              bm &= ~(0x80000000u >> t);
-              atomicMin(&lb[ww * 32 + t], gu);
-            }
-          }
-        } else {
-          const uint32_t cm = rec.x & cw;
-          if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
-        }
-      }
+      const uint32_t k0 = tid & 31;
+      const uint2 r0 = k0 < cnt ? words[wb + k0] : make_uint2(0u, 0u);
+      const uint2 r1 = k0 + 32u < cnt ? words[wb + k0 + 32u] : make_uint2(0u, 0u);
+      const uint2 r2 = k0 + 64u < cnt ? words[wb + k0 + 64u] : make_uint2(0u, 0u);
+      const uint2 r3 = k0 + 96u < cnt ? words[wb + k0 + 96u] : make_uint2(0u, 0u);
+      if (k0 < cnt) scatter(r0);
+      if (k0 + 32u < cnt) scatter(r1);
+      if (k0 + 64u < cnt) scatter(r2);
+      if (k0 + 96u < cnt) scatter(r3);
+      for (uint32_t k = k0 + 128u; k < cnt; k += 32) scatter(words[wb + k]);  // not reached: <= 128
     }
     __syncthreads();
     // minimum neighbour of every core column = first row (ascending) holding it:
     // OR per row block, exclusive prefix OR over blocks, then a second scan writes
     // each column exactly once
     uint32_t acc = 0;
-    for (int r = 0; r < RB; ++r) acc |= R[w * TILE + cblk * RB + r];
+    for (int r = 0; r < RB; ++r) acc |= R[w * DIAG_RS + cblk * RB + r];
     M[cblk * WPR + w] = acc;
     __syncthreads();
     uint32_t seen = 0;
     for (int q = 0; q < cblk; ++q) seen |= M[q * WPR + w];
     for (int r = 0; r < RB; ++r) {
       const int u = cblk * RB + r;
-      const uint32_t x = R[w * TILE + u];
+      const uint32_t x = R[w * DIAG_RS + u];
       uint32_t fresh = x & ~seen;
       seen |= x;
       while (fresh) {
@@ -407,13 +425,16 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
       }
       __syncthreads();  // wroots / slot_root are rewritten below
     }
-    // pointer jumping over the min-neighbour forest (9 halvings cover 512 nodes)
+    // pointer jumping over the min-neighbour forest, in place (a node may read a
+    // pointer another thread already advanced: every value is still an ancestor, so
+    // it only jumps further), until no pointer moves; forests are shallow, and 9
+    // synchronous halvings would cover 512 nodes
 #pragma unroll 1
-    for (int r = 0; r < 9; ++r) {
-      const int nv = lp[lp[tid]];
-      __syncthreads();
-      lp[tid] = nv;
-      __syncthreads();
+    for (int r = 0; r < TILE; ++r) {
+      const int cur = lp[tid];
+      const int nv = lp[cur];
+      if (nv != cur) lp[tid] = nv;
+      if (!__syncthreads_or(nv != cur)) break;
     }
     // merge the min-neighbour trees. Roots get slots in index order; with <= 32
     // trees every word ANDs its row's complement mask against the tree masks to
@@ -450,7 +471,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
       __syncthreads();
       for (int r = 0; r < RB; ++r) {
         const int u = cblk * RB + r;
-        const uint32_t um = R[w * TILE + u];
+        const uint32_t um = R[w * DIAG_RS + u];
         if (!um) continue;
         const int k = hist[lp[u]];
         const uint32_t cross = um & ~M[k * WPR + w];
@@ -481,7 +502,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     } else {
       for (int r = 0; r < RB; ++r) {
         const int u = cblk * RB + r;
-        uint32_t um = R[w * TILE + u];
+        uint32_t um = R[w * DIAG_RS + u];
         const int ru = lp[u];
         while (um) {
           const int t = __clz(um);
@@ -946,7 +967,7 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // round 1: one CTA per tile (wide, dense in shared memory); round 2: a warp per unit
-  const size_t diag_smem = (size_t)(WPR * TILE + 512) * 4 + (size_t)3 * TILE * 4;
+  const size_t diag_smem = (size_t)(WPR * DIAG_RS + 512) * 4 + (size_t)3 * TILE * 4;
   // kernel attributes and occupancy are per device (idempotent if raced)
   static std::atomic<int> links_per_sm_dev[DS_MAX_DEVICES] = {};
   int links_per_sm = dev < DS_MAX_DEVICES ? links_per_sm_dev[dev].load() : 0;
