@@ -467,7 +467,11 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     }
     __syncthreads();
     if (ntrees <= 32) {
-      if (is_core) atomicOr(&M[hist[lp[tid]] * WPR + (tid >> 5)], 0x80000000u >> (tid & 31));
+      {  // tree masks: one store per (tree, warp) group instead of 32-way smem atomics
+        const int key = is_core ? hist[lp[tid]] : -1;
+        const uint32_t grp = __match_any_sync(0xffffffffu, key);
+        if (is_core && (tid & 31) == __ffs(grp) - 1) M[key * WPR + (tid >> 5)] = __brev(grp);
+      }
       __syncthreads();
       for (int r = 0; r < RB; ++r) {
         const int u = cblk * RB + r;
@@ -485,10 +489,10 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
       if (tid < 32) {  // symmetric transitive closure of the tree graph (one warp)
         uint32_t row = adj[tid] | (1u << tid);
         uint32_t col = 0;
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < ntrees; ++j)  // lanes >= ntrees hold only their self bit
           if ((__shfl_sync(0xffffffffu, row, j) >> tid) & 1u) col |= 1u << j;
         row |= col;
-        for (int p = 0; p < 32; ++p) {
+        for (int p = 0; p < ntrees; ++p) {
           const uint32_t rp = __shfl_sync(0xffffffffu, row, p);
           if ((row >> p) & 1u) row |= rp;
         }
