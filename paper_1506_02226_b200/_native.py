@@ -185,6 +185,7 @@ class Context:
 
     def set_tile_cull(self, on: bool) -> None:
         """Bounding-box culling of provably empty tile pairs (default on; exact)."""
+        self._schedule = None
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_TILE_CULL, 1 if on else 0),
                   self.lib)
 
@@ -193,6 +194,7 @@ class Context:
 
     def set_spatial_sort(self, on: bool) -> None:
         """Visit points in Morton order (compact tiles; exact, default on)."""
+        self._schedule = None
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_SPATIAL_SORT, 1 if on else 0),
                   self.lib)
 
@@ -202,8 +204,15 @@ class Context:
                   self.lib)
 
     def configure(self, prune: bool = True, spatial_order: bool = True) -> None:
+        """Set both schedule options; a no-op when they are unchanged since the last call
+        (run_dbscan calls this every time)."""
+        state = (bool(prune), bool(spatial_order))
+        if getattr(self, "_schedule", None) == state:
+            return
+        self._schedule = None
         self.set_tile_cull(prune)
         self.set_spatial_sort(spatial_order)
+        self._schedule = state
 
     # -- entry points --------------------------------------------------------
     def run_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
@@ -351,17 +360,27 @@ def pin_frozen(arr: np.ndarray, owner) -> bool:
     return True
 
 
+_pin_torch = []  # [torch module or None], resolved on first use
+
+
 def pinned_empty(n: int, dtype=np.int64) -> np.ndarray:
     """Page-locked host array from torch's caching host allocator when available
     (device->host copies into it run at DMA speed); plain numpy otherwise."""
-    try:
-        import torch
-        if torch.cuda.is_available():
-            tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+    if not _pin_torch:
+        try:
+            import torch
+            _pin_torch.append(torch if torch.cuda.is_available() else None)
+        except Exception:
+            _pin_torch.append(None)
+    torch = _pin_torch[0]
+    dt = np.dtype(dtype)
+    if torch is not None and dt in (np.dtype(np.int64), np.dtype(np.int32)):
+        try:
+            tdt = torch.int64 if dt == np.dtype(np.int64) else torch.int32
             return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
-    except Exception:
-        pass
-    return np.empty(n, dtype=dtype)
+        except Exception:
+            pass
+    return np.empty(n, dtype=dt)
 
 
 _ctx_local = threading.local()
