@@ -255,6 +255,22 @@ def run_b200(args):
             tile_ms.append(last[0])
     torch.cuda.synchronize()
     ms = statistics.mean(times)
+    # the roofline's kernel time by CUDA events recorded around the eps-tile kernel on
+    # its launching stream (a separate leg: events between kernels cost device time,
+    # so the timed steps above take the stage split from the kernels' stamps)
+    tile_ms_stamps = list(tile_ms)
+    if world == 1:
+        ctx.set_event_timing(True)
+        try:
+            for _ in range(args.warmup):
+                step()
+            tile_ms = []
+            for _ in range(args.steps):
+                flush.zero_()
+                tile_ms.append(step()[0])
+            torch.cuda.synchronize()
+        finally:
+            ctx.set_event_timing(False)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -350,7 +366,9 @@ def run_b200(args):
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz "
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
                      "ops_per_pair": ops, "pairs_per_launch": pairs,
-                     "tile_ms": statistics.mean(tile_ms)},
+                     "tile_ms": statistics.mean(tile_ms),
+                     "tile_ms_stamps": statistics.mean(tile_ms_stamps),
+                     "tile_timing": "CUDA events around the kernel (DS_OPT_EVENT_TIMING leg)"},
         "dense_schedule": (None if dense is None else {
             "what": "prune=False, spatial_order=False: all 512x512 upper-triangle tile pairs",
             "tile_ms": dense["tile_ms"], "pairs_per_launch": dense["pairs_per_launch"],

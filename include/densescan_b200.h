@@ -54,8 +54,11 @@ typedef enum {
 } ds_formula;
 
 /* Per-call measurements; mirrors StageTimings (pipeline.py:52-67) plus the
- * counters the benchmark needs. All times are device (CUDA event) times
- * except total_ms, which covers the whole call including copies. */
+ * counters the benchmark needs. All times are device times except total_ms, which
+ * covers the whole call including copies: copies by CUDA events; fused_ms, tile_ms
+ * and merge_ms of ds_run_dbscan[_device] by %globaltimer stamps at the kernel
+ * boundaries (CUDA events with DS_OPT_EVENT_TIMING), of the other entry points by
+ * CUDA events. */
 typedef struct {
   double fused_ms;          /* stage 1+2: prep + eps-tile kernel (+ core flags)      */
   double merge_ms;          /* stage 3: union-find, borders, canonical labels        */
@@ -102,8 +105,12 @@ void ds_ctx_destroy(ds_ctx* ctx);
  * coordinates so tiles are compact (more tile pairs culled); index-dependent
  * rules still use original indices, results are bit-identical with 0.
  * DS_OPT_CUDA_GRAPH (default 1): record the device pipeline into a CUDA graph
- * on the second call with an identical shape/buffers/options and replay it. */
-enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3 };
+ * on the second call with an identical shape/buffers/options and replay it.
+ * DS_OPT_EVENT_TIMING (default 0): time stage 1+2, the eps-tile kernel and stage 3
+ * of ds_run_dbscan / ds_run_dbscan_device with CUDA events recorded between the
+ * kernels; 0 takes them from %globaltimer stamps the kernels write (events between
+ * kernels cost device time: they break the programmatic overlap of the launches). */
+enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3, DS_OPT_EVENT_TIMING = 4 };
 ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
 int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
 

@@ -20,7 +20,7 @@ LIB_NAME = "libdensescan_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
-DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT, DS_OPT_CUDA_GRAPH = 1, 2, 3
+DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT, DS_OPT_CUDA_GRAPH, DS_OPT_EVENT_TIMING = 1, 2, 3, 4
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
@@ -196,6 +196,12 @@ class Context:
         """Visit points in Morton order (compact tiles; exact, default on)."""
         self._schedule = None
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_SPATIAL_SORT, 1 if on else 0),
+                  self.lib)
+
+    def set_event_timing(self, on: bool) -> None:
+        """Stage timings from CUDA events between the kernels (default off: from the
+        kernels' %globaltimer stamps; events cost device time)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_EVENT_TIMING, 1 if on else 0),
                   self.lib)
 
     def set_cuda_graph(self, on: bool) -> None:

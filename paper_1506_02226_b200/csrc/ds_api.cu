@@ -58,6 +58,8 @@ struct Scalars {
   int32_t kept32;
   uint32_t unsafe_flag;
   int32_t nclusters;
+  unsigned int label_blocks;                // label_kernel blocks finished
+  unsigned long long stamps[ST_COUNT];      // device stage boundaries (Stamp)
 };
 
 // The per-call zero region: one memset clears the scalars, the spatial-sort bounding
@@ -88,7 +90,9 @@ struct ds_ctx {
   unsigned long long gkey[12] = {};
   unsigned long long seen_key[12] = {};
   bool capturing = false;  // events become external graph nodes while recording
+  bool stamp_timing = false;  // stage timings from device stamps: no events inside
   int sort = 1;          // DS_OPT_SPATIAL_SORT
+  int event_timing = 0;  // DS_OPT_EVENT_TIMING
   bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
   unsigned long long units_cap = 0;  // culled unit list capacity (units)
@@ -314,8 +318,8 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, zr_bytes(n), s));  // the zero region (cnt: prep)
   const bool do_sort = c->sort && T > 1;
   unsigned int* bbox = (unsigned int*)((char*)c->scalars.p + zr_bbox());
-  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, do_sort ? bbox : nullptr,
-                    (int32_t*)c->cnt.p, s));
+  DS_CK(launch_prep(d_coords, n, d, (float*)c->rec.p, &sc->unsafe_flag, sc->stamps,
+                    do_sort ? bbox : nullptr, (int32_t*)c->cnt.p, s));
   const float* rec = (const float*)c->rec.p;
   c->sorted = false;
   const int dp = padded_dim(d);
@@ -374,6 +378,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.unsafe_flag = &sc->unsafe_flag;
   a.pairs_done = &sc->pairs_done;
   a.work_ctr = &sc->work_ctr;
+  a.stamps = sc->stamps;
   a.unit_list = nullptr;
   if (pl.cull) {
     if (!bnd.lo && dp <= 4) DS_CK(launch_block_bounds(rec, n, d, (float*)c->blk.p, s));
@@ -390,9 +395,11 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   a.uchunks = (uint2*)c->uchunks.p;
   c->units = a;
   c->unit_lb = lane_blocks(d);
-  DS_CK(record(c, c->ev[1], s));
+  // an event record between two kernels breaks their programmatic overlap (a few us
+  // of device time each): with stamp timing the tile kernel is timed by its stamps
+  if (!c->stamp_timing) DS_CK(record(c, c->ev[1], s));
   DS_CK(launch_units_kernel(a, d, formula, c->sm_count, s));
-  DS_CK(record(c, c->ev[2], s));
+  if (!c->stamp_timing) DS_CK(record(c, c->ev[2], s));
   if (want_dir)
     DS_CK(launch_unit_dir(a, d, pl.all_items, pl.cull ? (const uint2*)c->ucnt.p : nullptr,
                           &sc->kept, (uint4*)c->chunks.p, &sc->nonempty_count, s));
@@ -479,6 +486,11 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
                          int64_t* d_counts64, cudaStream_t s, Plan& pl, bool captured,
                          const HostIO* io) {
   c->capturing = captured;
+  c->stamp_timing = !c->event_timing;
+  struct Reset {
+    ds_ctx* c;
+    ~Reset() { c->stamp_timing = false; }
+  } reset{c};
   auto rec = [&](cudaEvent_t e) { return record(c, e, s); };
   if (io && io->coords) {
     DS_CK(rec(c->ev[5]));
@@ -489,7 +501,9 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   if (st != DS_OK) return st;
   MergeWs w = merge_ws(c, n);
   w.scan_zeroed = true;
-  DS_CK(rec(c->ev[3]));
+  w.stamps = ((Scalars*)c->scalars.p)->stamps;
+  w.label_blocks = &((Scalars*)c->scalars.p)->label_blocks;
+  if (c->event_timing) DS_CK(rec(c->ev[3]));
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
@@ -541,7 +555,8 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     std::memcpy(&eps_bits, &eps_sq, 8);
     key[0] = (unsigned long long)n;
     key[1] = (unsigned long long)d | ((unsigned long long)formula << 8) |
-             ((unsigned long long)c->cull << 16) | ((unsigned long long)c->sort << 17) | 1ull << 40;
+             ((unsigned long long)c->cull << 16) | ((unsigned long long)c->sort << 17) |
+             ((unsigned long long)c->event_timing << 18) | 1ull << 40;
     key[2] = eps_bits;
     key[3] = (unsigned long long)min_pts;
     key[4] = (unsigned long long)(uintptr_t)d_coords;
@@ -643,9 +658,21 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
   }
   if (t) {
     float f = 0, m = 0, k = 0, o = 0;
-    DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
-    DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
-    DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    // stage 1+2 / tile / stage 3 from the device stamps (copied back with the
+    // scalars); events only if a stamp is missing or out of order
+    const unsigned long long* st = c->h_scalars->stamps;
+    if (c->event_timing) {
+      DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[3]));
+      DS_CK(cudaEventElapsedTime(&m, c->ev[3], c->ev[4]));
+      DS_CK(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+    } else if (st[ST_PREP] && st[ST_PREP] <= st[ST_TILE] && st[ST_TILE] <= st[ST_MERGE] &&
+               st[ST_MERGE] <= st[ST_LABELS_DONE]) {
+      f = (float)((st[ST_MERGE] - st[ST_PREP]) * 1e-6);
+      k = (float)((st[ST_MERGE] - st[ST_TILE]) * 1e-6);
+      m = (float)((st[ST_LABELS_DONE] - st[ST_MERGE]) * 1e-6);
+    } else {  // no split available: the whole device part as stage 1+2
+      DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[4]));
+    }
     DS_CK(cudaEventElapsedTime(&o, c->ev[4], c->ev[7]));
     t->fused_ms = f;
     t->merge_ms = m;
@@ -861,6 +888,10 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
     c->use_graph = value ? 1 : 0;
     return DS_OK;
   }
+  if (option == DS_OPT_EVENT_TIMING) {
+    c->event_timing = value ? 1 : 0;
+    return DS_OK;
+  }
   set_error("option: unknown option id");
   return DS_EINVAL;
 }
@@ -869,6 +900,7 @@ int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   if (c && option == DS_OPT_TILE_CULL) return c->cull;
   if (c && option == DS_OPT_SPATIAL_SORT) return c->sort;
   if (c && option == DS_OPT_CUDA_GRAPH) return c->use_graph;
+  if (c && option == DS_OPT_EVENT_TIMING) return c->event_timing;
   return -1;
 }
 
@@ -1038,7 +1070,7 @@ ds_status ladder_prep(ds_ctx* c, const double* coords, int64_t n, int32_t d) {
   DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
   DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
   DS_CK(launch_prep((const double*)c->coords64.p, n, d, (float*)c->rec.p,
-                    &((Scalars*)c->scalars.p)->unsafe_flag, nullptr, nullptr, s));
+                    &((Scalars*)c->scalars.p)->unsafe_flag, nullptr, nullptr, nullptr, s));
   return DS_OK;
 }
 

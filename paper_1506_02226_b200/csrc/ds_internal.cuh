@@ -82,7 +82,14 @@ struct UnitArgs {
   const uint32_t* unsafe_flag;
   unsigned long long* pairs_done;       // ordered pairs evaluated (32 x 32*KP per unit)
   unsigned long long* work_ctr;         // batch counter (zeroed before the launch)
+  unsigned long long* stamps = nullptr; // %globaltimer stamps (Stamp), or nullptr
 };
+
+// Device-side stage boundaries of one call, in %globaltimer ns, written by thread 0 of
+// block 0 after its griddep_wait (i.e. once the preceding kernel has completed):
+// the host turns them into the stage timings without cudaEventElapsedTime calls
+// (about 3 us of host time each, on the critical path of every call).
+enum Stamp { ST_PREP = 0, ST_TILE = 1, ST_MERGE = 2, ST_LABELS_DONE = 3, ST_COUNT = 4 };
 
 // ---- programmatic dependent launch ------------------------------------------------
 // Pipeline kernels are launched with programmatic stream serialization: a kernel may
@@ -91,6 +98,13 @@ struct UnitArgs {
 // griddep_wait() first, which returns once the predecessor grid has completed and
 // its memory is visible (a no-op for an ordinary launch).
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void stamp(unsigned long long* st, int k) {
+  if (st && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    st[k] = t;
+  }
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -149,6 +163,7 @@ __device__ __forceinline__ unsigned int ord_bits(float f) {
 // bbox words must be zero on entry (lo is stored as ~ord_bits, hi as ord_bits, so
 // both reduce with atomicMax); cnt (nullable): zeroed here for stage 1's counts
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
+                        unsigned long long* stamps,
                         unsigned int* bbox, int32_t* cnt, cudaStream_t s);
 cudaError_t launch_units_kernel(const UnitArgs& a, int d, int formula, int sm_count,
                                 cudaStream_t s);
@@ -210,6 +225,8 @@ struct MergeWs {
   unsigned long long* ncore;
   const int32_t* perm = nullptr;  // sorted -> original index (nullptr: identity)
   const int32_t* inv = nullptr;   // original -> sorted index
+  unsigned long long* stamps = nullptr;  // Stamp slots (ST_LABELS_DONE), or nullptr
+  unsigned int* label_blocks = nullptr;  // finished label_kernel blocks (zeroed per call)
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);

@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(512) union_diag_kernel(
     const uint32_t* __restrict__ corew_in, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm) {
   griddep_wait();
+  stamp(A.stamps, ST_MERGE);  // stage 1+2 complete
   constexpr int THREADS = 512;
   constexpr int RB = TILE / (THREADS / WPR);  // rows per block: 16
   extern __shared__ uint32_t dsm[];
@@ -886,12 +887,22 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* d
 
 __global__ void label_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
                              const int32_t* __restrict__ id, int64_t n,
-                             const int32_t* __restrict__ perm, int64_t* __restrict__ labels) {
+                             const int32_t* __restrict__ perm, int64_t* __restrict__ labels,
+                             unsigned long long* stamps, unsigned int* done) {
   griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int r = root[i];
-  labels[perm ? perm[i] : i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
+  if (i < n) {
+    const int r = root[i];
+    labels[perm ? perm[i] : i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
+  }
+  if (stamps) {  // the last block to finish stamps the end of stage 3
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      stamps[ST_LABELS_DONE] = t;
+    }
+  }
 }
 
 __global__ void counts_i64_kernel(const int32_t* __restrict__ cnt, int64_t n,
@@ -1024,7 +1035,8 @@ cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
                  reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters);
   if (e != cudaSuccess) return e;
   return launch_pdl(label_kernel, dim3(b), dim3(t), 0, s, (const int32_t*)w.root,
-                    (const int32_t*)w.cmin, (const int32_t*)w.flag, w.n, w.perm, labels);
+                    (const int32_t*)w.cmin, (const int32_t*)w.flag, w.n, w.perm, labels,
+                    w.stamps, w.label_blocks);
 }
 
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R,

@@ -580,6 +580,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 template <int D, int F>
 __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel(const UnitArgs A) {
   griddep_wait();
+  stamp(A.stamps, ST_TILE);
   if (*A.unsafe_flag != 0) eps_unit_body<D, F, false>(A);
   else eps_unit_body<D, F, true>(A);
 }
@@ -798,9 +799,11 @@ __global__ void unit_dir_kernel(const UnitArgs A, int64_t all_items, const uint2
 __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ coords, int64_t n,
                                                    int d, int dpad, int S, float* __restrict__ rec,
                                                    uint32_t* unsafe_flag,
+                                                   unsigned long long* stamps,
                                                    unsigned int* __restrict__ bbox,
                                                    int32_t* __restrict__ cnt) {
   griddep_wait();
+  stamp(stamps, ST_PREP);
   float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
@@ -1098,7 +1101,8 @@ cudaError_t launch_d(const UnitArgs& a, int formula, int sm_count, cudaStream_t 
 int padded_dim(int d) { return pad_dim(d); }
 
 cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint32_t* unsafe_flag,
-                        unsigned int* bbox, int32_t* cnt, cudaStream_t s) {
+                        unsigned long long* stamps, unsigned int* bbox, int32_t* cnt,
+                        cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int threads = 256;
@@ -1106,7 +1110,7 @@ cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   return launch_pdl(prep_kernel, dim3((unsigned)blocks), dim3(threads), 0, s, coords, n, d, dp, S,
-                    rec, unsafe_flag, bbox, cnt);
+                    rec, unsafe_flag, stamps, bbox, cnt);
 }
 
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,

@@ -435,3 +435,24 @@ def test_degenerate_inputs_against_oracle(ds, rng):
                     ctx.configure(True, True)
                 assert np.array_equal(counts, wc), (name, fname, prune)
                 assert np.array_equal(labels, want), (name, fname, prune)
+
+
+def test_stage_timings_stamps_and_events(ds):
+    """Stage times come from the kernels' %globaltimer stamps by default and from CUDA
+    events with DS_OPT_EVENT_TIMING; both are positive, nested (tile <= stage 1+2) and
+    leave the labels unchanged."""
+    pts = ds.generate_blobs(30_000, 6, 0.4, 0.1, 9, 2)
+    params = ds.validate_params(0.1, 5)
+    ctx = ds._native.context()
+    out = {}
+    for ev in (False, True):
+        ctx.set_event_timing(ev)
+        try:
+            for _ in range(3):  # eager, recorded, replayed
+                labels, _, t = ctx.run_dbscan(pts.coords_aos, params.eps_sq, 5, 1, 0)
+                assert 0 < t.tile_ms <= t.fused_ms and t.merge_ms > 0 and t.d2h_ms > 0
+                assert t.fused_ms + t.merge_ms < t.total_ms
+        finally:
+            ctx.set_event_timing(False)
+        out[ev] = labels.copy()
+    assert np.array_equal(out[False], out[True])
