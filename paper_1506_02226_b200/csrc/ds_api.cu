@@ -470,6 +470,8 @@ struct HostIO {
   size_t in_bytes = 0;
   int64_t* labels = nullptr;
   int64_t* counts = nullptr;
+  bool time_h2d = false;  // ev5 -> ev0 brackets the caller's coordinate copy
+  float h2d_ms = 0.f;     // measured while the rest of the pipeline runs
 };
 
 bool host_pinned(const void* p) {
@@ -542,7 +544,7 @@ cudaGraphNode_t find_copy_node(cudaGraph_t g, const void* host) {
 // cost); an adjacency-word overflow invalidates the graph.
 ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double eps_sq,
                    int64_t min_pts, int formula, int64_t mem_cap, int64_t* d_labels,
-                   int64_t* d_counts64, cudaStream_t s, ds_timings* t, const HostIO* io = nullptr) {
+                   int64_t* d_counts64, cudaStream_t s, ds_timings* t, HostIO* io = nullptr) {
   Plan pl;
   // host copies are recorded into the graph (and re-pointed per launch) when every
   // host buffer is page-locked; pageable buffers run the pipeline eagerly
@@ -641,6 +643,10 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       key[8] = g_alloc_generation.load();
       key[11] = c->units_cap;
       std::memcpy(c->seen_key, key, sizeof key);
+    }
+    if (io && io->time_h2d) {  // the copy is done long before the pipeline: time it meanwhile
+      DS_CK(cudaEventSynchronize(c->ev[0]));
+      DS_CK(cudaEventElapsedTime(&io->h2d_ms, c->ev[5], c->ev[0]));
     }
     DS_CK(cudaStreamSynchronize(s));
     bool retry = false;
@@ -795,13 +801,12 @@ ds_status ds_run_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, d
   HostIO io;
   io.labels = labels_out;
   io.counts = counts_out;
+  io.time_h2d = true;
   st = pipeline(c, (const double*)c->coords64.p, n, d, eps_sq, min_pts, formula, mem_cap,
                 (int64_t*)c->labels.p, counts_out ? (int64_t*)c->counts64.p : nullptr, s, &local,
                 &io);
   if (st != DS_OK) return st;
-  float h2d = 0;
-  DS_CK(cudaEventElapsedTime(&h2d, c->ev[5], c->ev[0]));
-  local.h2d_ms = h2d;
+  local.h2d_ms = io.h2d_ms;
   local.total_ms = now_ms() - t0;
   if (t) *t = local;
   return DS_OK;
