@@ -69,7 +69,14 @@ inline size_t zr_round(size_t b) { return (b + ZR_ALIGN - 1) / ZR_ALIGN * ZR_ALI
 inline size_t zr_bbox() { return zr_round(sizeof(Scalars)); }
 inline size_t zr_diag() { return zr_bbox() + ZR_ALIGN; }
 inline size_t zr_scan(int64_t n) { return zr_diag() + zr_round((size_t)n_tiles(n) * 8); }
-inline size_t zr_bytes(int64_t n) { return zr_scan(n) + (size_t)scan_partials_len(n) * 4; }
+// the tile-root link table of union_links (one CAS slot per linked pair of tile roots)
+inline int link_tab_bits(int64_t n) {
+  int b = 8;
+  while (b < 14 && ((int64_t)1 << b) < 4 * n_tiles(n)) ++b;
+  return b;
+}
+inline size_t zr_links(int64_t n) { return zr_round(zr_scan(n) + (size_t)scan_partials_len(n) * 4); }
+inline size_t zr_bytes(int64_t n) { return zr_links(n) + ((size_t)8 << link_tab_bits(n)); }
 
 }  // namespace
 
@@ -78,6 +85,7 @@ struct ds_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
+  Buf troot;  // per-tile uniform roots of the diagonal union pass (single GPU)
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
       keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits;
@@ -129,7 +137,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                       &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                      &c->dist, &c->dbits};
+                      &c->dist, &c->dbits, &c->troot};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -228,6 +236,7 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->core, N));
   DS_CK(ensure(c->corew, ((N + 31) / 32) * 4));
   DS_CK(ensure(c->parent, N * 4));
+  DS_CK(ensure(c->troot, (size_t)n_tiles(n) * 4));
   DS_CK(ensure(c->bmin, N * 4));
   DS_CK(ensure(c->cmin, N * 4));
   DS_CK(ensure(c->root, N * 4));
@@ -505,6 +514,9 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   w.scan_zeroed = true;
   w.stamps = ((Scalars*)c->scalars.p)->stamps;
   w.label_blocks = &((Scalars*)c->scalars.p)->label_blocks;
+  w.tile_root = (int32_t*)c->troot.p;
+  w.link_tab = (unsigned long long*)((char*)c->scalars.p + zr_links(n));
+  w.link_mask = (1u << link_tab_bits(n)) - 1u;
   if (c->event_timing) DS_CK(rec(c->ev[3]));
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
@@ -746,7 +758,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                 &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                &c->dist, &c->dbits};
+                &c->dist, &c->dbits, &c->troot};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)

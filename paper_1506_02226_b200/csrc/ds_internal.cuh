@@ -227,6 +227,10 @@ struct MergeWs {
   const int32_t* inv = nullptr;   // original -> sorted index
   unsigned long long* stamps = nullptr;  // Stamp slots (ST_LABELS_DONE), or nullptr
   unsigned int* label_blocks = nullptr;  // finished label_kernel blocks (zeroed per call)
+  int32_t* tile_root = nullptr;  // per tile: the root all its core points share after the
+                                 // diagonal pass, or -1 (single GPU only; nullptr: unused)
+  unsigned long long* link_tab = nullptr;  // zeroed per call: tile-root pairs already linked
+  unsigned int link_mask = 0;              // slots - 1 (a power of two)
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);

@@ -9,7 +9,7 @@ cp $L /tmp/ab_keep.so
 for r in 1 2; do
   for v in $VARS; do
     cp $v $L
-    python tools/run_configs.py --configs $CFG --reps 7 2>/dev/null | python -c "
+    python tools/run_configs.py --configs $CFG --reps ${REPS:-7} 2>/dev/null | python -c "
 import sys, json
 for l in sys.stdin:
     d = json.loads(l)
