@@ -257,7 +257,7 @@ __device__ __forceinline__ int min_orig(const int32_t* perm, int jb0, uint32_t b
 // TILE made them 16-way conflicts)
 constexpr int DIAG_RS = TILE + 1;
 
-__global__ void __launch_bounds__(512) union_diag_kernel(
+__global__ void __launch_bounds__(512, 4) union_diag_kernel(
     const UnitArgs A, int LB, const uint2* __restrict__ diag_range, const CoreInit ci,
     const uint32_t* __restrict__ corew_in, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm, int32_t* __restrict__ tile_root) {

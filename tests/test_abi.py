@@ -101,3 +101,19 @@ def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
     k2 = [f for f in tile if "eps_unit_kernelILi2ELi1EE" in f.split("\n")[0]]
     assert k2 and "FMUL2" in k2[0] and "FADD2" in k2[0]
     assert "LDGSTS" in k2[0]
+
+
+@pytest.mark.skipif(not shutil.which("cuobjdump"), reason="cuobjdump not available")
+def test_stage3_kernels_register_budget(lib):
+    """The stage-3 union kernels are latency-bound and need their occupancy: union_diag
+    (512 threads) four CTAs per SM, i.e. <= 32 registers (ptxas otherwise picked 64
+    and the kernel ran 40 % slower), union_links (256 threads) five, <= 48."""
+    out = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True,
+                         check=True).stdout
+    regs = {}
+    for name, body in re.findall(r"Function (\S+):\n\s*(REG:\d+)", out):
+        regs[name] = int(body.split(":")[1])
+    diag = [r for k, r in regs.items() if "union_diag_kernel" in k]
+    links = [r for k, r in regs.items() if "union_links_kernel" in k]
+    assert diag and max(diag) <= 32, diag
+    assert links and max(links) <= 48, links
