@@ -85,7 +85,7 @@ struct ds_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
-  Buf troot;  // per-tile uniform roots of the diagonal union pass (single GPU)
+  Buf troot;  // per-block uniform roots of the diagonal union pass (single GPU)
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
       keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits;
@@ -236,7 +236,7 @@ ds_status alloc_common(ds_ctx* c, int64_t n, int d) {
   DS_CK(ensure(c->core, N));
   DS_CK(ensure(c->corew, ((N + 31) / 32) * 4));
   DS_CK(ensure(c->parent, N * 4));
-  DS_CK(ensure(c->troot, (size_t)n_tiles(n) * 4));
+  DS_CK(ensure(c->troot, (size_t)((n + 31) / 32) * 4));
   DS_CK(ensure(c->bmin, N * 4));
   DS_CK(ensure(c->cmin, N * 4));
   DS_CK(ensure(c->root, N * 4));
@@ -514,7 +514,7 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   w.scan_zeroed = true;
   w.stamps = ((Scalars*)c->scalars.p)->stamps;
   w.label_blocks = &((Scalars*)c->scalars.p)->label_blocks;
-  w.tile_root = (int32_t*)c->troot.p;
+  w.blk_root = (int32_t*)c->troot.p;
   w.link_tab = (unsigned long long*)((char*)c->scalars.p + zr_links(n));
   w.link_mask = (1u << link_tab_bits(n)) - 1u;
   if (c->event_timing) DS_CK(rec(c->ev[3]));

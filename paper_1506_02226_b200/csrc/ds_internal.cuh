@@ -227,8 +227,8 @@ struct MergeWs {
   const int32_t* inv = nullptr;   // original -> sorted index
   unsigned long long* stamps = nullptr;  // Stamp slots (ST_LABELS_DONE), or nullptr
   unsigned int* label_blocks = nullptr;  // finished label_kernel blocks (zeroed per call)
-  int32_t* tile_root = nullptr;  // per tile: the root all its core points share after the
-                                 // diagonal pass, or -1 (single GPU only; nullptr: unused)
+  int32_t* blk_root = nullptr;  // per 32-point block: the root all its core points share
+                                // after the diagonal pass, or -1 (single GPU; nullptr: unused)
   unsigned long long* link_tab = nullptr;  // zeroed per call: tile-root pairs already linked
   unsigned int link_mask = 0;              // slots - 1 (a power of two)
 };

@@ -260,7 +260,7 @@ constexpr int DIAG_RS = TILE + 1;
 __global__ void __launch_bounds__(512, 4) union_diag_kernel(
     const UnitArgs A, int LB, const uint2* __restrict__ diag_range, const CoreInit ci,
     const uint32_t* __restrict__ corew_in, int32_t* parent, int32_t* bmin,
-    const int32_t* __restrict__ perm, int32_t* __restrict__ tile_root) {
+    const int32_t* __restrict__ perm, int32_t* __restrict__ blk_root) {
   griddep_wait();
   stamp(A.stamps, ST_MERGE);  // stage 1+2 complete
   constexpr int THREADS = 512;
@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       u_hi = (q + 1) * LB < r_hi ? (q + 1) * LB : r_hi;
     }
     if (u_lo >= u_hi) {  // no words on this launch: only the core init (uniform per CTA)
-      if (tile_root && tid == 0) tile_root[tile] = -1;
+      if (blk_root && (tid & 31) == 0 && (int64_t)tile * WPR + (tid >> 5) < nw)
+        blk_root[(int64_t)tile * WPR + (tid >> 5)] = -1;
       __syncthreads();
       continue;
     }
@@ -417,7 +418,11 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
 #pragma unroll
       for (int q = 0; q < THREADS / 32; ++q) nroots += wroots[q];
       if (nroots <= 1) {  // uniform per CTA
-        if (tile_root && tid == 0) tile_root[tile] = nroots == 1 ? base + slot_root[0] : -1;
+        if (blk_root) {  // every core point of the tile has the root slot_root[0]
+          const uint32_t cores = __ballot_sync(0xffffffffu, core0 && (int64_t)base + tid < n);
+          const int64_t gw = (int64_t)tile * WPR + (tid >> 5);
+          if ((tid & 31) == 0 && gw < nw) blk_root[gw] = cores ? base + slot_root[0] : -1;
+        }
         const int64_t g = (int64_t)base + tid;
         if (g < n) {
           if (nroots == 1 && core0 && tid != slot_root[0]) parent[g] = base + slot_root[0];
@@ -506,11 +511,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
         const int kmin = __ffs(adj[hist[lp[tid]]]) - 1;
         lp[tid] = slot_root[kmin];
       }
-      // one component (slot 0 reaches every tree): the tile's core points share a root
-      if (tile_root && tid == 0)
-        tile_root[tile] = __popc(adj[0]) == ntrees ? base + slot_root[0] : -1;
     } else {
-      if (tile_root && tid == 0) tile_root[tile] = -1;
       for (int r = 0; r < RB; ++r) {
         const int u = cblk * RB + r;
         uint32_t um = R[w * DIAG_RS + u];
@@ -527,10 +528,22 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
     {
       const int v = tid;
       const int64_t g = (int64_t)base + v;
+      int r = -1;
       if (g < n) {
-        const int r = find_local(lp, v);
+        r = find_local(lp, v);
         if (r != v) parent[g] = base + r;  // r < v: parent[x] <= x holds
         if (lb[v] != NONE) atomicMin(&bmin[g], lb[v]);
+      }
+      if (blk_root) {  // the 32-point block's common root, if all its core points share one
+        const bool cv = g < n && ((lcw[tid >> 5] >> (31 - (tid & 31))) & 1u);
+        const uint32_t cores = __ballot_sync(0xffffffffu, cv);
+        const uint32_t grp = __match_any_sync(0xffffffffu, cv ? r : -1);
+        const int first = cores ? __ffs(cores) - 1 : 0;
+        const uint32_t grp0 = __shfl_sync(0xffffffffu, grp, first);
+        const int r0 = __shfl_sync(0xffffffffu, r, first);
+        const int64_t gw = (int64_t)tile * WPR + (tid >> 5);
+        if ((tid & 31) == 0 && gw < nw)
+          blk_root[gw] = (cores && (cores & ~grp0) == 0u) ? base + r0 : -1;
       }
     }
     __syncthreads();
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
 constexpr int LINK_WARPS = 8;
 __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
     const UnitArgs A, int LB, const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
-    const int32_t* __restrict__ perm, const int32_t* __restrict__ tile_root,
+    const int32_t* __restrict__ perm, const int32_t* __restrict__ blk_root,
     unsigned long long* link_tab, unsigned int link_mask) {
   griddep_wait();
   __shared__ int rows_sh[LINK_WARPS][TILE / WPR * 4];  // up to 128 rows per lane block
@@ -571,7 +584,7 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
   // the uniform-tile shortcut (below) pays when warps walk several units each (it
   // saves per-unit load latency); with about one unit per warp (small inputs, e.g.
   // C1) its burst of simultaneous links is slower than the full path
-  const bool uniform_ok = tile_root && (r_hi - r_lo) > 2 * nw;
+  const bool uniform_ok = blk_root && (r_hi - r_lo) > 2 * nw;
   // loads are issued a step ahead where the data does not depend on them: the next
   // unit's list entry and chunk entries during the current unit, and per column block
   // the core word, the 32 parents and the first 32 words together
@@ -606,39 +619,42 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
     const bool ok = cnt != 0u && base + cnt <= A.words_cap;  // overflowed run: the host re-runs
     uint32_t todo = __ballot_sync(0xffffffffu, ok);
     if (!todo) continue;
-    // Both tiles uniform (union_diag: all core points of the tile share one root) and
-    // every row of the lane block and every column of its column blocks core: every
-    // word is a core-core word and no border candidates exist, so the unit is exactly
-    // one link of the two tile roots — no parents or words need to be read.
+    // Uniform blocks (union_diag: all core points of a 32-point block share one root):
+    // when the lane block's row blocks share one root, every column block has a root,
+    // and every row and column is core, every word is a core-core word and no border
+    // candidates exist — the unit is exactly the links of the row root with the column
+    // roots, made without reading parents or words.
     if (uniform_ok) {
-      // the two tile roots and the core words are loaded together (one round trip)
-      const int ta = tile_root[a], tb = tile_root[b];
-      uint32_t w = 0xffffffffu, vm = 0xffffffffu;
-      const int rw = (a * TILE + lb * KPL) >> 5;  // first core word of the lane block
-      if (lane < KPL / 32) {
-        const int g0 = (rw + lane) * 32;
-        w = g0 < n ? corew[rw + lane] : 0u;
-        vm = n - g0 >= 32 ? 0xffffffffu : (g0 < n ? ~(0xffffffffu >> (n - g0)) : 0u);
-      } else if (lane >= 32 - WPR && ((todo >> (lane - (32 - WPR))) & 1u)) {
-        const int g0 = b * TILE + (lane - (32 - WPR)) * 32;  // column block lane - 16
-        w = corew[g0 >> 5];
+      // core words and block roots of the row blocks (lanes 0..) and of the column
+      // blocks (lanes 16 + jw), loaded together: one round trip
+      const int rw = (a * TILE + lb * KPL) >> 5;  // first row block
+      const bool rl = lane < KPL / 32 && (rw + lane) * 32 < n;
+      const bool cl = lane >= 32 - WPR && ((todo >> (lane - (32 - WPR))) & 1u);
+      const int gw = rl ? rw + lane : (cl ? ((b * TILE) >> 5) + lane - (32 - WPR) : -1);
+      uint32_t w = 0u, vm = 0u;
+      int br = -1;
+      if (gw >= 0) {
+        const int g0 = gw * 32;
+        w = corew[gw];
+        br = blk_root[gw];
         vm = n - g0 >= 32 ? 0xffffffffu : ~(0xffffffffu >> (n - g0));
       }
-      if (ta >= 0 && tb >= 0) {
-        if (__all_sync(0xffffffffu, w == vm)) {
-          // many units of a tile pair arrive here at once: the first to claim the
-          // pair's slot links it, the rest skip (a slot taken by another pair: link)
-          if (lane == 0 && ta != tb && !(ta == last_a && tb == last_b)) {
-            const unsigned long long key = ((unsigned long long)(unsigned)ta << 32 | (unsigned)tb) + 1ull;
-            const unsigned slot = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & link_mask;
-            unsigned long long old = link_tab[slot];
-            if (old == 0ull) old = atomicCAS(&link_tab[slot], 0ull, key);
-            if (old != key) link_root(parent, find_plain(parent, ta), tb);
-            last_a = ta;
-            last_b = tb;
-          }
-          continue;
+      const int urow = __shfl_sync(0xffffffffu, br, 0);  // lane 0 holds a row block
+      if (__all_sync(0xffffffffu, w == vm && (!rl || br == urow) && (!cl || br >= 0)) && urow >= 0) {
+        // one link per distinct column root; many units of a block pair arrive here at
+        // once: the first to claim the pair's slot links it, the rest skip (a slot
+        // taken by another pair: link anyway)
+        const unsigned grp = __match_any_sync(0xffffffffu, cl ? br : -1);
+        if (cl && lane == __ffs(grp) - 1 && br != urow && !(urow == last_a && br == last_b)) {
+          const unsigned long long key = ((unsigned long long)(unsigned)urow << 32 | (unsigned)br) + 1ull;
+          const unsigned slot = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & link_mask;
+          unsigned long long old = link_tab[slot];
+          if (old == 0ull) old = atomicCAS(&link_tab[slot], 0ull, key);
+          if (old != key) link_root(parent, find_plain(parent, urow), br);
+          last_a = urow;
+          last_b = br;
         }
+        continue;
       }
     }
     // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not core)
@@ -1045,12 +1061,12 @@ cudaError_t launch_union_chunks(const MergeWs& w, const UnitArgs& units, int lan
   const int64_t grid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
   cudaError_t e = launch_pdl(union_diag_kernel, dim3((unsigned)grid), dim3(512), diag_smem, s, units,
                              lane_blocks, diag_range, ci, (const uint32_t*)w.corew, w.parent,
-                             w.bmin, w.perm, w.tile_root);
+                             w.bmin, w.perm, w.blk_root);
   if (e != cudaSuccess) return e;
   // one resident wave of union_links: warps take units grid-stride
   return launch_pdl(union_links_kernel, dim3(sms * links_per_sm), dim3(LINK_WARPS * 32), 0, s, units,
                     lane_blocks, (const uint32_t*)w.corew, w.parent, w.bmin, w.perm,
-                    (const int32_t*)w.tile_root, w.link_tab, w.link_mask);
+                    (const int32_t*)w.blk_root, w.link_tab, w.link_mask);
 }
 
 cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t stride_words,
