@@ -521,13 +521,15 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
+  // the scalars (final once the label kernel is done) go back before the labels, so
+  // the call ends with the label copy rather than a small copy's latency after it
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   DS_CK(rec(c->ev[4]));
   if (io && io->labels)
     DS_CK(cudaMemcpyAsync(io->labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
   if (io && io->counts && d_counts64)
     DS_CK(cudaMemcpyAsync(io->counts, d_counts64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
   DS_CK(rec(c->ev[7]));
-  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   c->capturing = false;
   return DS_OK;
 }
