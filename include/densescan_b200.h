@@ -109,8 +109,13 @@ void ds_ctx_destroy(ds_ctx* ctx);
  * DS_OPT_EVENT_TIMING (default 0): time stage 1+2, the eps-tile kernel and stage 3
  * of ds_run_dbscan / ds_run_dbscan_device with CUDA events recorded between the
  * kernels; 0 takes them from %globaltimer stamps the kernels write (events between
- * kernels cost device time: they break the programmatic overlap of the launches). */
-enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3, DS_OPT_EVENT_TIMING = 4 };
+ * kernels cost device time: they break the programmatic overlap of the launches).
+ * DS_OPT_TEST_CAPACITY (default 0; test hook): > 0 starts the next stage 1+2 from
+ * a unit-list and adjacency-word capacity of `value` entries and at most doubles it
+ * per re-run, so one call walks through many capacity grow steps. Every launch that
+ * overflowed is discarded and re-run; a call never returns results from one. */
+enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3, DS_OPT_EVENT_TIMING = 4,
+       DS_OPT_TEST_CAPACITY = 5 };
 ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
 int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
 
@@ -155,6 +160,35 @@ ds_status ds_fused_build(ds_ctx* ctx, const double* coords, int64_t n, int32_t d
 ds_status ds_merge_bits(ds_ctx* ctx, const uint8_t* bits, const int64_t* counts,
                         const uint8_t* valid, int64_t n, int64_t min_pts,
                         int64_t* labels_out, ds_timings* timings);
+
+/*
+ * The Warshall backend's merge (merge_warshall, merge.py:218-238): like
+ * ds_merge_bits, but the core set is `core` (uint8[n]) exactly as given — the
+ * reference reads valid_vec.valid and never checks it against the counts.
+ * Label-equivalent to the closure for the symmetric neighbourhood relation
+ * stage 1+2 produces (SPEC merge contract).
+ */
+ds_status ds_merge_bits_core(ds_ctx* ctx, const uint8_t* bits, const uint8_t* core, int64_t n,
+                             int64_t* labels_out, ds_timings* timings);
+
+/*
+ * build_core_adjacency (merge.py:179-188): the n x ceil(n/8) packbits matrix
+ * restricted to the rows and columns of the m valid points. core_indices_out
+ * (int64[m], ascending) and adj_out (m x ceil(m/8) packbits rows) are written;
+ * m must equal the number of non-zero entries of valid (DS_EINVAL otherwise).
+ */
+ds_status ds_core_adjacency(ds_ctx* ctx, const uint8_t* bits, const uint8_t* valid, int64_t n,
+                            int64_t m, int64_t* core_indices_out, uint8_t* adj_out,
+                            ds_timings* timings);
+
+/*
+ * warshall_closure (merge.py:191-215): transitive closure of an m x m packbits
+ * relation (m x ceil(m/8) bytes) into closed_out (same layout), identical to the
+ * reference's pivot recurrence for any input relation (blocked over 32-pivot
+ * blocks on the device). The input is not modified.
+ */
+ds_status ds_warshall_closure(ds_ctx* ctx, const uint8_t* adj, int64_t m, uint8_t* closed_out,
+                              ds_timings* timings);
 
 /* ---- materialising ladder (kernels.py:153-308) ----
  * The BASELINE / SOA / TILED / TILED_UNROLLED rungs all compute the same

@@ -241,3 +241,28 @@ def dbscan(coords, eps_sq: float, min_pts: int, formula: int = ALGEBRAIC):
 
 def unpack_ref_bits(bits: np.ndarray, n: int) -> np.ndarray:
     return np.unpackbits(bits, axis=-1, count=n).view(bool)
+
+
+# ---- Warshall backend (reference merge.py:169-238) --------------------------------
+
+def core_adjacency(bits: np.ndarray, valid: np.ndarray):
+    """build_core_adjacency (merge.py:179-188): (core_indices int64, packbits rows of
+    the bits restricted to core rows and columns)."""
+    valid = np.asarray(valid, dtype=bool)
+    n = valid.shape[0]
+    ci = np.nonzero(valid)[0].astype(np.int64)
+    rows = np.unpackbits(bits[ci], axis=-1, count=n).view(bool)[:, ci]
+    return ci, np.packbits(rows, axis=-1)
+
+
+def warshall_closure_bits(adj_bits: np.ndarray, m: int) -> np.ndarray:
+    """warshall_closure (merge.py:191-215): for each pivot k in order, every row with
+    bit k set (other than k itself) ORs in row k. Returns packbits rows."""
+    rel = np.unpackbits(adj_bits, axis=-1, count=m).view(bool).copy()
+    for k in range(m):
+        col = rel[:, k].copy()
+        col[k] = False
+        rows = np.nonzero(col)[0]
+        if rows.size:
+            rel[rows] |= rel[k]
+    return np.packbits(rel, axis=-1)

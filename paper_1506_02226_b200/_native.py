@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
 DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT, DS_OPT_CUDA_GRAPH, DS_OPT_EVENT_TIMING = 1, 2, 3, 4
+DS_OPT_TEST_CAPACITY = 5
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
@@ -29,7 +30,8 @@ EXPORTS = (
     "ds_ctx_create", "ds_ctx_destroy", "ds_ctx_set_option", "ds_ctx_get_option",
     "ds_host_register", "ds_host_unregister",
     "ds_run_dbscan", "ds_run_dbscan_device",
-    "ds_fused_build", "ds_merge_bits", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
+    "ds_fused_build", "ds_merge_bits", "ds_merge_bits_core", "ds_core_adjacency",
+    "ds_warshall_closure", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
     "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
     "ds_shard_stage3_local", "ds_shard_stage3_merge",
 )
@@ -112,6 +114,13 @@ def load_library(path: str = LIB_PATH):
         lib.ds_merge_bits.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
                                       ctypes.POINTER(Timings)]
         lib.ds_merge_bits.restype = ctypes.c_int
+        lib.ds_merge_bits_core.argtypes = [vp, vp, vp, ctypes.c_int64, vp, ctypes.POINTER(Timings)]
+        lib.ds_merge_bits_core.restype = ctypes.c_int
+        lib.ds_core_adjacency.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp,
+                                          ctypes.POINTER(Timings)]
+        lib.ds_core_adjacency.restype = ctypes.c_int
+        lib.ds_warshall_closure.argtypes = [vp, vp, ctypes.c_int64, vp, ctypes.POINTER(Timings)]
+        lib.ds_warshall_closure.restype = ctypes.c_int
         lib.ds_dist_matrix.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp,
                                        ctypes.POINTER(Timings)]
         lib.ds_dist_matrix.restype = ctypes.c_int
@@ -209,6 +218,12 @@ class Context:
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_CUDA_GRAPH, 1 if on else 0),
                   self.lib)
 
+    def set_test_capacity(self, entries: int) -> None:
+        """Test hook: start the next stage 1+2 from `entries` unit-list / word slots and
+        at most double them per re-run (0: normal sizing)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_TEST_CAPACITY, int(entries)),
+                  self.lib)
+
     def configure(self, prune: bool = True, spatial_order: bool = True) -> None:
         """Set both schedule options; a no-op when they are unchanged since the last call
         (run_dbscan calls this every time)."""
@@ -219,6 +234,11 @@ class Context:
         self.set_tile_cull(prune)
         self.set_spatial_sort(spatial_order)
         self._schedule = state
+
+    def schedule(self) -> tuple[bool, bool]:
+        """The current (prune, spatial_order) options of this context."""
+        return (self.lib.ds_ctx_get_option(self.handle, DS_OPT_TILE_CULL) == 1,
+                self.lib.ds_ctx_get_option(self.handle, DS_OPT_SPATIAL_SORT) == 1)
 
     # -- entry points --------------------------------------------------------
     def run_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
@@ -307,6 +327,48 @@ class Context:
         raise_for(st, self.lib)
         return labels, t
 
+
+    def merge_bits_core(self, bits: np.ndarray, core: np.ndarray):
+        """Union-find merge with the core set taken as given (merge_warshall)."""
+        n = core.shape[0]
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        if bits.shape != (n, (n + 7) // 8):
+            raise ValueError(f"bits must have shape {(n, (n + 7) // 8)}, got {bits.shape}")
+        core8 = np.ascontiguousarray(core, dtype=np.uint8)
+        labels = np.empty(n, dtype=np.int64)
+        t = Timings()
+        st = self.lib.ds_merge_bits_core(self.handle, bits.ctypes.data, core8.ctypes.data, n,
+                                         labels.ctypes.data, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return labels, t
+
+    def core_adjacency(self, bits: np.ndarray, valid: np.ndarray):
+        """(core_indices int64[m], m x ceil(m/8) packbits rows) of build_core_adjacency."""
+        n = valid.shape[0]
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        if bits.shape != (n, (n + 7) // 8):
+            raise ValueError(f"bits must have shape {(n, (n + 7) // 8)}, got {bits.shape}")
+        valid8 = np.ascontiguousarray(valid, dtype=np.uint8)
+        m = int(np.count_nonzero(valid8))
+        core_indices = np.empty(m, dtype=np.int64)
+        adj = np.empty((m, (m + 7) // 8), dtype=np.uint8)
+        t = Timings()
+        st = self.lib.ds_core_adjacency(self.handle, bits.ctypes.data, valid8.ctypes.data, n, m,
+                                        core_indices.ctypes.data if m else None,
+                                        adj.ctypes.data if m else None, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return core_indices, adj, t
+
+    def warshall_closure(self, adj: np.ndarray, m: int):
+        adj = np.ascontiguousarray(adj, dtype=np.uint8)
+        if adj.shape != (m, (m + 7) // 8):
+            raise ValueError(f"adjacency must have shape {(m, (m + 7) // 8)}, got {adj.shape}")
+        out = np.empty_like(adj)
+        t = Timings()
+        st = self.lib.ds_warshall_closure(self.handle, adj.ctypes.data if m else None, m,
+                                          out.ctypes.data if m else None, ctypes.byref(t))
+        raise_for(st, self.lib)
+        return out, t
 
     # ---- materialising ladder (kernels.py:153-308) ----
     def dist_matrix(self, coords: np.ndarray, mem_cap: int):

@@ -88,7 +88,7 @@ struct ds_ctx {
   Buf troot;  // per-block uniform roots of the diagonal union pass (single GPU)
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits;
+      keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits, adjm, ci32, ci64, cws;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -107,6 +107,12 @@ struct ds_ctx {
   UnitArgs units{};                  // the last eps-tile launch (read by stage 3)
   int unit_lb = 4;                   // its lane blocks per tile
   Scalars* h_scalars = nullptr;      // pinned
+  // DS_OPT_TEST_CAPACITY (test hook): > 0 forces this initial unit-list and word
+  // capacity on the next stage 1+2 and limits every regrow to x2, so one call walks
+  // through many grow steps; 0 (default) = normal sizing
+  int64_t test_cap = 0;
+  bool test_cap_pending = false;
+  bool no_graph_key = false;         // the recorded graph lacked a host-copy node
 };
 
 namespace {
@@ -137,7 +143,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                       &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                      &c->dist, &c->dbits, &c->troot};
+                      &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -293,8 +299,13 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   pl.item_hi = pl.all_items * (rank + 1) / world;
   const int64_t T = pl.T;
   pl.dense_units = pl.all_items * lane_blocks(d);
+  if (c->test_cap_pending) {  // test hook: start from a tiny capacity (see ds_ctx)
+    c->units_cap = (unsigned long long)c->test_cap;
+    c->words_cap = (unsigned long long)c->test_cap;
+    c->test_cap_pending = false;
+  }
   if (pl.cull) {  // row-unit list + chunk table sized from earlier calls (lazy, like the words)
-    const unsigned long long guess = (unsigned long long)n / 8 + 4096;
+    const unsigned long long guess = c->test_cap > 0 ? 1 : (unsigned long long)n / 8 + 4096;
     pl.units_cap = std::max<unsigned long long>(c->units_cap, guess);
   } else {
     pl.units_cap = (unsigned long long)pl.dense_units;
@@ -303,7 +314,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
 
   const unsigned long long run_slack = (unsigned long long)c->sm_count * 16 * WORD_RUN;
   unsigned long long want = std::max<unsigned long long>(
-      c->words_cap, (unsigned long long)n * 8 + (1ull << 20) + run_slack);
+      c->words_cap, c->test_cap > 0 ? 1 : (unsigned long long)n * 8 + (1ull << 20) + run_slack);
   if (mem_cap > 0) {
     const int64_t room = mem_cap - (int64_t)pl.base;
     if (room < 16 * 1024) {
@@ -314,7 +325,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     want = std::min<unsigned long long>(want, (unsigned long long)(room / WORD_BYTES));
   }
   if (c->words.bytes < want * WORD_BYTES) DS_CK(ensure(c->words, want * WORD_BYTES));
-  c->words_cap = c->words.bytes / WORD_BYTES;
+  c->words_cap = c->test_cap > 0 ? want : c->words.bytes / WORD_BYTES;
   if (mem_cap > 0) {  // a buffer kept from an earlier, larger call must not bypass the cap
     const unsigned long long room_words =
         (unsigned long long)((mem_cap - (int64_t)pl.base) / WORD_BYTES);
@@ -415,44 +426,66 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
   return DS_OK;
 }
 
-// After the caller's sync (h_scalars copied): did the words overflow? If so grow the
-// buffer to the exact need (+6%) and ask for a re-run.
+// After the caller's sync (h_scalars copied): did the unit list or the adjacency
+// words overflow? If so grow what overflowed and ask for a re-run (*retry). A
+// launch that overflowed dropped work, so its results must never be returned: the
+// callers loop while *retry is set (every re-run has strictly larger capacities)
+// and fail with DS_ECAPACITY once the cap, or the attempt budget, is exhausted.
+constexpr int MAX_ATTEMPTS = 40;
+
 ds_status check_words(ds_ctx* c, const Plan& pl, int64_t mem_cap, bool* retry) {
   *retry = false;
-  if (pl.cull && c->h_scalars->unit_count > pl.units_cap) {  // unit list overflowed: grow, re-run
-    const unsigned long long nu = c->h_scalars->unit_count;
-    const unsigned long long grow = nu + nu / 16 + 1024;
-    const int64_t required = (int64_t)(pl.base + (grow - pl.units_cap) * unit_bytes(true));
-    if (mem_cap > 0 && required > mem_cap) {
-      set_capacity(required, mem_cap);
-      set_error("work-unit list exceeds the memory cap");
-      return DS_ECAPACITY;
-    }
-    c->units_cap = grow;
-    *retry = true;
+  const bool limited = c->test_cap > 0;  // test hook: at most x2 per grow step
+  const unsigned long long nu = c->h_scalars->unit_count;
+  const unsigned long long need = c->h_scalars->words_count;  // reserved slots (runs)
+  unsigned long long units_next = c->units_cap, words_next = c->words_cap;
+  if (pl.cull && nu > pl.units_cap) {  // the unit list overflowed: grow it
+    units_next = nu + nu / 16 + 1024;
+    if (limited) units_next = std::min<unsigned long long>(units_next, 2 * pl.units_cap + 1);
+    // the launch evaluated only the first units_cap units: its word count scales
+    // with the share of units it saw, so grow the words in the same step
+    const double share = (double)nu / (double)std::max<unsigned long long>(pl.units_cap, 1);
+    const unsigned long long est = (unsigned long long)((double)need * share);
+    if (est > c->words_cap) words_next = est + est / 4;
+  } else if (need > c->words_cap) {
+    // reservations of a re-run differ only by warp scheduling (need >= words); +25%
+    // and a run per resident warp covers that in practice
+    words_next = need + need / 4;
+  } else {
     return DS_OK;
   }
-  const unsigned long long need = c->h_scalars->words_count;  // reserved slots (runs)
-  if (need <= c->words_cap) return DS_OK;
-  // reservations of a re-run differ only by warp scheduling (need >= words); +25% and
-  // a run per resident warp covers that in practice, another overflow re-runs again
-  const unsigned long long grow =
-      need + need / 4 + (unsigned long long)c->sm_count * 16 * WORD_RUN + 1024;
-  const int64_t required = (int64_t)(pl.base + grow * WORD_BYTES);
+  if (words_next > c->words_cap) {
+    words_next += (unsigned long long)c->sm_count * 16 * WORD_RUN + 1024;
+    if (limited) words_next = std::min<unsigned long long>(words_next, 2 * c->words_cap + 1);
+  }
+  const int64_t required = (int64_t)(pl.base + (units_next - pl.units_cap) * unit_bytes(pl.cull) +
+                                     words_next * WORD_BYTES);
   if (mem_cap > 0 && required > mem_cap) {
-    set_capacity((int64_t)(pl.base + need * WORD_BYTES), mem_cap);
-    set_error("adjacency words exceed the memory cap");
+    set_capacity(required, mem_cap);
+    set_error(units_next > c->units_cap ? "work-unit list exceeds the memory cap"
+                                        : "adjacency words exceed the memory cap");
     return DS_ECAPACITY;
   }
-  if (c->words.bytes < grow * WORD_BYTES) {
+  if (words_next > c->words_cap && c->words.bytes < words_next * WORD_BYTES) {
     if (c->words.p) cudaFree(c->words.p);
+    ++g_alloc_generation;
     c->words.p = nullptr;
     c->words.bytes = 0;
-    DS_CK(ensure(c->words, grow * WORD_BYTES));
+    DS_CK(ensure(c->words, words_next * WORD_BYTES));
   }
-  c->words_cap = grow;
+  c->units_cap = units_next;
+  c->words_cap = words_next;
   *retry = true;
   return DS_OK;
+}
+
+// A re-run was requested by check_words: fail instead of looping forever.
+ds_status retry_budget(int attempt) {
+  if (attempt < MAX_ATTEMPTS) return DS_OK;
+  set_error("adjacency capacity did not converge after " + std::to_string(attempt) +
+            " stage 1+2 launches");
+  set_capacity(0, 0);
+  return DS_ECAPACITY;
 }
 
 void stage12_timings(const ds_ctx* c, const Plan& pl, int launches, ds_timings* t) {
@@ -585,7 +618,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[11] = c->units_cap;
     key[1] |= (unsigned long long)(io && io->coords) << 41 | (unsigned long long)(io && io->labels) << 42 |
               (unsigned long long)(io && io->counts) << 43;
-    const bool use_graph = c->use_graph && io_graphable;
+    const bool use_graph = c->use_graph && io_graphable && !c->no_graph_key;
     const bool graph_hit = use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
     if (graph_hit) {
       if (io && io->coords && c->gn_h2d)
@@ -645,8 +678,17 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
         c->gn_h2d = io ? find_copy_node(graph, io->coords) : nullptr;
         c->gn_labels = io ? find_copy_node(graph, io->labels) : nullptr;
         c->gn_counts = io ? find_copy_node(graph, io->counts) : nullptr;
-        std::memcpy(c->gkey, key, sizeof key);
         DS_CK(cudaGraphLaunch(c->gexec, s));
+        const bool nodes_ok = !io || ((!io->coords || c->gn_h2d) && (!io->labels || c->gn_labels) &&
+                                      (!io->counts || c->gn_counts));
+        if (nodes_ok) {
+          std::memcpy(c->gkey, key, sizeof key);
+        } else {
+          // a host copy could not be re-pointed on replay: this key runs eagerly from
+          // now on (the launch above used this call's own buffers, so it is correct)
+          std::memset(c->gkey, 0, sizeof key);
+          c->no_graph_key = true;
+        }
       }
     } else {
       ds_status st = enqueue_device(c, d_coords, n, d, eps_sq, min_pts, formula, mem_cap,
@@ -671,7 +713,9 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
       }
-      if (attempt < 3) continue;
+      st = retry_budget(attempt);
+      if (st != DS_OK) return st;
+      continue;
     }
     stage12_timings(c, pl, attempt, t);
     break;
@@ -760,7 +804,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                 &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                &c->dist, &c->dbits, &c->troot};
+                &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -873,7 +917,11 @@ ds_status ds_fused_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, 
     bool retry = false;
     st = check_words(c, pl, mem_cap, &retry);
     if (st != DS_OK) return st;
-    if (retry && attempt < 3) continue;
+    if (retry) {
+      st = retry_budget(attempt);
+      if (st != DS_OK) return st;
+      continue;
+    }
     stage12_timings(c, pl, attempt, &local);
     break;
   }
@@ -911,6 +959,20 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
     c->event_timing = value ? 1 : 0;
     return DS_OK;
   }
+  if (option == DS_OPT_TEST_CAPACITY) {
+    if (value < 0) {
+      set_error("DS_OPT_TEST_CAPACITY: value must be >= 0");
+      return DS_EINVAL;
+    }
+    c->test_cap = value;
+    c->test_cap_pending = value > 0;
+    if (c->gexec) {
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+    }
+    std::memset(c->seen_key, 0, sizeof c->seen_key);
+    return DS_OK;
+  }
   set_error("option: unknown option id");
   return DS_EINVAL;
 }
@@ -920,6 +982,7 @@ int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   if (c && option == DS_OPT_SPATIAL_SORT) return c->sort;
   if (c && option == DS_OPT_CUDA_GRAPH) return c->use_graph;
   if (c && option == DS_OPT_EVENT_TIMING) return c->event_timing;
+  if (c && option == DS_OPT_TEST_CAPACITY) return c->test_cap;
   return -1;
 }
 
@@ -975,7 +1038,11 @@ ds_status ds_shard_stage12(ds_ctx* c, const double* d_coords, int64_t n, int32_t
     bool retry = false;
     st = check_words(c, pl, mem_cap, &retry);
     if (st != DS_OK) return st;
-    if (retry && attempt < 3) continue;
+    if (retry) {
+      st = retry_budget(attempt);
+      if (st != DS_OK) return st;
+      continue;
+    }
     stage12_timings(c, pl, attempt, &local);
     break;
   }
@@ -1242,30 +1309,21 @@ ds_status ds_dist_build(ds_ctx* c, const double* coords, int64_t n, int32_t d, d
   return DS_OK;
 }
 
-ds_status ds_merge_bits(ds_ctx* c, const uint8_t* bits, const int64_t* counts, const uint8_t* valid,
-                        int64_t n, int64_t min_pts, int64_t* labels_out, ds_timings* t) {
-  if (!c || !bits || !counts || !valid || !labels_out) {
-    set_error("ctx, bits, counts, valid and labels_out must be non-NULL");
-    return DS_EINVAL;
-  }
-  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
-  if (st != DS_OK) return st;
-  for (int64_t i = 0; i < n; ++i) {
-    if ((counts[i] >= min_pts) != (valid[i] != 0)) {  // merge.py:141-145
-      set_error("valid[" + std::to_string(i) + "] disagrees with neighbor_count[" +
-                std::to_string(i) + "] >= min_pts");
-      return DS_EINCONSISTENT;
-    }
-  }
+}  // extern "C"
+
+namespace {
+
+// Stage 3 from a reference-layout matrix: union-find over (bits AND core x core) with
+// core = cnt32 >= min_pts, lowest-core borders, canonical labels.
+ds_status merge_bits_impl(ds_ctx* c, const uint8_t* bits, const std::vector<int32_t>& cnt32,
+                          int64_t n, int64_t min_pts, int64_t* labels_out, ds_timings* t) {
   DS_CK(cudaSetDevice(c->device));
   const double t0 = now_ms();
   ds_timings local{};
   cudaStream_t s = c->stream;
-  st = alloc_common(c, n, 1);
+  ds_status st = alloc_common(c, n, 1);
   if (st != DS_OK) return st;
   c->sorted = false;  // the reference-layout matrix is in original order
-  std::vector<int32_t> cnt32((size_t)n);
-  for (int64_t i = 0; i < n; ++i) cnt32[i] = (int32_t)std::min<int64_t>(counts[i], 0x7fffffff);
   const int64_t stride = (n + 31) / 32;
   const size_t dense = (size_t)n * stride * 4;
   const size_t row_bytes = (size_t)(n + 7) / 8;
@@ -1295,6 +1353,175 @@ ds_status ds_merge_bits(ds_ctx* c, const uint8_t* bits, const int64_t* counts, c
   local.device_bytes = (int64_t)held_bytes(c);
   local.total_ms = now_ms() - t0;
   if (t) *t = local;
+  return DS_OK;
+}
+
+// reference-layout rows (n x ceil(n/8) bytes) -> native words on the device (c->dense)
+ds_status upload_rows(ds_ctx* c, const uint8_t* bits, int64_t n, int64_t* stride_out) {
+  cudaStream_t s = c->stream;
+  const int64_t stride = (n + 31) / 32;
+  const size_t dense = (size_t)n * stride * 4;
+  const size_t row_bytes = (size_t)(n + 7) / 8;
+  DS_CK(ensure(c->dense, dense));
+  DS_CK(cudaMemsetAsync(c->dense.p, 0, dense, s));
+  DS_CK(cudaMemcpy2DAsync(c->dense.p, stride * 4, bits, row_bytes, row_bytes, (size_t)n,
+                          cudaMemcpyHostToDevice, s));
+  DS_CK(launch_bswap_rows((uint32_t*)c->dense.p, n, stride, s));
+  *stride_out = stride;
+  return DS_OK;
+}
+
+// native words (m rows of stride words in buf) -> reference-layout rows on the host
+ds_status download_rows(ds_ctx* c, uint32_t* words, int64_t m, int64_t stride, uint8_t* out) {
+  cudaStream_t s = c->stream;
+  DS_CK(launch_bswap_rows(words, m, stride, s));
+  const size_t row_bytes = (size_t)(m + 7) / 8;
+  DS_CK(cudaMemcpy2DAsync(out, row_bytes, words, stride * 4, row_bytes, (size_t)m,
+                          cudaMemcpyDeviceToHost, s));
+  return DS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ds_status ds_merge_bits(ds_ctx* c, const uint8_t* bits, const int64_t* counts, const uint8_t* valid,
+                        int64_t n, int64_t min_pts, int64_t* labels_out, ds_timings* t) {
+  if (!c || !bits || !counts || !valid || !labels_out) {
+    set_error("ctx, bits, counts, valid and labels_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  for (int64_t i = 0; i < n; ++i) {
+    if ((counts[i] >= min_pts) != (valid[i] != 0)) {  // merge.py:141-145
+      set_error("valid[" + std::to_string(i) + "] disagrees with neighbor_count[" +
+                std::to_string(i) + "] >= min_pts");
+      return DS_EINCONSISTENT;
+    }
+  }
+  std::vector<int32_t> cnt32((size_t)n);
+  for (int64_t i = 0; i < n; ++i) cnt32[i] = (int32_t)std::min<int64_t>(counts[i], 0x7fffffff);
+  return merge_bits_impl(c, bits, cnt32, n, min_pts, labels_out, t);
+}
+
+ds_status ds_merge_bits_core(ds_ctx* c, const uint8_t* bits, const uint8_t* core, int64_t n,
+                             int64_t* labels_out, ds_timings* t) {
+  if (!c || !bits || !core || !labels_out) {
+    set_error("ctx, bits, core and labels_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, 1, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  // the core set is taken as given (merge_warshall, merge.py:218-238, reads
+  // valid_vec.valid and never checks it against the counts): core <=> 1 >= 1
+  std::vector<int32_t> flag((size_t)n);
+  for (int64_t i = 0; i < n; ++i) flag[i] = core[i] ? 1 : 0;
+  return merge_bits_impl(c, bits, flag, n, 1, labels_out, t);
+}
+
+ds_status ds_core_adjacency(ds_ctx* c, const uint8_t* bits, const uint8_t* valid, int64_t n,
+                            int64_t m, int64_t* core_indices_out, uint8_t* adj_out,
+                            ds_timings* t) {
+  if (!c || !bits || !valid || (m > 0 && (!core_indices_out || !adj_out))) {
+    set_error("ctx, bits, valid (and core_indices_out, adj_out when m > 0) must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, 1, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  if (m < 0 || m > n) {
+    set_error("m: must be the number of valid points");
+    return DS_EINVAL;
+  }
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  ds_status a = alloc_common(c, n, 1);
+  if (a != DS_OK) return a;
+  int64_t stride_n = 0;
+  st = upload_rows(c, bits, n, &stride_n);
+  if (st != DS_OK) return st;
+  DS_CK(ensure(c->core, (size_t)n));
+  DS_CK(cudaMemcpyAsync(c->core.p, valid, (size_t)n, cudaMemcpyHostToDevice, s));
+  DS_CK(ensure(c->ci32, (size_t)std::max<int64_t>(m, 1) * 4));
+  DS_CK(ensure(c->ci64, (size_t)std::max<int64_t>(m, 1) * 8));
+  Scalars* sc = (Scalars*)c->scalars.p;
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(launch_core_index((const uint8_t*)c->core.p, n, (int32_t*)c->flag.p,
+                          (int32_t*)c->partials.p, &sc->kept32, (int32_t*)c->ci32.p,
+                          (int64_t*)c->ci64.p, s));
+  const int64_t stride_m = (m + 31) / 32;
+  if (m > 0) {
+    DS_CK(ensure(c->adjm, (size_t)m * stride_m * 4));
+    DS_CK(launch_core_gather((const uint32_t*)c->dense.p, stride_n, (const int32_t*)c->ci32.p, m,
+                             (uint32_t*)c->adjm.p, stride_m, s));
+  }
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  int32_t m_dev = 0;
+  DS_CK(cudaMemcpyAsync(&c->h_scalars->kept32, &sc->kept32, 4, cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  m_dev = c->h_scalars->kept32;
+  if (m_dev != m) {
+    set_error("m: " + std::to_string(m) + " given but valid has " + std::to_string(m_dev) +
+              " set entries");
+    return DS_EINVAL;
+  }
+  if (m > 0) {
+    DS_CK(cudaMemcpyAsync(core_indices_out, c->ci64.p, (size_t)m * 8, cudaMemcpyDeviceToHost, s));
+    st = download_rows(c, (uint32_t*)c->adjm.p, m, stride_m, adj_out);
+    if (st != DS_OK) return st;
+    DS_CK(cudaStreamSynchronize(s));
+  }
+  if (t) {
+    ds_timings local{};
+    float k = 0;
+    DS_CK(cudaEventElapsedTime(&k, c->ev[3], c->ev[4]));
+    local.merge_ms = k;
+    local.core_count = m;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
+  }
+  return DS_OK;
+}
+
+ds_status ds_warshall_closure(ds_ctx* c, const uint8_t* adj, int64_t m, uint8_t* closed_out,
+                              ds_timings* t) {
+  if (!c || (m > 0 && (!adj || !closed_out))) {
+    set_error("ctx, adj and closed_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  if (m < 0 || m >= (int64_t)0x7fffffff) {
+    set_error("m: must be in [0, 2^31)");
+    return DS_EINVAL;
+  }
+  if (m == 0) {
+    if (t) *t = ds_timings{};
+    return DS_OK;
+  }
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  int64_t stride = 0;
+  ds_status st = upload_rows(c, adj, m, &stride);
+  if (st != DS_OK) return st;
+  DS_CK(ensure(c->cws, (size_t)(m + 32) * 4));
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  uint32_t* C = (uint32_t*)c->dense.p;
+  DS_CK(launch_closure(C, m, stride, (uint32_t*)c->cws.p + m, (uint32_t*)c->cws.p, s));
+  DS_CK(cudaEventRecord(c->ev[4], s));
+  st = download_rows(c, C, m, stride, closed_out);
+  if (st != DS_OK) return st;
+  DS_CK(cudaStreamSynchronize(s));
+  if (t) {
+    ds_timings local{};
+    float k = 0;
+    DS_CK(cudaEventElapsedTime(&k, c->ev[3], c->ev[4]));
+    local.merge_ms = k;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
+  }
   return DS_OK;
 }
 

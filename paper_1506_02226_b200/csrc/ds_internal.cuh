@@ -268,6 +268,19 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
                                 cudaStream_t s);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
+// ---- Warshall backend building blocks (ds_closure.cu) -----------------------------
+// core_indices of the valid points (ascending) as int32 and int64; flags / partials:
+// scan workspace (n ints, scan_partials_len(n) ints); *total = m
+cudaError_t launch_core_index(const uint8_t* valid, int64_t n, int32_t* flags, int32_t* partials,
+                              int32_t* total, int32_t* ci32, int64_t* ci64, cudaStream_t s);
+// adj (m x stride_m native words) = bits (n x stride_n) restricted to rows and columns ci
+cudaError_t launch_core_gather(const uint32_t* bits, int64_t stride_n, const int32_t* ci, int64_t m,
+                               uint32_t* adj, int64_t stride_m, cudaStream_t s);
+// transitive closure of the m x m native bit matrix C in place (dplus: 32 words,
+// W: m words of workspace)
+cudaError_t launch_closure(uint32_t* C, int64_t m, int64_t stride, uint32_t* dplus, uint32_t* W,
+                           cudaStream_t s);
+
 // ---- materialising ladder (ds_dist.cu) -----------------------------------------
 int64_t dist_pitch(int64_t n);  // floats per device matrix row (roundup4(n))
 // rows [row0, row0 + rows) of the direct-formula n x n matrix into out (pitch floats)

@@ -146,9 +146,15 @@ def _fused(points: PointSet, params: DbscanParams, formula: int, mem_cap, device
     # the exported matrix is n x ceil(n/8) host bytes, guarded like kernels.py:318
     ensure_capacity(n * row_bytes(n), mem_cap)
     ctx = _native.context(device)
+    # the stage-level entry points always run the default (culled, spatially ordered)
+    # schedule; the caller's options on this thread's shared context are restored
+    previous = ctx.schedule()
     ctx.configure(True, True)
-    bits, counts, valid, t = ctx.fused_build(points.coords_aos, params.eps_sq, params.min_pts,
-                                             formula, 0)
+    try:
+        bits, counts, valid, t = ctx.fused_build(points.coords_aos, params.eps_sq,
+                                                 params.min_pts, formula, 0)
+    finally:
+        ctx.configure(*previous)
     return (NeighborhoodMatrix(n=n, bits=bits, neighbor_count=counts),
             ValidVector(valid=valid, min_pts=params.min_pts), t)
 

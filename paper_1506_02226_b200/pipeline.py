@@ -51,8 +51,8 @@ class PipelineConfig:
     spatial_order: bool = True
 
     def __post_init__(self):
-        if isinstance(self.threads, bool) or not (
-                isinstance(self.threads, (int, np.integer)) and self.threads >= 1):
+        # the reference's predicate exactly (pipeline.py:39-41): bool is an int
+        if not (isinstance(self.threads, (int, np.integer)) and self.threads >= 1):
             raise ValueError(f"threads must be an integer >= 1, got {self.threads!r}")
 
 

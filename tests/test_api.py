@@ -17,17 +17,52 @@ class TestParams:
         p = ds.validate_params(1.5, 4)
         assert (p.eps, p.eps_sq, p.min_pts) == (1.5, 2.25, 4)
 
-    @pytest.mark.parametrize("eps", [0.0, -1.0, math.inf, math.nan, "1", None, True])
+    @pytest.mark.parametrize("eps", [0.0, -1.0, math.inf, math.nan, "1", None, False,
+                                     np.float32(0.3), np.int64(1)])
     def test_rejects_bad_eps(self, eps):
         with pytest.raises(ds.InvalidParams) as exc:
             ds.validate_params(eps, 4)
         assert exc.value.field == "eps"
 
-    @pytest.mark.parametrize("min_pts", [0, -3, 2.5, "4", True])
+    @pytest.mark.parametrize("min_pts", [0, -3, 2.5, "4", False, np.float64(4.0)])
     def test_rejects_bad_min_pts(self, min_pts):
         with pytest.raises(ds.InvalidParams) as exc:
             ds.validate_params(1.0, min_pts)
         assert exc.value.field == "min_pts"
+
+    def test_matches_reference_outcomes(self):
+        """Every (type, value) case of tests/golden/params.json (made by running the
+        reference's validate_params / PipelineConfig, core.py:86-93, pipeline.py:39-41):
+        same accepted values, same rejected field."""
+        import json
+        import os
+        import sys
+        sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+        from make_golden_params import make
+        with open(os.path.join(os.path.dirname(__file__), "golden", "params.json")) as fh:
+            rows = json.load(fh)
+        assert len(rows) >= 40
+
+        def run(fn):
+            try:
+                return {"ok": fn()}
+            except Exception as e:  # noqa: BLE001
+                return {"error": type(e).__name__, "field": getattr(e, "field", None)}
+
+        for row in rows:
+            x = make(row["kind"], row["value"])
+            got_eps = run(lambda: list(map(float, ds.validate_params(x, 4).__dict__.values())))
+            got_pts = run(lambda: list(map(float, ds.validate_params(1.0, x).__dict__.values())))
+            got_thr = run(lambda: int(ds.PipelineConfig(
+                variant=ds.KernelVariant(ds.VariantId.FUSED), threads=x).threads))
+            assert got_eps == row["eps"], (row["kind"], row["value"])
+            assert got_pts == row["min_pts"], (row["kind"], row["value"])
+            assert got_thr == row["threads"], (row["kind"], row["value"])
+
+    def test_bool_and_float64_accepted_like_reference(self):
+        assert ds.validate_params(True, 4).eps == 1.0
+        assert ds.validate_params(1.0, True).min_pts == 1
+        assert ds.validate_params(np.float64(0.3), np.int64(8)).min_pts == 8
 
     def test_threshold_is_float32_of_float64_square(self):
         # core.py:93 + kernels.py:355: eps^2 in float64, then narrowed
