@@ -41,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SM_COUNT_DEFAULT = 148
+METRIC = "points clustered/sec (end-to-end DBSCAN) with Gpair-evals/sec vs FP32 roofline"
 FP32_LANES_PER_SM = 128
 
 
@@ -134,50 +135,71 @@ def tile_traffic(config: str):
         return None
 
 
+def golden_labels(config: str):
+    """The committed labels of a BASELINE config (the reference's own for C1/C2, the
+    pinned C oracle's for C3-C5; tests/golden/), or None."""
+    path = os.path.join(ROOT, "tests", "golden", f"{config.lower()}.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    key = "labels" if "labels" in g.files else "alg/labels"
+    return g[key].astype(np.int64)
+
+
+def stage3_hbm(stages: dict, n: int, peaks: dict):
+    """Stage 3 (union-find merge, borders, canonical labels) against the HBM roofline:
+    algorithmic bytes = the adjacency word records read once (8 B per reserved slot,
+    stage 1's output) + the O(n) arrays it touches: counts 4, core flag 1, parent
+    read + write 8, border minimum 4, root 4, first-appearance flag 4, id scan 4,
+    int64 label 8 = 37 B per point."""
+    ms = stages.get("merge")
+    if not ms:
+        return None
+    nbytes = 8 * int(stages.get("words_emitted", 0)) + 37 * n
+    gbs = nbytes / (ms / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs")
+    return {"ms": ms, "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "peak_gbs": peak,
+            "frac": (gbs / peak) if peak else None,
+            "timing": "%globaltimer stamps at the stage boundary (device)"}
+
+
 def algorithmic_ops_per_pair(d: int, formula: int) -> int:
     # SURVEY §8(d): ALGEBRAIC 2d+1, DIRECT 3d-1 separately rounded FP32 ops per pair
     return 2 * d + 1 if formula == 1 else 3 * d - 1
 
 
 # ---------------------------------------------------------------------------------
-def cpu_sample(points, eps_sq: float, min_pts: int, rows: int, threads: int):
-    """Reference CPU path (oracle port) on `rows` rows x all N columns, threaded
-    over row blocks like the reference's run_partitioned (_parallel.py:24-39)."""
-    from concurrent.futures import ThreadPoolExecutor
-
+def cpu_full_run(points_aos, eps_sq: float, min_pts: int, threads: int):
+    """One complete clustering of the workload by the reference's CPU flow (oracle port
+    of run_dbscan, pipeline.py:70-92: threaded 256-row blocks materialising the packbits
+    neighbourhood matrix, kernels.py:311-337, then the core-core merge, border rule and
+    canonical ids, merge.py:116-166 / core.py:116-132). No sampling, no extrapolation.
+    Returns (seconds, stage-1+2 seconds, stage-3 seconds, labels)."""
     from oracle import densescan_oracle as oracle
-    p32 = oracle.narrow(points)
-    norms = oracle.sq_norms(p32)
-    thr = oracle.thr32(eps_sq)
-    n = p32.shape[0]
-    rows = min(rows, n)
-    blocks = [(r0, min(r0 + 256, rows)) for r0 in range(0, rows, 256)]
-
-    def work(b):
-        r0, r1 = b
-        hit = oracle.in_range_block(p32, norms, r0, r1, thr, oracle.ALGEBRAIC)
-        np.packbits(hit, axis=-1)
-        return int(hit.sum())
-
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as pool:
-        list(pool.map(work, blocks))
-    return time.perf_counter() - t0, rows
+    labels, _, s12, s3 = oracle.dbscan_reference_flow(points_aos, eps_sq, min_pts,
+                                                      oracle.ALGEBRAIC, threads=threads)
+    return time.perf_counter() - t0, s12, s3, labels
 
 
-def cpu_baseline(points_aos, eps_sq, min_pts, n, target_s=12.0):
+def cpu_baseline(points_aos, eps_sq, min_pts, n, runs: int = 1, golden=None):
     threads = os.cpu_count() or 1
-    # calibrate on a small slice, then size the sample for ~target_s of work
-    t_small, r_small = cpu_sample(points_aos, eps_sq, min_pts, 512, threads)
-    rows = int(max(512, min(n, r_small * target_s / max(t_small, 1e-6))))
-    rows = (rows + 255) // 256 * 256
-    secs, rows = cpu_sample(points_aos, eps_sq, min_pts, rows, threads)
-    full_s = secs * n / rows  # rows are of uniform cost (every row spans all N columns)
-    return {"value": n / full_s, "unit": "points/s", "cores": threads, "kind": "port",
-            "sample": (f"stage-1 rows 0..{rows} of {n} x all {n} columns (algebraic, numpy "
-                       f"oracle port, {threads} threads, {secs:.1f}s), extrapolated x{n / rows:.1f};"
-                       " merge excluded (<3% of the reference's time, SURVEY §6)"),
-            "seconds_extrapolated": full_s}
+    secs, s12, s3 = [], [], []
+    equal = None
+    for _ in range(runs):
+        t, a, b, labels = cpu_full_run(points_aos, eps_sq, min_pts, threads)
+        secs.append(t)
+        s12.append(a)
+        s3.append(b)
+        if golden is not None:
+            equal = bool(np.array_equal(labels, golden))
+    best = min(secs)
+    return {"value": n / best, "unit": "points/s", "cores": threads, "kind": "port",
+            "sample": (f"full workload: {n} points clustered end to end (stage 1+2 and merge), "
+                       f"{runs} run(s), min taken; numpy oracle port of the reference's "
+                       f"run_dbscan flow on {threads} host threads; no sampling or extrapolation"),
+            "seconds": best, "stage12_s": min(s12), "stage3_s": min(s3),
+            "labels_equal_reference": equal}
 
 
 # ---------------------------------------------------------------------------------
@@ -190,9 +212,12 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = ds.CONFIGS[args.config]
@@ -213,9 +238,10 @@ def run_b200(args):
     def step():
         """One clustering of the resident points -> (tile_ms, pairs_evaluated, stage dict)."""
         if world > 1:
-            labeling, tm = D.run_dbscan_sharded(None, params, formula=formula, mem_cap=mem_cap,
-                                                backend=backend, coords=coords_dev)
-            labels_dev.copy_(torch.from_numpy(labeling.labels))
+            labels, tm = D.run_dbscan_sharded(None, params, formula=formula, mem_cap=mem_cap,
+                                              backend=backend, coords=coords_dev,
+                                              return_device=True)
+            labels_dev.copy_(labels)  # device to device: no host copy in the device-timed value
             return tm.tile_ms, tm.pairs_evaluated, {
                 "stage12": tm.stage12_ms, "exchange1": tm.exchange1_ms,
                 "stage3_local": tm.stage3_local_ms, "exchange2": tm.exchange2_ms,
@@ -232,10 +258,9 @@ def run_b200(args):
 
     # parity of the benchmarked configuration against the committed reference labels
     parity = None
-    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config.lower()}.npz")
-    if os.path.exists(gpath):
-        ref = np.load(gpath)
-        parity = bool(np.array_equal(labels_dev.cpu().numpy(), ref["labels"]))
+    golden = golden_labels(args.config)
+    if golden is not None:
+        parity = bool(np.array_equal(labels_dev.cpu().numpy(), golden))
 
     if world > 1:
         torch.distributed.barrier()
@@ -336,7 +361,7 @@ def run_b200(args):
     launches_per_step = 16 * last[3] if world == 1 else 18
 
     line = {
-        "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",
+        "metric": METRIC,
         "value": n / (ms / 1e3),
         "unit": "points/s",
         "n_gpus": world,
@@ -378,12 +403,14 @@ def run_b200(args):
         "gpair_evals_per_s": pairs / tile_s / 1e9,
         "n2_decisions_per_s": (n * n if world == 1 else n * n / world) / tile_s / 1e9,
         "stages_ms": last[2],
+        "stage3_hbm": stage3_hbm(last[2], n, peaks) if world == 1 else None,
         "gpu_launches": launches_per_step * args.steps,
         "parity_vs_reference_labels": parity,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(pts.coords_aos, params.eps_sq, params.min_pts, n)
+        line["cpu_baseline"] = cpu_baseline(pts.coords_aos, params.eps_sq, params.min_pts, n,
+                                            golden=golden)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -391,6 +418,8 @@ def run_b200(args):
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU flow (oracle port, all host threads) on the
+    same workload, every warm-up and timed step a complete clustering of all N points."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -399,29 +428,59 @@ def run_reference(args):
     pts = cfg.points()
     params = ds.validate_params(cfg.eps, cfg.min_pts)
     n = pts.n
-    # each step: a bounded row sample of the same workload, extrapolated to N
-    per_step_target = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_baseline(pts.coords_aos, params.eps_sq, params.min_pts, n, per_step_target)
-    vals = [cpu_baseline(pts.coords_aos, params.eps_sq, params.min_pts, n, per_step_target)
+        cpu_full_run(pts.coords_aos, params.eps_sq, params.min_pts, threads)
+    runs = [cpu_full_run(pts.coords_aos, params.eps_sq, params.min_pts, threads)
             for _ in range(args.steps)]
-    value = statistics.mean(v["value"] for v in vals)
-    last = vals[-1]
+    ms = statistics.mean(r[0] for r in runs) * 1e3
+    value = n / (ms / 1e3)
+    golden = golden_labels(args.config)
+    parity = None if golden is None else bool(np.array_equal(runs[-1][3], golden))
     line = {
-        "metric": "points clustered/sec (end-to-end DBSCAN, C2) with Gpair-evals/sec vs FP32 roofline",
+        "metric": METRIC,
         "impl": "reference",
-        "value": value, "unit": "points/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "value": value, "unit": "points/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))),
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.description}", "n": n, "d": pts.d,
                    "eps": cfg.eps, "min_pts": cfg.min_pts, "formula": "algebraic"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": last["cores"],
-                         "kind": "port", "sample": last["sample"]},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": (f"full workload every step: {n} points clustered end to "
+                                    "end (stage 1+2 and merge) by the numpy oracle port of "
+                                    f"the reference's run_dbscan flow on {threads} host "
+                                    "threads; no sampling or extrapolation")},
+        "stages_s": {"stage12": statistics.mean(r[1] for r in runs),
+                     "stage3": statistics.mean(r[2] for r in runs)},
+        "parity_vs_reference_labels": parity,
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def _rank_entry(rank, world, port, fn, fn_args):
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1",
+                       "MASTER_PORT": str(port)})
+    fn(*fn_args)
+
+
+def spawn_ranks(world: int, fn, *fn_args):
+    """One process per GPU on this node (what torchrun --nproc-per-node does): each
+    rank gets RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* in its environment and runs
+    fn(*fn_args). Used when bench.py --gpus N > 1 is started without torchrun."""
+    import torch.multiprocessing as mp
+    mp.spawn(_rank_entry, args=(world, _free_port(), fn, fn_args), nprocs=world, join=True)
 
 
 def main():
@@ -437,6 +496,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args.gpus, run_b200, args)
     else:
         run_b200(args)
 

@@ -244,8 +244,16 @@ ds_status ds_shard_stage3_local(ds_ctx* ctx, const int32_t* d_counts, int64_t n,
                                 int32_t* d_parent, int32_t* d_bmin, void* stream,
                                 ds_timings* timings);
 
-/* Fold nparents gathered forests (nparents x n) and the min-reduced border
- * minima into canonical int64 labels. */
+/* One round of the pairwise forest exchange: d_parent (int32[n], a shard forest
+ * in the context's internal order) becomes the union of itself and d_other, and is
+ * flattened (every entry points at its root). Folding the R shard forests pairwise
+ * (recursive doubling, log2 R rounds; paper_1506_02226_b200/distributed.py) gives
+ * every rank the forest of all edges with O(n log R) work per rank. */
+ds_status ds_shard_fold(ds_ctx* ctx, int32_t* d_parent, const int32_t* d_other, int64_t n,
+                        void* stream);
+
+/* Fold nparents forests (nparents x n; 1 after the pairwise exchange) and the
+ * min-reduced border minima into canonical int64 labels. */
 ds_status ds_shard_stage3_merge(ds_ctx* ctx, const int32_t* d_counts, int64_t n, int64_t min_pts,
                                 const int32_t* d_parents, int32_t nparents, const int32_t* d_bmin,
                                 int64_t* d_labels, void* stream, ds_timings* timings);

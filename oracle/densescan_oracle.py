@@ -266,3 +266,80 @@ def warshall_closure_bits(adj_bits: np.ndarray, m: int) -> np.ndarray:
         if rows.size:
             rel[rows] |= rel[k]
     return np.packbits(rel, axis=-1)
+
+
+# ---- the reference's run_dbscan flow, threaded: the CPU baseline of bench.py -------
+
+def dbscan_reference_flow(coords, eps_sq: float, min_pts: int, formula: int = ALGEBRAIC,
+                          threads: int = 1, block: int = 256):
+    """run_dbscan(points, params, default_config()) as the reference executes it
+    (pipeline.py:70-92), for timing on the host's cores: stage 1+2 materialises the
+    packbits NeighborhoodMatrix row block by row block of 256 in a fork-join pool over
+    contiguous row ranges (kernels.py:311-337, _parallel.py:16-39); stage 3 reads the
+    packed rows masked by the core flags, takes core-core pairs as edges and the first
+    in-range core of every non-core row (merge.py:116-166 contract), then components
+    and first-appearance ids (core.py:116-132). Returns (labels, counts, seconds of
+    stage 1+2, seconds of stage 3).
+    """
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+
+    t0 = time.perf_counter()
+    p32 = narrow(coords)
+    n = p32.shape[0]
+    thr = thr32(eps_sq)
+    norms = sq_norms(p32)
+    rb = (n + 7) // 8
+    bits = np.empty((n, rb), dtype=np.uint8)
+    counts = np.empty(n, dtype=np.int64)
+    bounds = np.linspace(0, n, max(1, min(threads, n)) + 1).astype(np.int64)
+
+    def stage12(w):
+        for r0 in range(int(bounds[w]), int(bounds[w + 1]), block):
+            r1 = min(r0 + block, int(bounds[w + 1]))
+            hit = in_range_block(p32, norms, r0, r1, thr, formula)
+            counts[r0:r1] = hit.sum(axis=1)
+            bits[r0:r1] = np.packbits(hit, axis=-1)
+
+    with ThreadPoolExecutor(max_workers=len(bounds) - 1) as pool:
+        list(pool.map(stage12, range(len(bounds) - 1)))
+    t1 = time.perf_counter()
+
+    core = counts >= min_pts
+    core_pk = np.packbits(core)
+    edges, borders = [], []
+
+    def stage3(r0):
+        r1 = min(r0 + 512, n)
+        masked = bits[r0:r1] & core_pk[None, :]
+        rc = core[r0:r1]
+        rows, cols = np.nonzero(masked[rc])
+        rows = np.nonzero(rc)[0][rows]
+        vals = masked[rows, cols]
+        if vals.size:
+            unpacked = np.unpackbits(vals[:, None], axis=1).view(bool)
+            k, bit = np.nonzero(unpacked)
+            i = rows[k] + r0
+            j = cols[k].astype(np.int64) * 8 + bit
+            keep = j > i
+            edges.append((i[keep], j[keep]))
+        nc = np.nonzero(~rc)[0]
+        if nc.size:
+            sub = masked[nc]
+            nz = sub != 0
+            has = nz.any(axis=1)
+            first = nz.argmax(axis=1)
+            v = sub[np.arange(nc.size), first]
+            lead = np.unpackbits(v[:, None], axis=1).argmax(axis=1)
+            borders.append((nc[has] + r0, first[has].astype(np.int64) * 8 + lead[has]))
+
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+        list(pool.map(stage3, range(0, n, 512)))
+    src = np.concatenate([e[0] for e in edges]) if edges else np.empty(0, np.int64)
+    dst = np.concatenate([e[1] for e in edges]) if edges else np.empty(0, np.int64)
+    border = np.full(n, -1, dtype=np.int64)
+    for p, c in borders:
+        border[p] = c
+    labels = labels_from_core_graph(n, core, src, dst, border)
+    t2 = time.perf_counter()
+    return labels, counts, t1 - t0, t2 - t1

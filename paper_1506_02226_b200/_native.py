@@ -33,7 +33,7 @@ EXPORTS = (
     "ds_fused_build", "ds_merge_bits", "ds_merge_bits_core", "ds_core_adjacency",
     "ds_warshall_closure", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
     "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
-    "ds_shard_stage3_local", "ds_shard_stage3_merge",
+    "ds_shard_stage3_local", "ds_shard_stage3_merge", "ds_shard_fold",
 )
 
 
@@ -144,6 +144,8 @@ def load_library(path: str = LIB_PATH):
         lib.ds_shard_stage3_merge.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, vp,
                                               ctypes.c_int32, vp, vp, vp, ctypes.POINTER(Timings)]
         lib.ds_shard_stage3_merge.restype = ctypes.c_int
+        lib.ds_shard_fold.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
+        lib.ds_shard_fold.restype = ctypes.c_int
         if lib.ds_abi_version() != 1:
             raise ImportError(f"{path}: unexpected ABI version {lib.ds_abi_version()}")
         _lib = lib
@@ -296,6 +298,12 @@ class Context:
                                             ctypes.c_void_p(stream_ptr or None), ctypes.byref(t))
         raise_for(st, self.lib)
         return t
+
+    def shard_fold(self, parent_ptr, other_ptr, n, stream_ptr=0):
+        st = self.lib.ds_shard_fold(self.handle, ctypes.c_void_p(parent_ptr),
+                                    ctypes.c_void_p(other_ptr), int(n),
+                                    ctypes.c_void_p(stream_ptr or None))
+        raise_for(st, self.lib)
 
     def fused_build(self, coords: np.ndarray, eps_sq: float, min_pts: int, formula: int,
                     mem_cap: int, want_bits: bool = True):

@@ -1127,6 +1127,21 @@ ds_status ds_shard_stage3_merge(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   return DS_OK;
 }
 
+ds_status ds_shard_fold(ds_ctx* c, int32_t* d_parent, const int32_t* d_other, int64_t n,
+                        void* stream) {
+  if (!c || !d_parent || !d_other) {
+    set_error("ctx, d_parent and d_other must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, 1, 1, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  DS_CK(launch_fold_forest(d_parent, d_other, n, s));
+  DS_CK(cudaStreamSynchronize(s));
+  return DS_OK;
+}
+
 // ---- materialising ladder (ds_dist.cu) ---------------------------------------------
 namespace {
 

@@ -245,6 +245,8 @@ cudaError_t launch_union_dense(const MergeWs& w, const uint32_t* bits32, int64_t
                                cudaStream_t s);
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R, cudaStream_t s);
 cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s);
+// parent <- union of the forests parent and other, flattened (multi-GPU fold round)
+cudaError_t launch_fold_forest(int32_t* parent, const int32_t* other, int64_t n, cudaStream_t s);
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
                               cudaStream_t s);
 cudaError_t launch_export_bits(const uint2* words, unsigned long long words_cap, const uint2* uchunks,

@@ -1025,9 +1025,35 @@ __global__ void merge_forests_kernel(const int32_t* __restrict__ parents, int R,
   }
 }
 
+// Multi-GPU pairwise fold: parent |= the forest `other` (link i with other[i] for every
+// i it moves), then every entry is pointed at its root so the forest sent on in the
+// next round of the exchange is flat.
+__global__ void fold_forest_kernel(const int32_t* __restrict__ other, int64_t n, int32_t* parent) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = other[i];
+    if (p != (int)i) link_root(parent, find_plain(parent, (int)i), p);
+  }
+}
+
+__global__ void flatten_forest_kernel(int64_t n, int32_t* parent) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    parent[i] = find_root_ro(parent, (int)i);  // roots are final: read-only walk
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
+
+cudaError_t launch_fold_forest(int32_t* parent, const int32_t* other, int64_t n, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  fold_forest_kernel<<<sms * 8, 256, 0, s>>>(other, n, parent);
+  flatten_forest_kernel<<<sms * 8, 256, 0, s>>>(n, parent);
+  return cudaGetLastError();
+}
 
 int64_t scan_partials_len(int64_t n) { return 2 * ((n + SCAN_BLK - 1) / SCAN_BLK + 1); }
 

@@ -36,6 +36,11 @@ class PipelineConfig:
 
     `threads` is validated as in the reference but the device ignores it.
     `device` picks the CUDA ordinal (None: $DENSESCAN_DEVICE or 0).
+    `devices` (a sequence of ordinals, optional) shards one call over several
+    devices inside this process — the stage-1 tile pairs are dealt to the shards,
+    counts / border minima / union-find forests are exchanged device to device
+    (distributed.run_dbscan_multi) — the device analogue of the reference's
+    worker threads (`threads`, _parallel.py:24-39). Labels do not depend on it.
     `prune` skips tile pairs whose bounding boxes prove every pair out of range
     (with a float32 error margin) and `spatial_order` visits the points in
     Morton order so tiles are compact; results are bit-identical either way,
@@ -47,6 +52,7 @@ class PipelineConfig:
     threads: int = 1
     mem_cap: int | None = None
     device: int | None = None
+    devices: tuple | list | None = None
     prune: bool = True
     spatial_order: bool = True
 
@@ -121,7 +127,17 @@ def run_dbscan(points: PointSet, params: DbscanParams, config: PipelineConfig):
     if variant.materializes_distance():
         # the reference allocates the 4 n^2 float32 matrix for these rungs (kernels.py:156)
         ensure_capacity(4 * points.n * points.n, mem_cap)
-    ctx = _native.context(config.device)
+    if config.devices is not None and len(config.devices) > 1:
+        from .distributed import run_dbscan_multi
+        labels, tm = run_dbscan_multi(points, params, config.devices, variant.formula, mem_cap,
+                                      config.prune, config.spatial_order)
+        st = StageTimings(fused_ms=tm.stage12_ms + tm.exchange1_ms,
+                          merge_ms=tm.stage3_local_ms + tm.exchange2_ms + tm.stage3_merge_ms,
+                          total_ms=(time.perf_counter() - t0) * 1e3, tile_ms=tm.tile_ms,
+                          pairs_evaluated=tm.pairs_evaluated)
+        return Labeling(labels), st
+    ctx = _native.context(config.device if config.devices is None or not config.devices
+                          else config.devices[0])
     ctx.configure(config.prune, config.spatial_order)
     _native.pin_frozen(points.coords_aos, points)
     labels, _, t = ctx.run_dbscan(points.coords_aos, params.eps_sq, params.min_pts,

@@ -82,10 +82,30 @@ class CpuShardBackend:
                     bmin[i] = min(bmin[i], j)
         return torch.from_numpy(parent.astype(np.int32)), torch.from_numpy(bmin.astype(np.int32))
 
+    def fold(self, parent, other):
+        """numpy stand-in of ds_shard_fold: union of two forests, flattened, in place."""
+        par = parent.numpy().astype(np.int64)
+        oth = other.numpy()
+
+        def find(x):
+            while par[x] != x:
+                par[x] = par[par[x]]
+                x = par[x]
+            return x
+
+        for i in np.nonzero(oth != np.arange(oth.size))[0].tolist():
+            ri, rj = find(i), find(int(oth[i]))
+            if ri != rj:
+                par[max(ri, rj)] = min(ri, rj)
+        parent.copy_(torch.from_numpy(np.array([find(i) for i in range(par.size)],
+                                               dtype=np.int32)))
+
     def stage3_merge(self, counts, min_pts, parents, bmin):
         n = self.n
         core = counts.numpy() >= min_pts
         par = parents.numpy()
+        if par.ndim == 1:
+            par = par[None, :]
         src = np.concatenate([np.arange(n)[core & (p != np.arange(n))] for p in par])
         dst = np.concatenate([p[core & (p != np.arange(n))] for p in par])
         border = bmin.numpy().astype(np.int64)
@@ -142,12 +162,38 @@ def test_shard_ranges_partition_items():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_fold_rounds_reach_every_forest():
+    """Simulate the schedule: each rank starts with its own set; after the rounds
+    every rank must hold the union of all sets, for any world size."""
+    for world in range(1, 13):
+        held = [{r} for r in range(world)]
+        for rnd in D.fold_rounds(world):
+            new = [set(h) for h in held]
+            for kind, a, b in rnd:
+                if kind == "swap":
+                    new[a] |= held[b]
+                    new[b] |= held[a]
+                elif kind == "fold":
+                    new[b] |= held[a]
+                else:
+                    new[b] = set(held[a])
+            held = new
+        assert all(h == set(range(world)) for h in held), world
+        # each rank takes part in at most one step per round (no conflicting writes)
+        for rnd in D.fold_rounds(world):
+            ranks = [r for _, a, b in rnd for r in (a, b)]
+            assert len(ranks) == len(set(ranks))
+        rounds = len(D.fold_rounds(world))
+        p = 1 << (world.bit_length() - 1)
+        assert rounds == (p.bit_length() - 1) + (2 if world > p else 0)
+
+
 @pytest.mark.parametrize("formula", [1, 0])
 def test_sharded_labels_equal_reference_any_world(formula):
     coords = generate_blobs(1300, 4, 0.15, 0.2, 21, 2).coords_aos
     eps, min_pts = 0.08, 5
     want, _ = oracle.dbscan(coords, eps * eps, min_pts, formula)
-    for world in (1, 2, 3):
+    for world in (1, 2, 3, 4, 5):
         out = run_world(world, coords, eps, min_pts, formula)
         items = sorted(v[1] for v in out.values())
         assert items[0][0] == 0 and items[-1][1] == D.tile_items(1300)

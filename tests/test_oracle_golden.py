@@ -95,3 +95,20 @@ def test_formulas_really_differ_somewhere():
     diffs = sum(not np.array_equal(g[f"{n}/alg/counts"], g[f"{n}/dir/counts"])
                 for n in (str(x) for x in g["names"]))
     assert diffs >= 1
+
+
+def test_reference_flow_port_matches_reference():
+    """The threaded CPU baseline (bench.py cpu_baseline / --impl reference) computes the
+    reference's labels and counts: C1 both formulas, the 48 random unfiltered sets."""
+    from paper_1506_02226_b200.datasets import CONFIGS
+    g = load_golden("c1.npz")
+    pts = CONFIGS["C1"].points()
+    for name, f in (("alg", 1), ("dir", 0)):
+        labels, counts, _, _ = oracle.dbscan_reference_flow(pts.coords_aos, 0.3 * 0.3, 4, f,
+                                                            threads=3)
+        assert np.array_equal(labels, g[f"{name}/labels"])
+        assert np.array_equal(counts, g[f"{name}/counts"])
+    r = load_golden("random.npz")
+    for name, coords, eps, eps_sq, min_pts in random_specs(r):
+        labels, counts, _, _ = oracle.dbscan_reference_flow(coords, eps_sq, min_pts, 1, threads=2)
+        assert np.array_equal(labels, r[f"{name}/alg/labels"]), name
