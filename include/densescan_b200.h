@@ -190,6 +190,19 @@ ds_status ds_core_adjacency(ds_ctx* ctx, const uint8_t* bits, const uint8_t* val
 ds_status ds_warshall_closure(ds_ctx* ctx, const uint8_t* adj, int64_t m, uint8_t* closed_out,
                               ds_timings* timings);
 
+/*
+ * serial_dbscan (oracle.py:48-111), the reference's float64 semantic oracle, on the
+ * device: d2 = ((x_j - x_i)^2 + (y_j - y_i)^2) + ... in float64 (one IEEE op each, no
+ * FMA), in range iff d2 <= eps_sq (float64), counts incl. self, clusters = connected
+ * components of core-core pairs, borders to their lowest-indexed in-range core,
+ * canonical labels. Used by the CLI's --variant serial and the bench equivalence gate
+ * (cli.py:94-122, 152-234). timings: tile_ms = distance + eps stage, fused_ms = core
+ * flags, merge_ms = components + borders + labels. Needs n * ceil(n/32) * 4 device bytes.
+ */
+ds_status ds_serial_dbscan(ds_ctx* ctx, const double* coords, int64_t n, int32_t d, double eps_sq,
+                           int64_t min_pts, int64_t* labels_out, int64_t* counts_out,
+                           ds_timings* timings);
+
 /* ---- materialising ladder (kernels.py:153-308) ----
  * The BASELINE / SOA / TILED / TILED_UNROLLED rungs all compute the same
  * direct-formula squared distances (kernels.py:21-25, _direct_block 197-210):

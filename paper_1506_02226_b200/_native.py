@@ -31,7 +31,7 @@ EXPORTS = (
     "ds_host_register", "ds_host_unregister",
     "ds_run_dbscan", "ds_run_dbscan_device",
     "ds_fused_build", "ds_merge_bits", "ds_merge_bits_core", "ds_core_adjacency",
-    "ds_warshall_closure", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
+    "ds_warshall_closure", "ds_serial_dbscan", "ds_dist_matrix", "ds_dist_threshold", "ds_dist_build",
     "ds_tile_items", "ds_tile_side", "ds_shard_stage12",
     "ds_shard_stage3_local", "ds_shard_stage3_merge", "ds_shard_fold",
 )
@@ -121,6 +121,9 @@ def load_library(path: str = LIB_PATH):
         lib.ds_core_adjacency.restype = ctypes.c_int
         lib.ds_warshall_closure.argtypes = [vp, vp, ctypes.c_int64, vp, ctypes.POINTER(Timings)]
         lib.ds_warshall_closure.restype = ctypes.c_int
+        lib.ds_serial_dbscan.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                         ctypes.c_int64, vp, vp, ctypes.POINTER(Timings)]
+        lib.ds_serial_dbscan.restype = ctypes.c_int
         lib.ds_dist_matrix.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, vp,
                                        ctypes.POINTER(Timings)]
         lib.ds_dist_matrix.restype = ctypes.c_int
@@ -349,6 +352,18 @@ class Context:
                                          labels.ctypes.data, ctypes.byref(t))
         raise_for(st, self.lib)
         return labels, t
+
+    def serial_dbscan(self, coords: np.ndarray, eps_sq: float, min_pts: int):
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n, d = coords.shape
+        labels = np.empty(n, dtype=np.int64)
+        counts = np.empty(n, dtype=np.int64)
+        t = Timings()
+        st = self.lib.ds_serial_dbscan(self.handle, coords.ctypes.data, n, d, float(eps_sq),
+                                       int(min_pts), labels.ctypes.data, counts.ctypes.data,
+                                       ctypes.byref(t))
+        raise_for(st, self.lib)
+        return labels, counts, t
 
     def core_adjacency(self, bits: np.ndarray, valid: np.ndarray):
         """(core_indices int64[m], m x ceil(m/8) packbits rows) of build_core_adjacency."""

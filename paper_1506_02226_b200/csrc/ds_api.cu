@@ -88,7 +88,7 @@ struct ds_ctx {
   Buf troot;  // per-block uniform roots of the diagonal union pass (single GPU)
   Buf coords64, rec, cnt, core, corew, parent, bmin, cmin, root, flag, partials, labels, counts64,
       words, chunks, scalars, dense, tbox, items, iflags, ipartials, rec_sorted, perm, inv, keys,
-      keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits, adjm, ci32, ci64, cws;
+      keys_alt, kidx, sort_temp, blk, ulist, uchunks, ucnt, dist, dbits, adjm, ci32, ci64, cws, soa64;
   int cull = 1;          // DS_OPT_TILE_CULL
   int use_graph = 1;     // DS_OPT_CUDA_GRAPH
   // CUDA graph of the device pipeline, replayed while the key matches
@@ -143,7 +143,7 @@ size_t held_bytes(const ds_ctx* c) {
                       &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                       &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                       &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                      &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws};
+                      &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws, &c->soa64};
   size_t s = 0;
   for (const Buf* b : all) s += b->bytes;
   return s;
@@ -804,7 +804,7 @@ void ds_ctx_destroy(ds_ctx* c) {
                 &c->tbox,     &c->items,  &c->iflags, &c->ipartials,
                 &c->rec_sorted, &c->perm, &c->inv, &c->keys, &c->keys_alt, &c->kidx,
                 &c->sort_temp, &c->blk, &c->ulist, &c->uchunks, &c->ucnt,
-                &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws};
+                &c->dist, &c->dbits, &c->troot, &c->adjm, &c->ci32, &c->ci64, &c->cws, &c->soa64};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : c->ev)
@@ -1493,6 +1493,66 @@ ds_status ds_core_adjacency(ds_ctx* c, const uint8_t* bits, const uint8_t* valid
     DS_CK(cudaEventElapsedTime(&k, c->ev[3], c->ev[4]));
     local.merge_ms = k;
     local.core_count = m;
+    local.device_bytes = (int64_t)held_bytes(c);
+    local.total_ms = now_ms() - t0;
+    *t = local;
+  }
+  return DS_OK;
+}
+
+ds_status ds_serial_dbscan(ds_ctx* c, const double* coords, int64_t n, int32_t d, double eps_sq,
+                           int64_t min_pts, int64_t* labels_out, int64_t* counts_out,
+                           ds_timings* t) {
+  if (!c || !coords || !labels_out) {
+    set_error("ctx, coords and labels_out must be non-NULL");
+    return DS_EINVAL;
+  }
+  ds_status st = check_args(n, d, min_pts, DS_FORMULA_DIRECT);
+  if (st != DS_OK) return st;
+  DS_CK(cudaSetDevice(c->device));
+  const double t0 = now_ms();
+  cudaStream_t s = c->stream;
+  st = alloc_common(c, n, 1);
+  if (st != DS_OK) return st;
+  c->sorted = false;
+  const int64_t stride = (n + 31) / 32;
+  const size_t in_bytes = (size_t)n * d * 8;
+  DS_CK(ensure(c->coords64, in_bytes));
+  DS_CK(ensure(c->soa64, in_bytes));
+  DS_CK(ensure(c->dense, (size_t)n * stride * 4));
+  DS_CK(ensure(c->labels, (size_t)n * 8));
+  DS_CK(ensure(c->counts64, (size_t)n * 8));
+  DS_CK(cudaMemcpyAsync(c->coords64.p, coords, in_bytes, cudaMemcpyHostToDevice, s));
+  DS_CK(cudaMemsetAsync(c->scalars.p, 0, sizeof(Scalars), s));
+  DS_CK(cudaEventRecord(c->ev[0], s));
+  DS_CK(launch_serial_words((const double*)c->coords64.p, n, d, eps_sq, (double*)c->soa64.p,
+                            (uint32_t*)c->dense.p, stride, (int32_t*)c->cnt.p, s));
+  DS_CK(cudaEventRecord(c->ev[1], s));
+  MergeWs w = merge_ws(c, n);
+  DS_CK(launch_core_init(w, min_pts, s));
+  DS_CK(cudaEventRecord(c->ev[2], s));
+  DS_CK(launch_union_dense(w, (const uint32_t*)c->dense.p, stride, s));
+  DS_CK(launch_finalize(w, (int64_t*)c->labels.p, s));
+  DS_CK(cudaEventRecord(c->ev[3], s));
+  DS_CK(cudaMemcpyAsync(labels_out, c->labels.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  if (counts_out) {
+    DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, nullptr, (int64_t*)c->counts64.p, s));
+    DS_CK(cudaMemcpyAsync(counts_out, c->counts64.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  }
+  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  DS_CK(cudaStreamSynchronize(s));
+  if (t) {
+    ds_timings local{};
+    float a = 0, b = 0, m = 0;
+    DS_CK(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+    DS_CK(cudaEventElapsedTime(&b, c->ev[1], c->ev[2]));
+    DS_CK(cudaEventElapsedTime(&m, c->ev[2], c->ev[3]));
+    local.tile_ms = a;   // dist_sq stage (fused with the eps test and counts)
+    local.fused_ms = b;  // core flags
+    local.merge_ms = m;
+    local.pairs_evaluated = n * n;
+    local.core_count = (int64_t)c->h_scalars->ncore;
+    local.cluster_count = c->h_scalars->nclusters;
     local.device_bytes = (int64_t)held_bytes(c);
     local.total_ms = now_ms() - t0;
     *t = local;

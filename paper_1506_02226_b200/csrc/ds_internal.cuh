@@ -283,6 +283,13 @@ cudaError_t launch_core_gather(const uint32_t* bits, int64_t stride_n, const int
 cudaError_t launch_closure(uint32_t* C, int64_t m, int64_t stride, uint32_t* dplus, uint32_t* W,
                            cudaStream_t s);
 
+// ---- float64 serial oracle (ds_serial.cu) ---------------------------------------
+// dense MSB-first neighbourhood words (n x stride) and int32 counts of the float64
+// direct formula (oracle.py:58-79); soa: n x d doubles of workspace
+cudaError_t launch_serial_words(const double* coords, int64_t n, int d, double eps_sq,
+                                double* soa, uint32_t* bits, int64_t stride, int32_t* cnt,
+                                cudaStream_t s);
+
 // ---- materialising ladder (ds_dist.cu) -----------------------------------------
 int64_t dist_pitch(int64_t n);  // floats per device matrix row (roundup4(n))
 // rows [row0, row0 + rows) of the direct-formula n x n matrix into out (pitch floats)
