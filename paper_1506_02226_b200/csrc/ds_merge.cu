@@ -211,13 +211,12 @@ __device__ __forceinline__ uint2 item_word(const ItemWords& iw, const uint2* __r
   return words[iw.base[lo] + (k - iw.pre[lo])];
 }
 
-__device__ __forceinline__ int find_local(int* lp, int v) {
+// read-only find: the only concurrent writes are unite_local's atomicCAS hooks
+__device__ __forceinline__ int find_local(const int* lp, int v) {
   int p = lp[v];
   while (p != v) {
-    const int gp = lp[p];
-    if (gp != p) lp[v] = gp;  // halving (smem; benign race)
     v = p;
-    p = gp;
+    p = lp[v];
   }
   return v;
 }
@@ -334,6 +333,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       lb[v] = NONE;
       hist[v] = 0;
     }
+    if (tid == 0) slot_root[0] = -1;  // atomicMax target of the single-root fast path
     __syncthreads();
     // scatter the tile pair's words into the dense matrix (core rows, core columns
     // only), one warp per chunk entry; non-core rows give their own border candidate
@@ -399,7 +399,9 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       while (fresh) {
         const int t = __clz(fresh);
         fresh &= ~(0x80000000u >> t);
-        lp[w * 32 + t] = u;  // u <= column: parent pointers decrease
+        // u <= column: parent pointers decrease; several row blocks may hit the same
+        // column, the smallest row wins (deterministic, no write-write race)
+        atomicMin(&lp[w * 32 + t], u);
       }
     }
     __syncthreads();
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       const bool root0 = core0 && lp[tid] == tid;
       const uint32_t rb0 = __ballot_sync(0xffffffffu, root0);
       if ((tid & 31) == 0) wroots[tid >> 5] = __popc(rb0);
-      if (root0) slot_root[0] = tid;  // read only when it is the single root
+      if (root0) atomicMax(&slot_root[0], tid);  // read only when it is the single root
       __syncthreads();
       int nroots = 0;
 #pragma unroll
@@ -433,14 +435,13 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       }
       __syncthreads();  // wroots / slot_root are rewritten below
     }
-    // pointer jumping over the min-neighbour forest, in place (a node may read a
-    // pointer another thread already advanced: every value is still an ancestor, so
-    // it only jumps further), until no pointer moves; forests are shallow, and 9
-    // synchronous halvings would cover 512 nodes
+    // synchronous pointer jumping over the min-neighbour forest (every node reads its
+    // grandparent, barrier, writes it) until no pointer moves: 9 rounds cover 512 nodes
 #pragma unroll 1
     for (int r = 0; r < TILE; ++r) {
       const int cur = lp[tid];
       const int nv = lp[cur];
+      __syncthreads();
       if (nv != cur) lp[tid] = nv;
       if (!__syncthreads_or(nv != cur)) break;
     }
