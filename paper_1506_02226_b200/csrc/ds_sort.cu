@@ -12,12 +12,21 @@
 // Keys: up to 4 leading dimensions quantised to a 2^(b/k)-per-dimension grid over
 // the global bounding box (reduced by the prep kernel), b = 16 bits (two radix passes)
 // for 1-2-D inputs up to 2^18 points and 24 bits otherwise — far finer than a
-// 512-point tile. The sort is CUB's stable LSD radix sort on (32-bit key, original
-// index), so the permutation is deterministic and identical on every rank.
+// 512-point tile. The sort is a hand-written stable LSD radix sort over 8-bit digits
+// on (key, original index) — ties keep index order — so the permutation is
+// deterministic and identical on every rank:
+//   morton_kernel   keys of one 2048-point chunk per CTA + the chunk's digit
+//                   histogram of pass 0 (shared-memory atomics, written per chunk) +
+//                   the global digit totals of every pass (order-independent);
+//   digit_scan      one CTA per digit: exclusive scan over the chunks of that digit's
+//                   per-chunk counts, plus the digit's base (sum of smaller digits);
+//   radix_scatter   one CTA per chunk of the pass's input order: stable rank of each
+//                   item among equal digits (warp match_any + per-warp counts in
+//                   shared memory, 8 rounds of 256 items in index order), written to
+//                   base + rank; it also counts the next pass's digits per output
+//                   chunk (global atomics) and, on the last pass, writes perm / inv.
 #include <cuda_runtime.h>
 #include <stdint.h>
-
-#include <cub/cub.cuh>
 
 #include "ds_internal.cuh"
 
@@ -36,40 +45,175 @@ __device__ __forceinline__ float unord(unsigned int u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-__global__ void morton_kernel(const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits,
-                              const unsigned int* __restrict__ lo_bits,
-                              const unsigned int* __restrict__ hi_bits,
-                              uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+constexpr int RS_T = 256;               // threads per radix CTA
+constexpr int RS_ITEMS = 8;             // items per thread
+constexpr int RS_CHUNK = RS_T * RS_ITEMS;  // 2048 items per chunk
+constexpr int RS_MAXP = 3;              // passes (24-bit keys)
+
+__host__ __device__ inline int64_t rs_chunks(int64_t n) { return (n + RS_CHUNK - 1) / RS_CHUNK; }
+
+// Keys of chunk c (items c*CHUNK + r*256 + t) and the chunk's pass-0 digit counts
+// (counts0[d * nch + c]); the digit totals of all passes go to totals[p * 256 + d]
+// (zeroed per call); the per-chunk counts of passes >= 1 are zeroed here (their
+// radix_scatter adds to them once this kernel has completed).
+__global__ void __launch_bounds__(RS_T) morton_kernel(
+    const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits, int npass,
+    const unsigned int* __restrict__ lo_bits, const unsigned int* __restrict__ hi_bits,
+    uint32_t* __restrict__ keys, int32_t* __restrict__ counts, int32_t* __restrict__ totals) {
   griddep_wait();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  __shared__ int hist[RS_MAXP][256];
+  const int t = threadIdx.x;
+  const int64_t nch = rs_chunks(n);
+  const int64_t c = blockIdx.x;
+  for (int p = 0; p < RS_MAXP; ++p) hist[p][t] = 0;
+  __syncthreads();
   const int bits = total_bits / kd;
   const double levels = (double)((1ull << bits) - 1);
-  uint32_t q[4] = {0, 0, 0, 0};
+  double lo[4], span[4];
   for (int k = 0; k < kd; ++k) {
-    const double lo = unord(~lo_bits[k]), hi = unord(hi_bits[k]);  // lo is stored inverted
-    const double span = hi - lo;
-    double t = span > 0 ? ((double)rec[i * S + k] - lo) / span * levels : 0.0;
-    t = t < 0 ? 0 : (t > levels ? levels : t);  // NaN -> 0 via the comparisons below
-    q[k] = (t == t) ? (uint32_t)t : 0u;
+    lo[k] = unord(~lo_bits[k]);  // lo is stored inverted
+    span[k] = (double)unord(hi_bits[k]) - lo[k];
   }
-  uint32_t key = 0;  // <= 24 bits
-  for (int b = bits - 1; b >= 0; --b)
-    for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
-  keys[i] = key;
-  idx[i] = (int32_t)i;
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const int64_t i = c * RS_CHUNK + r * RS_T + t;
+    if (i >= n) break;
+    uint32_t q[4] = {0, 0, 0, 0};
+    for (int k = 0; k < kd; ++k) {
+      double v = span[k] > 0 ? ((double)rec[i * S + k] - lo[k]) / span[k] * levels : 0.0;
+      v = v < 0 ? 0 : (v > levels ? levels : v);
+      q[k] = (v == v) ? (uint32_t)v : 0u;  // NaN -> 0
+    }
+    uint32_t key = 0;  // <= 24 bits
+    for (int b = bits - 1; b >= 0; --b)
+      for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
+    keys[i] = key;
+    for (int p = 0; p < npass; ++p) atomicAdd(&hist[p][(key >> (8 * p)) & 255u], 1);
+  }
+  __syncthreads();
+  const int64_t stride = 256 * nch;  // counts of one pass
+  counts[(int64_t)t * nch + c] = hist[0][t];
+  for (int p = 1; p < npass; ++p) counts[p * stride + (int64_t)t * nch + c] = 0;
+  for (int p = 0; p < npass; ++p)
+    if (hist[p][t]) atomicAdd(&totals[p * 256 + t], hist[p][t]);
+}
+
+// One CTA per digit d: offs[d * nch + c] = sum of totals of digits < d + sum of the
+// digit's counts of chunks < c (exclusive scan over the chunks, in place).
+__global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ counts,
+                                                          const int32_t* __restrict__ totals,
+                                                          int64_t nch) {
+  griddep_wait();
+  __shared__ int warp_sum[RS_T / 32];
+  __shared__ int carry_sh;
+  const int d = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // base = sum of the totals of the smaller digits
+  int v = t < d ? totals[t] : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) warp_sum[warp] = v;
+  __syncthreads();
+  if (t == 0) {
+    int b = 0;
+    for (int w = 0; w < RS_T / 32; ++w) b += warp_sum[w];
+    carry_sh = b;
+  }
+  __syncthreads();
+  int carry = carry_sh;
+  int32_t* row = counts + (int64_t)d * nch;
+  for (int64_t base = 0; base < nch; base += RS_T) {
+    const int64_t c = base + t;
+    const int x = c < nch ? row[c] : 0;
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    __syncthreads();  // warp_sum of the previous round is consumed
+    if (lane == 31) warp_sum[warp] = inc;
+    __syncthreads();
+    int wpre = 0, all = 0;
+    for (int w = 0; w < RS_T / 32; ++w) {
+      const int ws = warp_sum[w];
+      if (w < warp) wpre += ws;
+      all += ws;
+    }
+    if (c < nch) row[c] = carry + wpre + inc - x;
+    carry += all;
+  }
+}
+
+// Stable scatter of one pass: chunk c of the input order (keys_in / vals_in, vals
+// implicit = index on pass 0). Items are ranked in index order; on the last pass the
+// permutation goes to perm / inv, otherwise keys / values to the output arrays and the
+// next pass's digit is counted for the output chunk.
+__global__ void __launch_bounds__(RS_T) radix_scatter_kernel(
+    int64_t n, int shift, const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
+    const int32_t* __restrict__ offs, uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
+    int32_t* __restrict__ next_counts, int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+  griddep_wait();
+  __shared__ int base[256];
+  __shared__ int wcnt[2][RS_T / 32][256];  // double-buffered over the rounds
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t nch = rs_chunks(n);
+  const int64_t c = blockIdx.x;
+  base[t] = offs[(int64_t)t * nch + c];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const int64_t i = c * RS_CHUNK + r * RS_T + t;
+    const bool valid = i < n;
+    uint32_t key = 0;
+    int32_t val = 0;
+    if (valid) {
+      key = keys_in[i];
+      val = vals_in ? vals_in[i] : (int32_t)i;
+    }
+    const int dig = valid ? (int)((key >> shift) & 255u) : 256;
+    // buffer r & 1 was last read two rounds ago: the barriers of round r - 1 separate
+    // those reads from this zeroing
+    int(*wc)[256] = wcnt[r & 1];
+#pragma unroll
+    for (int w = 0; w < RS_T / 32; ++w) wc[w][t] = 0;
+    __syncthreads();  // also orders base[] (round 0)
+    const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+    const int lrank = __popc(peers & lt);
+    if (valid && lrank == 0) wc[warp][dig] = __popc(peers);
+    __syncthreads();
+    {  // per digit: exclusive prefix over the warps, then advance the digit's base
+      int run = base[t];
+#pragma unroll
+      for (int w = 0; w < RS_T / 32; ++w) {
+        const int x = wc[w][t];
+        wc[w][t] = run;
+        run += x;
+      }
+      base[t] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      const int64_t pos = (int64_t)wc[warp][dig] + lrank;
+      if (perm) {
+        perm[pos] = val;
+        inv[val] = (int32_t)pos;
+      } else {
+        keys_out[pos] = key;
+        vals_out[pos] = val;
+        if (next_counts)
+          atomicAdd(&next_counts[(int64_t)((key >> (shift + 8)) & 255u) * nch + pos / RS_CHUNK], 1);
+      }
+    }
+  }
 }
 
 __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
-                               const int32_t* __restrict__ perm, float* __restrict__ out,
-                               int32_t* __restrict__ inv) {
+                               const int32_t* __restrict__ perm, float* __restrict__ out) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t o = perm[s];
   const float4* src = reinterpret_cast<const float4*>(rec + o * S);
   float4* dst = reinterpret_cast<float4*>(out + s * S);
   for (int v = 0; v < S / 4; ++v) dst[v] = src[v];
-  inv[o] = (int32_t)s;
 }
 
 // permute_kernel fused with the culling bounds (stage 1+2 with culling on): one CTA
@@ -79,7 +223,7 @@ __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
 // norm (lo / hi / maxnorm, the layout of tile_bounds_kernel).
 __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
     const float* __restrict__ rec, int64_t n, int S, int dpad, const int32_t* __restrict__ perm,
-    float* __restrict__ out, int32_t* __restrict__ inv, float* __restrict__ lo,
+    float* __restrict__ out, float* __restrict__ lo,
     float* __restrict__ hi, float* __restrict__ maxnorm, float* __restrict__ blk) {
   griddep_wait();
   __shared__ float smn[TILE / 32], smx[TILE / 32];
@@ -92,7 +236,6 @@ __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
     const float4* src = reinterpret_cast<const float4*>(rec + o * S);
     float4* dst = reinterpret_cast<float4*>(out + s * S);
     for (int v = 0; v < S / 4; ++v) dst[v] = src[v];
-    inv[o] = (int32_t)s;
   }
   const int64_t wb = tile * (TILE / 32) + warp;  // global 32-point block
   const bool wvalid = wb * 32 < n;
@@ -137,10 +280,7 @@ __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
 }  // namespace
 
 size_t sort_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
-  return bytes;
+  return (size_t)RS_MAXP * 256 * rs_chunks(n) * 4;  // per-pass per-chunk digit counts
 }
 
 cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
@@ -151,23 +291,50 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   const int dp = padded_dim(d);
   const int S = rec_stride(d);
   const int kd = d < 4 ? d : 4;
-  // the bounding box was reduced by the prep kernel (launch_prep with a bbox buffer)
-  const unsigned blocks = (unsigned)((n + 255) / 256);
+  // the bounding box was reduced by the prep kernel (launch_prep with a bbox buffer);
+  // the digit totals follow it in the per-call zero region
   const int kb = key_bits(n, kd);
-  uint32_t* k32 = reinterpret_cast<uint32_t*>(keys);
-  uint32_t* k32_alt = reinterpret_cast<uint32_t*>(keys_alt);
-  cudaError_t e = launch_pdl(morton_kernel, dim3(blocks), dim3(256), 0, s, rec, n, S, kd, kb,
-                             (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), k32, idx);
+  const int end_bit = (kb / kd) * kd;
+  const int npass = (end_bit + 7) / 8;
+  const int64_t nch = rs_chunks(n);
+  if (temp_bytes < sort_temp_bytes(n)) return cudaErrorInvalidValue;
+  int32_t* counts = reinterpret_cast<int32_t*>(temp);
+  int32_t* totals = reinterpret_cast<int32_t*>(bbox + 64);
+  // ping-pong: keys A / B in the two halves of `keys`, values in idx / keys_alt
+  uint32_t* kA = reinterpret_cast<uint32_t*>(keys);
+  uint32_t* kB = kA + n;
+  int32_t* vA = idx;
+  int32_t* vB = reinterpret_cast<int32_t*>(keys_alt);
+  cudaError_t e = launch_pdl(morton_kernel, dim3((unsigned)nch), dim3(RS_T), 0, s, rec, n, S, kd, kb,
+                             npass, (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA,
+                             counts, totals);
   if (e != cudaSuccess) return e;
-  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k32, k32_alt, idx, perm,
-                                                  (int)n, 0, (kb / kd) * kd, s);
-  if (e != cudaSuccess) return e;
+  const uint32_t* kin = kA;
+  const int32_t* vin = nullptr;
+  for (int p = 0; p < npass; ++p) {
+    int32_t* cp = counts + (int64_t)p * 256 * nch;
+    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp,
+                   (const int32_t*)(totals + p * 256), nch);
+    if (e != cudaSuccess) return e;
+    const bool last = p == npass - 1;
+    uint32_t* kout = (p & 1) ? kA : kB;
+    int32_t* vout = (p & 1) ? vA : vB;
+    e = launch_pdl(radix_scatter_kernel, dim3((unsigned)nch), dim3(RS_T), 0, s, n, 8 * p, kin, vin,
+                   (const int32_t*)cp, last ? (uint32_t*)nullptr : kout,
+                   last ? (int32_t*)nullptr : vout,
+                   last ? (int32_t*)nullptr : counts + (int64_t)(p + 1) * 256 * nch,
+                   last ? perm : (int32_t*)nullptr, last ? inv : (int32_t*)nullptr);
+    if (e != cudaSuccess) return e;
+    kin = kout;
+    vin = vout;
+  }
   if (bnd.lo) {
     e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(TILE), 0, s, rec, n, S, dp,
-                   (const int32_t*)perm, rec_sorted, inv, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk);
+                   (const int32_t*)perm, rec_sorted, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk);
     if (e != cudaSuccess) return e;
   } else {
-    permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted, inv);
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    permute_kernel<<<blocks, 256, 0, s>>>(rec, n, S, perm, rec_sorted);
   }
   return cudaGetLastError();
 }

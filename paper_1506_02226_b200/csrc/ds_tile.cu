@@ -213,7 +213,11 @@ struct Geo {
 #endif
   static constexpr int UNROLL = D <= 4 ? 32 : DS_UNROLL_WIDE;
   // resident CTAs (x 4 warps) per SM: 16-D holds 4 lane points x 17 floats per lane
-  static constexpr int MINB = (D <= 8 || D == 32) ? 4 : (D == 16 ? DS_MINB16 : 3);
+#ifndef DS_MINB_SMALL
+#define DS_MINB_SMALL 4
+#endif
+  static constexpr int MINB = D <= 4 ? DS_MINB_SMALL
+                                     : ((D <= 8 || D == 32) ? 4 : (D == 16 ? DS_MINB16 : 3));
 };
 
 // Column-side counts of one unit: the number of set bits of every column over the

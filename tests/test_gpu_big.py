@@ -138,3 +138,24 @@ def test_capacity_cap_still_raises(ds):
             ctx.run_dbscan(pts.coords_aos, params.eps_sq, 4, 1, 12_000_000)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("name,pairs,tiles", [("C2", 211_812_352, 3823)])
+def test_spatial_sort_is_the_stable_key_order(ds, name, pairs, tiles):
+    """The hand-written LSD radix sort (ds_sort.cu) must give the stable (key, index)
+    order — the one round 1's library sort produced: the work counters of the culled
+    schedule depend on the exact permutation, so they must equal round 1's numbers, on
+    two independent contexts and on repeated calls."""
+    cfg = ds.CONFIGS[name]
+    pts = cfg.points()
+    params = ds.validate_params(cfg.eps, cfg.min_pts)
+    seen = set()
+    for _ in range(2):
+        ctx = ds._native.Context(0)
+        try:
+            for _ in range(2):
+                _, _, t = ctx.run_dbscan(pts.coords_aos, params.eps_sq, cfg.min_pts, 1, MEM_CAP)
+                seen.add((t.pairs_evaluated, t.tiles_total))
+        finally:
+            ctx.close()
+    assert seen == {(pairs, tiles)}
