@@ -67,8 +67,7 @@ struct Scalars {
 constexpr size_t ZR_ALIGN = 256;
 inline size_t zr_round(size_t b) { return (b + ZR_ALIGN - 1) / ZR_ALIGN * ZR_ALIGN; }
 inline size_t zr_bbox() { return zr_round(sizeof(Scalars)); }
-// bbox: 8 uints at +0, the spatial sort's digit totals (3 x 256 ints) at +256 bytes
-inline size_t zr_diag() { return zr_bbox() + 16 * ZR_ALIGN; }
+inline size_t zr_diag() { return zr_bbox() + ZR_ALIGN; }
 inline size_t zr_scan(int64_t n) { return zr_diag() + zr_round((size_t)n_tiles(n) * 8); }
 // the tile-root link table of union_links (one CAS slot per linked pair of tile roots)
 inline int link_tab_bits(int64_t n) {

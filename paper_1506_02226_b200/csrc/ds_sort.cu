@@ -15,14 +15,14 @@
 // 512-point tile. The sort is a hand-written stable LSD radix sort over 8-bit digits
 // on (key, original index) — ties keep index order — so the permutation is
 // deterministic and identical on every rank:
-//   morton_kernel   keys of one 2048-point chunk per CTA + the chunk's digit
-//                   histogram of pass 0 (shared-memory atomics, written per chunk) +
-//                   the global digit totals of every pass (order-independent);
+//   morton_kernel   keys of one chunk of points per CTA + the chunk's digit
+//                   histogram of pass 0 (shared-memory atomics, written per chunk);
 //   digit_scan      one CTA per digit: exclusive scan over the chunks of that digit's
-//                   per-chunk counts, plus the digit's base (sum of smaller digits);
-//   radix_scatter   one CTA per chunk of the pass's input order: stable rank of each
+//                   per-chunk counts, and the digit's total;
+//   radix_scatter   one CTA per chunk of the pass's input order: digit bases (scan of
+//                   the 256 totals), stable rank of each
 //                   item among equal digits (warp match_any + per-warp counts in
-//                   shared memory, 8 rounds of 256 items in index order), written to
+//                   shared memory, rounds of 256 items in index order), written to
 //                   base + rank; it also counts the next pass's digits per output
 //                   chunk (global atomics) and, on the last pass, writes perm / inv.
 #include <cuda_runtime.h>
@@ -46,26 +46,28 @@ __device__ __forceinline__ float unord(unsigned int u) {
 }
 
 constexpr int RS_T = 256;               // threads per radix CTA
-constexpr int RS_ITEMS = 8;             // items per thread
-constexpr int RS_CHUNK = RS_T * RS_ITEMS;  // 2048 items per chunk
+#ifndef DS_RS_ITEMS
+#define DS_RS_ITEMS 2
+#endif
+constexpr int RS_ITEMS = DS_RS_ITEMS;   // items per thread
+constexpr int RS_CHUNK = RS_T * RS_ITEMS;  // items per chunk (one CTA)
 constexpr int RS_MAXP = 3;              // passes (24-bit keys)
 
 __host__ __device__ inline int64_t rs_chunks(int64_t n) { return (n + RS_CHUNK - 1) / RS_CHUNK; }
 
 // Keys of chunk c (items c*CHUNK + r*256 + t) and the chunk's pass-0 digit counts
-// (counts0[d * nch + c]); the digit totals of all passes go to totals[p * 256 + d]
-// (zeroed per call); the per-chunk counts of passes >= 1 are zeroed here (their
-// radix_scatter adds to them once this kernel has completed).
+// (counts0[d * nch + c]); the per-chunk counts of passes >= 1 are zeroed here (the
+// previous pass's radix_scatter adds to them once this kernel has completed).
 __global__ void __launch_bounds__(RS_T) morton_kernel(
     const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits, int npass,
     const unsigned int* __restrict__ lo_bits, const unsigned int* __restrict__ hi_bits,
-    uint32_t* __restrict__ keys, int32_t* __restrict__ counts, int32_t* __restrict__ totals) {
+    uint32_t* __restrict__ keys, int32_t* __restrict__ counts) {
   griddep_wait();
-  __shared__ int hist[RS_MAXP][256];
+  __shared__ int hist[1][256];
   const int t = threadIdx.x;
   const int64_t nch = rs_chunks(n);
   const int64_t c = blockIdx.x;
-  for (int p = 0; p < RS_MAXP; ++p) hist[p][t] = 0;
+  hist[0][t] = 0;
   __syncthreads();
   const int bits = total_bits / kd;
   const double levels = (double)((1ull << bits) - 1);
@@ -88,38 +90,23 @@ __global__ void __launch_bounds__(RS_T) morton_kernel(
     for (int b = bits - 1; b >= 0; --b)
       for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
     keys[i] = key;
-    for (int p = 0; p < npass; ++p) atomicAdd(&hist[p][(key >> (8 * p)) & 255u], 1);
+    atomicAdd(&hist[0][key & 255u], 1);
   }
   __syncthreads();
   const int64_t stride = 256 * nch;  // counts of one pass
   counts[(int64_t)t * nch + c] = hist[0][t];
   for (int p = 1; p < npass; ++p) counts[p * stride + (int64_t)t * nch + c] = 0;
-  for (int p = 0; p < npass; ++p)
-    if (hist[p][t]) atomicAdd(&totals[p * 256 + t], hist[p][t]);
 }
 
-// One CTA per digit d: offs[d * nch + c] = sum of totals of digits < d + sum of the
-// digit's counts of chunks < c (exclusive scan over the chunks, in place).
+// One CTA per digit d: exclusive scan over the chunks of the digit's counts (in
+// place) and the digit's total (totals[d]); the scatter adds the digit bases.
 __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ counts,
-                                                          const int32_t* __restrict__ totals,
+                                                          int32_t* __restrict__ totals,
                                                           int64_t nch) {
   griddep_wait();
   __shared__ int warp_sum[RS_T / 32];
-  __shared__ int carry_sh;
   const int d = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  // base = sum of the totals of the smaller digits
-  int v = t < d ? totals[t] : 0;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) warp_sum[warp] = v;
-  __syncthreads();
-  if (t == 0) {
-    int b = 0;
-    for (int w = 0; w < RS_T / 32; ++w) b += warp_sum[w];
-    carry_sh = b;
-  }
-  __syncthreads();
-  int carry = carry_sh;
+  int carry = 0;
   int32_t* row = counts + (int64_t)d * nch;
   for (int64_t base = 0; base < nch; base += RS_T) {
     const int64_t c = base + t;
@@ -130,10 +117,10 @@ __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ 
       const int y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
-    __syncthreads();  // warp_sum of the previous round is consumed
     if (lane == 31) warp_sum[warp] = inc;
     __syncthreads();
     int wpre = 0, all = 0;
+#pragma unroll
     for (int w = 0; w < RS_T / 32; ++w) {
       const int ws = warp_sum[w];
       if (w < warp) wpre += ws;
@@ -141,7 +128,9 @@ __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ 
     }
     if (c < nch) row[c] = carry + wpre + inc - x;
     carry += all;
+    __syncthreads();  // warp_sum is rewritten by the next round
   }
+  if (t == 0) totals[d] = carry;
 }
 
 // Stable scatter of one pass: chunk c of the input order (keys_in / vals_in, vals
@@ -151,14 +140,31 @@ __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ 
 __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(
     int64_t n, int shift, const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
     const int32_t* __restrict__ offs, uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
-    int32_t* __restrict__ next_counts, int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+    int32_t* __restrict__ next_counts, int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+    const int32_t* __restrict__ totals) {
   griddep_wait();
   __shared__ int base[256];
+  __shared__ int wsum[RS_T / 32];
   __shared__ int wcnt[2][RS_T / 32][256];  // double-buffered over the rounds
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t nch = rs_chunks(n);
   const int64_t c = blockIdx.x;
-  base[t] = offs[(int64_t)t * nch + c];
+  {  // digit base = exclusive scan of the digit totals, plus this chunk's offset
+    const int x = totals[t];
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int wpre = 0;
+#pragma unroll
+    for (int w = 0; w < RS_T / 32; ++w)
+      if (w < warp) wpre += wsum[w];
+    base[t] = wpre + inc - x + offs[(int64_t)t * nch + c];
+  }
   const uint32_t lt = (1u << lane) - 1u;
   for (int r = 0; r < RS_ITEMS; ++r) {
     const int64_t i = c * RS_CHUNK + r * RS_T + t;
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
 }  // namespace
 
 size_t sort_temp_bytes(int64_t n) {
-  return (size_t)RS_MAXP * 256 * rs_chunks(n) * 4;  // per-pass per-chunk digit counts
+  return ((size_t)RS_MAXP * 256 * rs_chunks(n) + RS_MAXP * 256) * 4;  // counts + totals
 }
 
 cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
@@ -291,15 +297,14 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   const int dp = padded_dim(d);
   const int S = rec_stride(d);
   const int kd = d < 4 ? d : 4;
-  // the bounding box was reduced by the prep kernel (launch_prep with a bbox buffer);
-  // the digit totals follow it in the per-call zero region
+  // the bounding box was reduced by the prep kernel (launch_prep with a bbox buffer)
   const int kb = key_bits(n, kd);
   const int end_bit = (kb / kd) * kd;
   const int npass = (end_bit + 7) / 8;
   const int64_t nch = rs_chunks(n);
   if (temp_bytes < sort_temp_bytes(n)) return cudaErrorInvalidValue;
   int32_t* counts = reinterpret_cast<int32_t*>(temp);
-  int32_t* totals = reinterpret_cast<int32_t*>(bbox + 64);
+  int32_t* totals = counts + (int64_t)RS_MAXP * 256 * nch;  // per pass, written by the scans
   // ping-pong: keys A / B in the two halves of `keys`, values in idx / keys_alt
   uint32_t* kA = reinterpret_cast<uint32_t*>(keys);
   uint32_t* kB = kA + n;
@@ -307,14 +312,13 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   int32_t* vB = reinterpret_cast<int32_t*>(keys_alt);
   cudaError_t e = launch_pdl(morton_kernel, dim3((unsigned)nch), dim3(RS_T), 0, s, rec, n, S, kd, kb,
                              npass, (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA,
-                             counts, totals);
+                             counts);
   if (e != cudaSuccess) return e;
   const uint32_t* kin = kA;
   const int32_t* vin = nullptr;
   for (int p = 0; p < npass; ++p) {
     int32_t* cp = counts + (int64_t)p * 256 * nch;
-    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp,
-                   (const int32_t*)(totals + p * 256), nch);
+    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp, totals + p * 256, nch);
     if (e != cudaSuccess) return e;
     const bool last = p == npass - 1;
     uint32_t* kout = (p & 1) ? kA : kB;
@@ -323,7 +327,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
                    (const int32_t*)cp, last ? (uint32_t*)nullptr : kout,
                    last ? (int32_t*)nullptr : vout,
                    last ? (int32_t*)nullptr : counts + (int64_t)(p + 1) * 256 * nch,
-                   last ? perm : (int32_t*)nullptr, last ? inv : (int32_t*)nullptr);
+                   last ? perm : (int32_t*)nullptr, last ? inv : (int32_t*)nullptr,
+                   (const int32_t*)(totals + p * 256));
     if (e != cudaSuccess) return e;
     kin = kout;
     vin = vout;
