@@ -555,13 +555,14 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
       }
       base = wpos;
       wpos += (unsigned long long)total;
-      unsigned long long pos = base + (unsigned long long)excl;
+      if (base + (unsigned long long)total <= A.words_cap) {  // else dropped: the host re-runs
+        uint2* dst = A.words + base + excl;
+        const uint32_t tag = ((uint32_t)((llb * 32 + lane) * KP) << 4) | (uint32_t)cur.jw;
+        int o = 0;
 #pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        if (w[k]) {
-          if (pos < A.words_cap)
-            A.words[pos] = make_uint2(w[k], (uint32_t)(((llb * 32 + lane) * KP + k) << 4 | cur.jw));
-          ++pos;
+        for (int k = 0; k < KP; ++k) {
+          if (w[k]) dst[o] = make_uint2(w[k], tag + ((uint32_t)k << 4));
+          o += w[k] ? 1 : 0;
         }
       }
     }
