@@ -808,11 +808,12 @@ __global__ void union_dense_kernel(const uint32_t* __restrict__ bits32, int64_t 
 __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __restrict__ parent,
                              const int32_t* __restrict__ bmin, int64_t n,
                              const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
-                             int32_t* __restrict__ root, int32_t* cmin) {
+                             int32_t* __restrict__ root, int32_t* cmin, int32_t* cid) {
   griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int r = -1, o = NONE;
   if (i < n) {
+    cid[i] = -1;  // cluster ids (indexed by root), written by scan_label_kernel
     if (core[i]) {
       r = find_root_ro(parent, (int)i);
     } else {
@@ -872,18 +873,6 @@ struct ScanInPlace {
   const int32_t* data;
   __device__ __forceinline__ int operator()(int64_t i) const { return data[i]; }
 };
-// scan input for canonical ids: 1 iff original index o is the first appearance
-// (lowest ORIGINAL member) of its cluster (core.py:116-132)
-struct ScanFirstAppearance {
-  const int32_t* root;  // sorted order
-  const int32_t* cmin;
-  const int32_t* inv;   // original -> sorted (nullptr: identity)
-  __device__ __forceinline__ int operator()(int64_t o) const {
-    const int r = root[inv ? inv[o] : o];
-    return (r >= 0 && cmin[r] == (int)o) ? 1 : 0;
-  }
-};
-
 template <class In>
 __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* data, int64_t n,
                                                                unsigned int* ticket,
@@ -948,15 +937,94 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* d
   }
 }
 
-__global__ void label_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
-                             const int32_t* __restrict__ id, int64_t n,
-                             const int32_t* __restrict__ perm, int64_t* __restrict__ labels,
-                             unsigned long long* stamps, unsigned int* done) {
+// Canonical labels in one pass over ORIGINAL indices o (decoupled look-back, tiles in
+// ticket order): flag(o) = 1 iff o is the first appearance (lowest original member) of
+// its cluster; the exclusive scan of the flags at o is that cluster's id. Each tile,
+// once its prefix is known, publishes the ids of the clusters that first appear in it
+// (cid[root]); then every o reads cid[root(o)]. A cluster's first appearance is never
+// after any of its members (cmin <= o), so it is in this tile or an earlier one — an
+// earlier tile got its ticket first and publishes its ids right after its own
+// look-back, so the wait below is short and cannot deadlock. Labels are written in
+// original order (coalesced int64 stores). Replaces scan_lookback + label_kernel.
+__global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
+    const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
+    const int32_t* __restrict__ inv, int32_t* cid, int64_t n, unsigned int* ticket,
+    unsigned long long* state, int32_t* total, int64_t* __restrict__ labels,
+    unsigned long long* stamps, unsigned int* done) {
   griddep_wait();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int r = root[i];
-    labels[perm ? perm[i] : i] = r >= 0 ? (int64_t)id[cmin[r]] : (int64_t)-1;
+  __shared__ unsigned int tile_sh;
+  __shared__ int prefix_sh;
+  if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const unsigned int tile = tile_sh;
+  const int64_t base = (int64_t)tile * SCAN_BLK + (int64_t)threadIdx.x * SCAN_PER;
+  int r[SCAN_PER];
+  int f[SCAN_PER];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t o = base + k;
+    r[k] = o < n ? root[inv ? inv[o] : o] : -1;
+    f[k] = (r[k] >= 0 && cmin[r[k]] == (int)o) ? 1 : 0;
+    sum += f[k];
+  }
+  int agg;
+  const int excl = block_exclusive_scan(sum, agg);
+  if (threadIdx.x < 32) {  // warp 0: publish the aggregate, look back 32 tiles at a time
+    const int lane = threadIdx.x;
+    volatile unsigned long long* st = state;
+    int prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st[0] = SC_PRE | (unsigned int)agg;
+    } else {
+      if (lane == 0) st[tile] = SC_AGG | (unsigned int)agg;
+      int64_t hi = (int64_t)tile - 1;
+      for (;;) {
+        const int64_t j = hi - lane;
+        const unsigned long long w = j >= 0 ? st[j] : (2ull << 62);
+        const unsigned flag = (unsigned)(w >> 62);
+        const unsigned pre = __ballot_sync(0xffffffffu, flag == 2u);
+        const int stop = pre ? __ffs(pre) - 1 : 31;
+        const unsigned need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+        if (__ballot_sync(0xffffffffu, flag == 0u) & need) continue;  // not published yet
+        int v = lane <= stop ? (int)(unsigned int)w : 0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        prefix += v;
+        if (pre) break;
+        hi -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        st[tile] = SC_PRE | (unsigned int)(prefix + agg);
+      }
+    }
+    if (lane == 0) {
+      prefix_sh = prefix;
+      if ((int64_t)(tile + 1) * SCAN_BLK >= n) *total = prefix + agg;  // last tile
+    }
+  }
+  __syncthreads();
+  int run = prefix_sh + excl;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    if (f[k]) cid[r[k]] = run;
+    run += f[k];
+  }
+  __threadfence();
+  __syncthreads();
+  const volatile int32_t* vc = cid;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t o = base + k;
+    if (o >= n) continue;
+    int64_t lab = -1;
+    if (r[k] >= 0) {
+      int v = vc[r[k]];
+      while (v < 0) v = vc[r[k]];  // published by an earlier tile (see above)
+      lab = v;
+    }
+    labels[o] = lab;
   }
   if (stamps) {  // the last block to finish stamps the end of stage 3
     __syncthreads();
@@ -1117,16 +1185,14 @@ cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
                                 : cudaMemsetAsync(state, 0, (size_t)(tiles + 1) * 8, s);
   if (e != cudaSuccess) return e;
   e = launch_pdl(roots_kernel, dim3(b), dim3(t), 0, s, (const uint8_t*)w.core,
-                 (const int32_t*)w.parent, (const int32_t*)w.bmin, w.n, w.perm, w.inv, w.root, w.cmin);
+                 (const int32_t*)w.parent, (const int32_t*)w.bmin, w.n, w.perm, w.inv, w.root, w.cmin,
+                 w.flag);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(scan_lookback_kernel<ScanFirstAppearance>, dim3((unsigned)tiles), dim3(SCAN_T), 0, s,
-                 ScanFirstAppearance{w.root, w.cmin, w.inv}, w.flag, w.n,
-                 reinterpret_cast<unsigned int*>(state),
-                 reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(label_kernel, dim3(b), dim3(t), 0, s, (const int32_t*)w.root,
-                    (const int32_t*)w.cmin, (const int32_t*)w.flag, w.n, w.perm, labels,
-                    w.stamps, w.label_blocks);
+  return launch_pdl(scan_label_kernel, dim3((unsigned)tiles), dim3(SCAN_T), 0, s,
+                    (const int32_t*)w.root, (const int32_t*)w.cmin, w.inv, w.flag, w.n,
+                    reinterpret_cast<unsigned int*>(state),
+                    reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters, labels, w.stamps,
+                    w.label_blocks);
 }
 
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R,
