@@ -214,11 +214,18 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank; DS_DIST_BACKEND=gloo (test hook) lets several ranks share the
+    # device(s) of a smaller box to exercise this path (host-staged exchanges)
+    dist_backend = os.environ.get("DS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(dist_backend)
 
     cfg = ds.CONFIGS[args.config]
     pts = cfg.points()

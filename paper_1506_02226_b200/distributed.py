@@ -122,6 +122,9 @@ def _fold_distributed(backend, parent, group):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     peer_rank = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    # NCCL moves device tensors directly; gloo has no device point-to-point, so its
+    # messages are staged through host memory (CPU tests, several ranks on one GPU)
+    staged = parent.is_cuda and dist.get_backend(group) != "nccl"
     buf = torch.empty_like(parent)
     for rnd in fold_rounds(world):
         for kind, a, b in rnd:
@@ -131,13 +134,17 @@ def _fold_distributed(backend, parent, group):
             ops = []
             sends = kind == "swap" or (rank == a)
             recvs = kind == "swap" or (rank == b)
+            out_t = parent.cpu() if staged else parent
+            in_t = torch.empty_like(out_t) if staged else buf
             if sends:
-                ops.append(dist.P2POp(dist.isend, parent, peer_rank(other), group))
+                ops.append(dist.P2POp(dist.isend, out_t, peer_rank(other), group))
             if recvs:
-                ops.append(dist.P2POp(dist.irecv, buf, peer_rank(other), group))
+                ops.append(dist.P2POp(dist.irecv, in_t, peer_rank(other), group))
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
             if recvs:
+                if staged:
+                    buf.copy_(in_t)
                 if kind == "copy":
                     parent.copy_(buf)
                 else:

@@ -79,3 +79,38 @@ def test_shard_fold_unions_forests(ds, rng):
         dst = np.concatenate([e[1] for e in edges])
         want = oracle.components(n, src, dst)
         assert np.array_equal(got, want)
+
+
+def _two_rank_worker(rank, world, port, out_dir):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1506_02226_b200 as ds
+    from paper_1506_02226_b200.distributed import NativeShardBackend, run_dbscan_sharded
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = ds.CONFIGS["C2"]
+        labels, tm = run_dbscan_sharded(cfg.points(), ds.validate_params(cfg.eps, cfg.min_pts),
+                                        backend=NativeShardBackend(0), return_device=True)
+        np.save(os.path.join(out_dir, f"r{rank}.npy"), labels.cpu().numpy())
+        assert tm.pairs_evaluated > 0
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_sharing_one_gpu_over_gloo(tmp_path, world):
+    """The one-process-per-GPU driver with its real device stages and the pairwise
+    forest fold, `world` ranks on this box's single GPU (gloo collectives, host-staged
+    point-to-point): every rank's labels equal the reference's."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_two_rank_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    g = load_golden("c2.npz")
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"r{r}.npy"), g["labels"]), r
