@@ -384,7 +384,8 @@ def run_b200(args):
         "config": {"workload": f"{cfg.name}: {cfg.description}", "n": n, "d": d,
                    "eps": cfg.eps, "min_pts": cfg.min_pts, "formula": "algebraic",
                    "l2": "flushed (512 MB write) before every timed step",
-                   "parallelism": (f"tile-pair items sharded over {world} GPUs (NCCL)"
+                   "parallelism": (f"tile-pair items sharded over {world} ranks "
+                                   f"({dist_backend}, {torch.cuda.device_count()} visible GPUs)"
                                    if world > 1 else "1 GPU")},
         "e2e": {"value": n / (e2e / 1e3), "unit": "points/s",
                 "h2d_bytes_per_step": n * d * 8 * (world if world > 1 else 1),

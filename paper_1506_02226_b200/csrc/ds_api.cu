@@ -1075,6 +1075,11 @@ ds_status ds_shard_stage3_local(ds_ctx* c, const int32_t* d_counts, int64_t n, i
   DS_CK(launch_permute_i32(d_counts, n, c->sorted ? (const int32_t*)c->perm.p : nullptr, 0,
                            (int32_t*)c->cnt.p, s));
   MergeWs w = merge_ws(c, n);
+  // per-block uniform roots of this shard's diagonal tiles (-1 elsewhere) and the
+  // tile-root link table (zeroed by the stage 1+2 call): union_links' shortcuts
+  w.blk_root = (int32_t*)c->troot.p;
+  w.link_tab = (unsigned long long*)((char*)c->scalars.p + zr_links(n));
+  w.link_mask = (1u << link_tab_bits(n)) - 1u;
   Scalars* sc = (Scalars*)c->scalars.p;
   DS_CK(cudaMemsetAsync(&sc->ncore, 0, sizeof(unsigned long long), s));
   DS_CK(launch_core_init(w, min_pts, s));
