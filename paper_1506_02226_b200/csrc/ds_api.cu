@@ -47,7 +47,7 @@ struct Buf {
   size_t bytes = 0;
 };
 
-struct Scalars {
+struct Scalars {  // a whole number of 8-byte words (the label kernel copies it by words)
   unsigned long long work_ctr;
   unsigned long long words_count;
   unsigned long long nonempty_count;
@@ -61,6 +61,7 @@ struct Scalars {
   unsigned int label_blocks;                // label_kernel blocks finished
   unsigned long long stamps[ST_COUNT];      // device stage boundaries (Stamp)
 };
+static_assert(sizeof(Scalars) % 8 == 0, "Scalars is copied in 8-byte words");
 
 // The per-call zero region: one memset clears the scalars, the spatial-sort bounding
 // box, the diagonal directory index and the label scan's look-back state.
@@ -107,6 +108,7 @@ struct ds_ctx {
   UnitArgs units{};                  // the last eps-tile launch (read by stage 3)
   int unit_lb = 4;                   // its lane blocks per tile
   Scalars* h_scalars = nullptr;      // pinned
+  unsigned long long* h_scalars_dev = nullptr;  // its device (mapped) alias
   // DS_OPT_TEST_CAPACITY (test hook): > 0 forces this initial unit-list and word
   // capacity on the next stage 1+2 and limits every regrow to x2, so one call walks
   // through many grow steps; 0 (default) = normal sizing
@@ -550,13 +552,17 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   w.blk_root = (int32_t*)c->troot.p;
   w.link_tab = (unsigned long long*)((char*)c->scalars.p + zr_links(n));
   w.link_mask = (1u << link_tab_bits(n)) - 1u;
+  // the scalars (final once the label kernel is done) are copied into page-locked
+  // memory by the label kernel's last block: no device-to-host copy node after it
+  w.dev_scalars = (const unsigned long long*)c->scalars.p;
+  w.host_scalars = c->h_scalars_dev;
+  w.scalar_words = (int)(sizeof(Scalars) / 8);
   if (c->event_timing) DS_CK(rec(c->ev[3]));
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
-  // the scalars (final once the label kernel is done) go back before the labels, so
-  // the call ends with the label copy rather than a small copy's latency after it
-  DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  if (!c->h_scalars_dev)
+    DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
   DS_CK(rec(c->ev[4]));
   if (io && io->labels)
     DS_CK(cudaMemcpyAsync(io->labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
@@ -737,7 +743,8 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     } else {  // no split available: the whole device part as stage 1+2
       DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[4]));
     }
-    DS_CK(cudaEventElapsedTime(&o, c->ev[4], c->ev[7]));
+    if (io && (io->labels || io->counts))  // host copies after the label kernel
+      DS_CK(cudaEventElapsedTime(&o, c->ev[4], c->ev[7]));
     t->fused_ms = f;
     t->merge_ms = m;
     t->tile_ms = k;
@@ -786,6 +793,14 @@ ds_status ds_ctx_create(int device, ds_ctx** out) {
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   for (int i = 0; e == cudaSuccess && i < 8; ++i) e = cudaEventCreate(&c->ev[i]);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scalars, sizeof(Scalars));
+  if (e == cudaSuccess) {
+    // device (mapped) alias of the page-locked scalar block: the label kernel's last
+    // block writes it; without one the pipeline copies the scalars with a copy node
+    void* p = nullptr;
+    if (cudaHostGetDevicePointer(&p, c->h_scalars, 0) == cudaSuccess)
+      c->h_scalars_dev = (unsigned long long*)p;
+    cudaGetLastError();
+  }
   if (e != cudaSuccess) {
     set_error(std::string("context creation failed: ") + cudaGetErrorString(e));
     ds_ctx_destroy(c);

@@ -231,6 +231,13 @@ struct MergeWs {
                                 // after the diagonal pass, or -1 (single GPU; nullptr: unused)
   unsigned long long* link_tab = nullptr;  // zeroed per call: tile-root pairs already linked
   unsigned int link_mask = 0;              // slots - 1 (a power of two)
+  // single-GPU pipeline: the label kernel's last block copies the scalar block into
+  // mapped page-locked memory (no device-to-host copy node for it). Labels written
+  // straight to page-locked host memory by the kernel were measured slower than the
+  // label kernel + a copy-engine copy (27 vs 47 GB/s at C2; tools/zerocopy_bench.cu).
+  const unsigned long long* dev_scalars = nullptr;
+  unsigned long long* host_scalars = nullptr;
+  int scalar_words = 0;
 };
 int64_t scan_partials_len(int64_t n);
 cudaError_t launch_core_init(const MergeWs& w, int64_t min_pts, cudaStream_t s);

@@ -945,15 +945,19 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* d
 // after any of its members (cmin <= o), so it is in this tile or an earlier one — an
 // earlier tile got its ticket first and publishes its ids right after its own
 // look-back, so the wait below is short and cannot deadlock. Labels are written in
-// original order (coalesced int64 stores). Replaces scan_lookback + label_kernel.
+// original order, staged in shared memory and stored as 16-byte runs (one contiguous
+// 32 KB span per tile, full sectors). Replaces scan_lookback + label_kernel. With
+// host_scalars set, the last block to finish copies the scalar block there.
 __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
     const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
     const int32_t* __restrict__ inv, int32_t* cid, int64_t n, unsigned int* ticket,
     unsigned long long* state, int32_t* total, int64_t* __restrict__ labels,
-    unsigned long long* stamps, unsigned int* done) {
+    unsigned long long* stamps, unsigned int* done, const unsigned long long* dev_scalars,
+    unsigned long long* host_scalars, int scalar_words) {
   griddep_wait();
   __shared__ unsigned int tile_sh;
   __shared__ int prefix_sh;
+  __shared__ __align__(16) long long lab_sh[SCAN_BLK];
   if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
   __syncthreads();
   const unsigned int tile = tile_sh;
@@ -1016,22 +1020,42 @@ __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
   const volatile int32_t* vc = cid;
 #pragma unroll
   for (int k = 0; k < SCAN_PER; ++k) {
-    const int64_t o = base + k;
-    if (o >= n) continue;
     int64_t lab = -1;
     if (r[k] >= 0) {
       int v = vc[r[k]];
       while (v < 0) v = vc[r[k]];  // published by an earlier tile (see above)
       lab = v;
     }
-    labels[o] = lab;
+    lab_sh[threadIdx.x * SCAN_PER + k] = lab;
   }
-  if (stamps) {  // the last block to finish stamps the end of stage 3
+  __syncthreads();
+  {
+    const int64_t t0 = (int64_t)tile * SCAN_BLK;
+    const int cnt = (int)(n - t0 < SCAN_BLK ? n - t0 : SCAN_BLK);
+    int64_t* out = labels + t0;
+    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+      longlong2* o2 = reinterpret_cast<longlong2*>(out);
+      const longlong2* s2 = reinterpret_cast<const longlong2*>(lab_sh);
+      for (int i = threadIdx.x; i < cnt / 2; i += SCAN_T) o2[i] = s2[i];
+      if ((cnt & 1) && threadIdx.x == 0) out[cnt - 1] = lab_sh[cnt - 1];
+    } else {
+      for (int i = threadIdx.x; i < cnt; i += SCAN_T) out[i] = lab_sh[i];
+    }
+  }
+  if (stamps || host_scalars) {  // the last block to finish: end-of-stage-3 stamp, scalars
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      stamps[ST_LABELS_DONE] = t;
+      if (stamps) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        stamps[ST_LABELS_DONE] = t;
+      }
+      if (host_scalars) {
+        __threadfence();
+        const volatile unsigned long long* src = dev_scalars;
+        for (int i = 0; i < scalar_words; ++i) host_scalars[i] = src[i];
+        __threadfence_system();
+      }
     }
   }
 }
@@ -1191,8 +1215,9 @@ cudaError_t launch_finalize(const MergeWs& w, int64_t* labels, cudaStream_t s) {
   return launch_pdl(scan_label_kernel, dim3((unsigned)tiles), dim3(SCAN_T), 0, s,
                     (const int32_t*)w.root, (const int32_t*)w.cmin, w.inv, w.flag, w.n,
                     reinterpret_cast<unsigned int*>(state),
-                    reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters, labels, w.stamps,
-                    w.label_blocks);
+                    reinterpret_cast<unsigned long long*>(state) + 1, w.nclusters, labels,
+                    w.stamps, w.label_blocks, w.dev_scalars, w.host_scalars,
+                    w.scalar_words);
 }
 
 cudaError_t launch_merge_forests(const MergeWs& w, const int32_t* parents, int R,
