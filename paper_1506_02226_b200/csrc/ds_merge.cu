@@ -122,6 +122,37 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
   return r;
 }
 
+// block-wide exclusive scan of one int per thread; also returns the block total
+__device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
+  __shared__ int warp_sums[32];
+  __shared__ int tot;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int s = lane < nw ? warp_sums[lane] : 0;
+    int si = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, si, off);
+      if (lane >= off) si += y;
+    }
+    if (lane < nw) warp_sums[lane] = si - s;
+    if (lane == nw - 1) tot = si;
+  }
+  __syncthreads();
+  total = tot;
+  const int excl = warp_sums[wid] + incl - v;
+  __syncthreads();  // the shared slots may be reused by the caller's next call
+  return excl;
+}
+
 // ---- union over tile-pair chunks (two rounds) --------------------------------------
 // Round 1, one CTA per diagonal chunk (tile a with itself, words hold j >= i):
 //   * every in-range core pair (u < v) proposes u as v's minimum neighbour
@@ -139,6 +170,7 @@ __device__ __forceinline__ int link_root(int32_t* parent, int r, int j) {
 // walk the tile pair's words as one flat index space (word k lives in the last
 // chunk whose prefix is <= k).
 constexpr int MAX_UPT = (TILE / 32) * WPR;  // 256 units per tile pair (KP = 1)
+static_assert(MAX_UPT <= 512, "union_diag loads one chunk entry per thread");
 
 struct ItemWords {
   uint32_t pre[MAX_UPT + 1];
@@ -274,6 +306,8 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
   __shared__ uint32_t adj[32];
   __shared__ int wroots[WPR], wpre[WPR], slot_root[32];
   __shared__ int ntrees_sh;
+  __shared__ int epre[MAX_UPT + 1];                  // chunk-entry prefix of the word counts
+  __shared__ unsigned long long ebase_sh[MAX_UPT];   // chunk-entry first word
   const int tid = threadIdx.x;
   const int w = tid % WPR, cblk = tid / WPR;
   const int64_t n = A.n;
@@ -327,6 +361,16 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
     }
     const long long e_lo = u_lo * WPR;
     const int nentries = (int)((u_hi - u_lo) * WPR);
+    // the pair's chunk entries (nentries <= MAX_UPT <= THREADS), loaded before the
+    // shared-memory setup so that their latency overlaps it
+    uint32_t ecnt = 0;
+    unsigned long long ebase = 0;
+    if (tid < nentries) {
+      const uint2 ce = uchunks[e_lo + tid];
+      ecnt = ce.y & 0xffffu;
+      ebase = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
+      if (ebase + ecnt > words_cap) ecnt = 0;  // overflowed run: the host re-runs
+    }
     for (int k = tid; k < WPR * DIAG_RS; k += THREADS) R[k] = 0u;
     for (int v = tid; v < TILE; v += THREADS) {
       lp[v] = v;
@@ -335,16 +379,6 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
     }
     if (tid == 0) slot_root[0] = -1;  // atomicMax target of the single-root fast path
     __syncthreads();
-    // scatter the tile pair's words into the dense matrix (core rows, core columns
-    // only), one warp per chunk entry; non-core rows give their own border candidate
-    // directly. Entries of an overflowed run are skipped (the host re-runs).
-    // the warp's chunk entries e = warp + 16 i are loaded together (lane i holds entry i)
-    const int nmine = nentries > (tid >> 5) ? (nentries - (tid >> 5) + THREADS / 32 - 1) / (THREADS / 32) : 0;
-    const uint2 mine = (tid & 31) < nmine ? uchunks[e_lo + (tid >> 5) + (THREADS / 32) * (tid & 31)]
-                                          : make_uint2(0u, 0u);
-    // An entry holds at most 32*KP <= 128 words: lane l takes words l + 32 q, q < 4,
-    // all loaded before any is scattered (one L2 round trip per entry instead of up to
-    // four dependent ones)
     auto scatter = [&](const uint2 rec) {
       const int u = (int)(rec.y >> 4);
       const int ww = (int)(rec.y & 15u);
@@ -365,43 +399,64 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
         if (cm) atomicMin(&lb[u], min_orig(perm, base + ww * 32, cm));
       }
     };
-    for (int i = 0; i < nmine; ++i) {  // nmine <= 32: 16 warps, <= 256 entries per tile pair
-      const uint2 ce = make_uint2(__shfl_sync(0xffffffffu, mine.x, i), __shfl_sync(0xffffffffu, mine.y, i));
-      const uint32_t cnt = ce.y & 0xffffu;
-      const unsigned long long wb = (unsigned long long)ce.x | ((unsigned long long)(ce.y >> 16) << 32);
-      if (cnt == 0u || wb + cnt > words_cap) continue;  // warp-uniform
-      const uint32_t k0 = tid & 31;
-      const uint2 r0 = k0 < cnt ? words[wb + k0] : make_uint2(0u, 0u);
-      const uint2 r1 = k0 + 32u < cnt ? words[wb + k0 + 32u] : make_uint2(0u, 0u);
-      const uint2 r2 = k0 + 64u < cnt ? words[wb + k0 + 64u] : make_uint2(0u, 0u);
-      const uint2 r3 = k0 + 96u < cnt ? words[wb + k0 + 96u] : make_uint2(0u, 0u);
-      if (k0 < cnt) scatter(r0);
-      if (k0 + 32u < cnt) scatter(r1);
-      if (k0 + 64u < cnt) scatter(r2);
-      if (k0 + 96u < cnt) scatter(r3);
-      for (uint32_t k = k0 + 128u; k < cnt; k += 32) scatter(words[wb + k]);  // not reached: <= 128
+    // scatter the tile pair's words into the dense matrix (core rows, core columns
+    // only); non-core rows give their own border candidate directly. The pair's words
+    // are one flat index space over its chunk entries (a block scan of the entry
+    // counts): every thread loads 4 words at a time from independent addresses, so the
+    // whole tile pair costs about two L2 round trips instead of one per entry.
+    {
+      int total;
+      const int pre = block_exclusive_scan((int)ecnt, total);
+      if (tid < nentries) {
+        epre[tid] = pre;
+        ebase_sh[tid] = ebase;
+      }
+      __syncthreads();
+      auto locate = [&](int j) -> unsigned long long {  // word j of the pair -> address
+        int lo = 0, hi = nentries;  // epre[lo] <= j < epre[hi], epre[nentries] taken as total
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (epre[mid] <= j) lo = mid;
+          else hi = mid;
+        }
+        return ebase_sh[lo] + (unsigned long long)(j - epre[lo]);
+      };
+      for (int j0 = tid; j0 < total; j0 += 4 * THREADS) {
+        uint2 rec[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + q * THREADS;
+          rec[q] = j < total ? words[locate(j)] : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j0 + q * THREADS < total) scatter(rec[q]);
+      }
     }
     __syncthreads();
-    // minimum neighbour of every core column = first row (ascending) holding it:
-    // OR per row block, exclusive prefix OR over blocks, then a second scan writes
-    // each column exactly once
+    // minimum neighbour of every core column = first row (ascending) holding it (the
+    // self bit makes it exist): OR per row block, then warp w takes word column w, lane
+    // l column 32 w + l — the first row block whose OR has the column (broadcast reads),
+    // then the first row of that block. No atomics, about 32 shared loads per lane
+    // (a per-bit atomicMin loop over the fresh bits of every row was 10 us of the
+    // kernel at C2).
     uint32_t acc = 0;
     for (int r = 0; r < RB; ++r) acc |= R[w * DIAG_RS + cblk * RB + r];
     M[cblk * WPR + w] = acc;
     __syncthreads();
-    uint32_t seen = 0;
-    for (int q = 0; q < cblk; ++q) seen |= M[q * WPR + w];
-    for (int r = 0; r < RB; ++r) {
-      const int u = cblk * RB + r;
-      const uint32_t x = R[w * DIAG_RS + u];
-      uint32_t fresh = x & ~seen;
-      seen |= x;
-      while (fresh) {
-        const int t = __clz(fresh);
-        fresh &= ~(0x80000000u >> t);
-        // u <= column: parent pointers decrease; several row blocks may hit the same
-        // column, the smallest row wins (deterministic, no write-write race)
-        atomicMin(&lp[w * 32 + t], u);
+    static_assert(THREADS / 32 == WPR, "one warp per word column");
+    {
+      const int ww = tid >> 5, l = tid & 31;
+      const uint32_t bit = 0x80000000u >> l;
+      int q0 = -1;
+#pragma unroll
+      for (int q = 0; q < THREADS / WPR; ++q)
+        if (q0 < 0 && (M[q * WPR + ww] & bit)) q0 = q;
+      if (q0 >= 0) {
+        const uint32_t* col = R + ww * DIAG_RS + q0 * RB;
+        int r = 0;
+        while (r < RB - 1 && !(col[r] & bit)) ++r;
+        lp[ww * 32 + l] = q0 * RB + r;
       }
     }
     __syncthreads();
@@ -554,28 +609,44 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
 // Round 2, off-diagonal tile pairs, one warp per row unit of the eps-tile launch
 // (lane block lb of tile a x the column blocks of tile b it evaluated). After round
 // 1 every core point's parent is its tile-local root. Per unit the warp stages the
-// parents and core flags of its 32*KP rows in shared memory; per non-empty column
-// block it stages that block's 32 parents and checks whether all of its core points
-// share one local root ("uniform", the common case inside a cluster). Then per word
-// (row u, column block jw, 32 bits):
-//   * core u, core columns: link root(u) with the uniform root, or with each core
-//     column's root; a per-lane cache of the last linked pair skips repeats;
+// parents and core flags of its 32*KP rows in shared memory and groups the rows of
+// each 32-row chunk by root (match_any: a group is named by its first lane); per
+// non-empty column block it stages that block's 32 parents and groups the columns the
+// same way. Then per word (row u, column block jw, 32 bits), all of a column block's
+// words loaded at once:
+//   * core u, core columns: the column groups the word touches are OR-ed into the
+//     row group's pair mask (shared memory) — after the block, one link per (row
+//     group, column group) pair that has a bit, made by the lanes in parallel, instead
+//     of a serial chain of per-bit links on one lane (the tail of this kernel);
 //   * core u, non-core columns: border candidates, atomicMin of u's ORIGINAL index;
 //   * non-core u with core columns: u's border candidate, the lowest ORIGINAL index
 //     among those columns (merge.py:116-130).
 // Links go through the global lock-free union-find (link_root: CAS hooks the larger
 // root under the smaller), so the result does not depend on the order.
 constexpr int LINK_WARPS = 8;
-__global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
+#ifndef DS_LINK_MINB
+#define DS_LINK_MINB 4
+#endif
+__global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_kernel(
     const UnitArgs A, int LB, const uint32_t* __restrict__ corew, int32_t* parent, int32_t* bmin,
     const int32_t* __restrict__ perm, const int32_t* __restrict__ blk_root,
     unsigned long long* link_tab, unsigned int link_mask) {
   griddep_wait();
-  __shared__ int rows_sh[LINK_WARPS][TILE / WPR * 4];  // up to 128 rows per lane block
+  constexpr int MAXR = TILE / WPR * 4;  // up to 128 rows per lane block
+  __shared__ int rows_sh[LINK_WARPS][MAXR];
   __shared__ int cols_sh[LINK_WARPS][32];
+  __shared__ uint8_t rlead_sh[LINK_WARPS][MAXR];     // row -> its group's first row
+  __shared__ uint8_t clead_sh[LINK_WARPS][32];       // column -> its group's first column
+  __shared__ uint32_t cmask_sh[LINK_WARPS][32];      // group (first column) -> its columns
+  __shared__ uint32_t pairs_sh[LINK_WARPS][MAXR];    // row group -> column groups linked
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* rows = rows_sh[warp];
   int* cols = cols_sh[warp];
+  uint8_t* rlead = rlead_sh[warp];
+  uint8_t* clead = clead_sh[warp];
+  uint32_t* cmask = cmask_sh[warp];
+  uint32_t* pairs = pairs_sh[warp];
+  for (int k = lane; k < MAXR; k += 32) pairs[k] = 0u;
   const int n = (int)A.n;
   const int KPL = TILE / LB;  // rows per lane block (32 * KP)
   long long r_lo, r_hi;
@@ -658,16 +729,20 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
         continue;
       }
     }
-    // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not core)
+    // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not
+    // core), grouped by root per 32-row chunk
     const int r0 = a * TILE + lb * KPL;
     int rfirst = -1;  // this lane's first core row root
     bool rsame = true;  // all of this lane's core rows share it
     bool rnoncore = false;  // this lane has a non-core row
-    for (int k = lane; k < KPL; k += 32) {
+    for (int k = lane; k < KPL; k += 32) {  // KPL is a multiple of 32: warp-uniform trips
       const int g = r0 + k;
       const int pg = g < n ? parent[g] : -1;
       const bool c = g < n && ((corew[g >> 5] >> (31 - (g & 31))) & 1u);
-      rows[k] = c ? pg : -1;
+      const int v = c ? pg : -1;
+      rows[k] = v;
+      const unsigned grp = __match_any_sync(0xffffffffu, v);
+      rlead[k] = (uint8_t)((k & ~31) + __ffs(grp) - 1);
       rnoncore |= g < n && !c;
       if (c) {
         if (rfirst < 0) rfirst = pg;
@@ -688,16 +763,22 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
     while (todo) {
       const int jw = __ffs(todo) - 1;
       todo &= todo - 1u;
-      const uint32_t wcnt = __shfl_sync(0xffffffffu, cnt, jw);
+      const uint32_t wcnt = __shfl_sync(0xffffffffu, cnt, jw);  // <= 32*KP <= 128 words
       const unsigned long long wbase = __shfl_sync(0xffffffffu, base, jw);
       const int c0 = b * TILE + jw * 32;
-      const uint2 rec0 = lane < wcnt ? A.words[wbase + lane] : make_uint2(0u, 0u);
+      uint2 rec[4];  // word k = lane + 32 q: all loads issued together
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        rec[q] = lane + 32u * q < wcnt ? A.words[wbase + lane + 32u * q] : make_uint2(0u, 0u);
       const int praw = c0 + lane < n ? parent[c0 + lane] : -1;
       const uint32_t cw = corew[(b * TILE >> 5) + jw];
       const bool cc = (cw >> (31 - lane)) & 1u;
       const int pv = cc ? praw : -1;
       cols[lane] = pv;
       const unsigned same = __match_any_sync(0xffffffffu, pv);
+      const int lead = __ffs(same) - 1;
+      clead[31 - lane] = (uint8_t)lead;  // indexed by bit position (bit 31 - l <-> lane l)
+      if (lane == lead) cmask[lane] = __brev(same);
       const unsigned corel = __brev(cw);  // bit l <-> lane l
       // uniform: every core lane in one match group
       const int first = corel ? __ffs(corel) - 1 : 0;
@@ -715,34 +796,25 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
       const uint32_t vmask = nvalid >= 32 ? 0xffffffffu : ~(0xffffffffu >> nvalid);
       const bool skip_words = one_link && rows_allcore && cw == vmask;
       if (skip_words) cc_any = wcnt > 0;
-      for (uint32_t k = skip_words ? wcnt : lane; k < wcnt; k += 32) {
-        const uint2 rec = k < 32 ? rec0 : A.words[wbase + k];
-        const uint32_t x = rec.x;
-        const int ul = (int)(rec.y >> 4);
-        const int au = rows[ul - lb * KPL];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (skip_words || lane + 32u * q >= wcnt) continue;
+        const uint32_t x = rec[q].x;
+        const int ul = (int)(rec[q].y >> 4);
+        const int kr = ul - lb * KPL;
         const uint32_t cm = x & cw;
-        if (au >= 0) {
+        if (rows[kr] >= 0) {
           if (cm) {
             if (one_link) {
               cc_any = true;
-            } else if (ub >= 0) {
-              if (au != ub && !(au == last_a && ub == last_b)) {
-                link_root(parent, find_plain(parent, au), ub);
-                last_a = au;
-                last_b = ub;
-              }
-            } else {
-              uint32_t bits = cm;
+            } else {  // the column groups this word touches
+              uint32_t bits = cm, m = 0u;
               while (bits) {
-                const int t = __clz(bits);
-                bits &= ~(0x80000000u >> t);
-                const int av = cols[t];
-                if (av != au && !(au == last_a && av == last_b)) {
-                  link_root(parent, find_plain(parent, au), av);
-                  last_a = au;
-                  last_b = av;
-                }
+                const int g = clead[__clz(bits) ^ 31];
+                m |= 1u << g;
+                bits &= ~cmask[g];
               }
+              atomicOr(&pairs[rlead[kr]], m);
             }
           }
           uint32_t bm = x & ~cw;
@@ -758,13 +830,35 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, 5) union_links_kernel(
           atomicMin(&bmin[a * TILE + ul], min_orig(perm, c0, cm));
         }
       }
-      if (one_link && __any_sync(0xffffffffu, cc_any) && lane == 0 && urow != ub &&
-          !(urow == last_a && ub == last_b)) {
-        link_root(parent, find_plain(parent, urow), ub);
-        last_a = urow;
-        last_b = ub;
+      if (one_link) {
+        if (__any_sync(0xffffffffu, cc_any) && lane == 0 && urow != ub &&
+            !(urow == last_a && ub == last_b)) {
+          link_root(parent, find_plain(parent, urow), ub);
+          last_a = urow;
+          last_b = ub;
+        }
+      } else {
+        __syncwarp();
+        // one link per (row group, column group) pair with a bit; lane l takes the
+        // row groups led by rows l, l + 32, ...
+        for (int k = lane; k < KPL; k += 32) {
+          uint32_t m = pairs[k];
+          if (!m) continue;
+          pairs[k] = 0u;
+          const int au = rows[k];
+          while (m) {
+            const int g = __ffs(m) - 1;
+            m &= m - 1u;
+            const int av = cols[g];
+            if (av != au && !(au == last_a && av == last_b)) {
+              link_root(parent, find_plain(parent, au), av);
+              last_a = au;
+              last_b = av;
+            }
+          }
+        }
       }
-      __syncwarp();  // cols is rewritten by the next column block
+      __syncwarp();  // cols / groups / pair masks are rewritten by the next column block
     }
   }
 }
@@ -828,37 +922,6 @@ __global__ void roots_kernel(const uint8_t* __restrict__ core, const int32_t* __
   const unsigned grp = __match_any_sync(0xffffffffu, r);
   const int m = (int)__reduce_min_sync(grp, (unsigned)o);  // o >= 0
   if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicMin(&cmin[r], m);
-}
-
-// block-wide exclusive scan of one int per thread; also returns the block total
-__device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
-  __shared__ int warp_sums[32];
-  __shared__ int tot;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += y;
-  }
-  if (lane == 31) warp_sums[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    const int s = lane < nw ? warp_sums[lane] : 0;
-    int si = s;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, si, off);
-      if (lane >= off) si += y;
-    }
-    if (lane < nw) warp_sums[lane] = si - s;
-    if (lane == nw - 1) tot = si;
-  }
-  __syncthreads();
-  total = tot;
-  const int excl = warp_sums[wid] + incl - v;
-  __syncthreads();  // the shared slots may be reused by the caller's next call
-  return excl;
 }
 
 // Single-pass exclusive scan (decoupled look-back): tiles of SCAN_BLK elements are
@@ -945,9 +1008,8 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback_kernel(In in, int32_t* d
 // after any of its members (cmin <= o), so it is in this tile or an earlier one — an
 // earlier tile got its ticket first and publishes its ids right after its own
 // look-back, so the wait below is short and cannot deadlock. Labels are written in
-// original order, staged in shared memory and stored as 16-byte runs (one contiguous
-// 32 KB span per tile, full sectors). Replaces scan_lookback + label_kernel. With
-// host_scalars set, the last block to finish copies the scalar block there.
+// original order. Replaces scan_lookback + label_kernel. With host_scalars set, the
+// last block to finish copies the scalar block there.
 __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
     const int32_t* __restrict__ root, const int32_t* __restrict__ cmin,
     const int32_t* __restrict__ inv, int32_t* cid, int64_t n, unsigned int* ticket,
@@ -957,7 +1019,6 @@ __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
   griddep_wait();
   __shared__ unsigned int tile_sh;
   __shared__ int prefix_sh;
-  __shared__ __align__(16) long long lab_sh[SCAN_BLK];
   if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
   __syncthreads();
   const unsigned int tile = tile_sh;
@@ -1026,21 +1087,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
       while (v < 0) v = vc[r[k]];  // published by an earlier tile (see above)
       lab = v;
     }
-    lab_sh[threadIdx.x * SCAN_PER + k] = lab;
-  }
-  __syncthreads();
-  {
-    const int64_t t0 = (int64_t)tile * SCAN_BLK;
-    const int cnt = (int)(n - t0 < SCAN_BLK ? n - t0 : SCAN_BLK);
-    int64_t* out = labels + t0;
-    if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
-      longlong2* o2 = reinterpret_cast<longlong2*>(out);
-      const longlong2* s2 = reinterpret_cast<const longlong2*>(lab_sh);
-      for (int i = threadIdx.x; i < cnt / 2; i += SCAN_T) o2[i] = s2[i];
-      if ((cnt & 1) && threadIdx.x == 0) out[cnt - 1] = lab_sh[cnt - 1];
-    } else {
-      for (int i = threadIdx.x; i < cnt; i += SCAN_T) out[i] = lab_sh[i];
-    }
+    if (base + k < n) labels[base + k] = lab;
   }
   if (stamps || host_scalars) {  // the last block to finish: end-of-stage-3 stamp, scalars
     __syncthreads();

@@ -107,7 +107,8 @@ def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
 def test_stage3_kernels_register_budget(lib):
     """The stage-3 union kernels are latency-bound and need their occupancy: union_diag
     (512 threads) four CTAs per SM, i.e. <= 32 registers (ptxas otherwise picked 64
-    and the kernel ran 40 % slower), union_links (256 threads) five, <= 48."""
+    and the kernel ran 40 % slower), union_links (256 threads) four, <= 64 (its
+    per-group link masks need more than 48: five CTAs spilled)."""
     out = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True,
                          check=True).stdout
     regs = {}
@@ -116,4 +117,4 @@ def test_stage3_kernels_register_budget(lib):
     diag = [r for k, r in regs.items() if "union_diag_kernel" in k]
     links = [r for k, r in regs.items() if "union_links_kernel" in k]
     assert diag and max(diag) <= 32, diag
-    assert links and max(links) <= 48, links
+    assert links and max(links) <= 64, links
