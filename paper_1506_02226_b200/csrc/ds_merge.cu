@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
       const uint2 e = __ldg(A.unit_list + u);
       a = (int)(e.x >> 16);
       b = (int)(e.x & 0xffffu);
-      lb = (int)(e.y >> 16);
+      lb = (int)((e.y >> 16) & 0xfu);
     } else {
       decode_item(u / LB, A.T, a, b);
       lb = (int)(u % LB);

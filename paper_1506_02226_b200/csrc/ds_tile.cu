@@ -88,9 +88,9 @@ struct Lanes {
   float t[KP];
 };
 
-// Squared distances of the KP lane points to staged point j (xj: its record,
+// Squared distances of lane points K0 .. K1-1 to staged point j (xj: its record,
 // pj = P_j), in the reference's order with one rounding per operation.
-template <int D, int F, int KP>
+template <int D, int F, int KP, int K0 = 0, int K1 = KP>
 __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, float pj,
                                         float (&d2)[KP]) {
   constexpr int DP = Lanes<D, KP>::DP;
@@ -99,7 +99,7 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
     // cross = ((X0*x0 + X1*x1) + X2*x2) + ...            (kernels.py:409-414)
     float c[KP];
 #pragma unroll
-    for (int k = 0; k < KP; ++k) {
+    for (int k = K0; k < K1; ++k) {
       float acc;
       if constexpr (DP > 0) {
         float2 m = __fmul2_rn(L.v2[k][0], make_float2(xj[0], xj[1]));
@@ -119,7 +119,7 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
     // d2 = (T + P) - cross, two lane points per FADD2       (kernels.py:415-417)
     if constexpr (KP % 2 == 0) {
 #pragma unroll
-      for (int k = 0; k < KP; k += 2) {
+      for (int k = K0; k < K1; k += 2) {
         const float2 tp = __fadd2_rn(make_float2(L.t[k], L.t[k + 1]), make_float2(pj, pj));
         const float2 d = __fadd2_rn(tp, make_float2(-c[k], -c[k + 1]));
         d2[k] = d.x;
@@ -127,12 +127,12 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < KP; ++k) d2[k] = __fsub_rn(__fadd_rn(L.t[k], pj), c[k]);
+      for (int k = K0; k < K1; ++k) d2[k] = __fsub_rn(__fadd_rn(L.t[k], pj), c[k]);
     }
   } else {
     // d2 = ((dx0^2 + dx1^2) + dx2^2) + ..., dx = x_col - x_row  (kernels.py:197-210)
 #pragma unroll
-    for (int k = 0; k < KP; ++k) {
+    for (int k = K0; k < K1; ++k) {
       float acc;
       if constexpr (DP > 0) {
         float2 dx = __fadd2_rn(make_float2(xj[0], xj[1]), L.v2[k][0]);
@@ -175,23 +175,24 @@ struct Pack {
   static constexpr int KC = !SAFE ? KP : (D <= 4 ? (3 * KP) / 4 : 0);
 };
 
-template <int KP, bool SAFE, int D>
+template <int KP, bool SAFE, int D, int K0 = 0, int K1 = KP>
 __device__ __forceinline__ void pack_bits(const float (&d2)[KP], float eps32, int jj,
                                           uint32_t (&acc)[KP]) {
   constexpr int KC = Pack<KP, SAFE, D>::KC;
+  constexpr int KS = KC > K0 ? KC : K0;  // first sign-bit lane point of the range
 #pragma unroll
-  for (int k = 0; k < KC; ++k) acc[k] |= (d2[k] <= eps32 ? 1u : 0u) << (31 - jj);
-  if constexpr (KC < KP) {
-    if constexpr ((KP - KC) % 2 == 0) {
+  for (int k = K0; k < (KC < K1 ? KC : K1); ++k) acc[k] |= (d2[k] <= eps32 ? 1u : 0u) << (31 - jj);
+  if constexpr (KS < K1) {
+    if constexpr ((K1 - KS) % 2 == 0) {
 #pragma unroll
-      for (int k = KC; k < KP; k += 2) {
+      for (int k = KS; k < K1; k += 2) {
         const float2 e = __fadd2_rn(make_float2(eps32, eps32), make_float2(-d2[k], -d2[k + 1]));
         acc[k] = __funnelshift_l(__float_as_uint(e.x), acc[k], 1);
         acc[k + 1] = __funnelshift_l(__float_as_uint(e.y), acc[k + 1], 1);
       }
     } else {
 #pragma unroll
-      for (int k = KC; k < KP; ++k)
+      for (int k = KS; k < K1; ++k)
         acc[k] = __funnelshift_l(__float_as_uint(__fsub_rn(eps32, d2[k])), acc[k], 1);
     }
   }
@@ -292,7 +293,36 @@ __device__ __forceinline__ uint32_t struct_mask(int n, int KP, int a, int b, int
 struct Step {
   long long u;
   int a, b, lb, jw;
+  int pm;  // row-block pairs to evaluate: bit 0 lane points 0-1, bit 1 lane points 2-3
 };
+
+// One column-block step's pair loop over lane points K0 .. K1-1 (KP = 4: one or both
+// pairs of lane points; the row-pair mask of the unit list, see box_pairs).
+template <int D, int F, bool SAFE, int K0, int K1>
+__device__ __forceinline__ void pair_loop(const Lanes<D, Geo<D>::KP>& L, const float* st, float eps32,
+                                          uint32_t (&acc)[Geo<D>::KP]) {
+  using G = Geo<D>;
+  constexpr int S = G::S;
+  constexpr int KP = G::KP;
+  // full unroll for d <= 4; wider records unroll by 8 to keep the independent
+  // warps' code inside the instruction cache
+#pragma unroll(G::UNROLL)
+  for (int jj = 0; jj < 32; ++jj) {
+    const float4* p4 = reinterpret_cast<const float4*>(st + jj * S);
+    float xj[S];
+#pragma unroll
+    for (int v = 0; v < S / 4; ++v) {
+      const float4 x = p4[v];
+      xj[4 * v + 0] = x.x;
+      xj[4 * v + 1] = x.y;
+      xj[4 * v + 2] = x.z;
+      xj[4 * v + 3] = x.w;
+    }
+    float d2[KP];
+    eval_d2<D, F, KP, K0, K1>(L, xj, xj[D], d2);
+    pack_bits<KP, SAFE, D, K0, K1>(d2, eps32, jj, acc);
+  }
+}
 
 // cp.async staging of one column block (16 bytes per instruction, zero-filled past n)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
@@ -340,6 +370,13 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   const int T = A.T;
   const float eps32 = A.eps32;
   const uint2* list = A.unit_list;
+  // tile-local row of lane point k of `lane` in lane block lb: with row-pair culling (d <=
+  // 4) lane point k is row block k of the lane block (rows lb*128 + 32k + lane), else the
+  // lane holds KP consecutive rows
+  constexpr bool STRIDED = KP == 4 && D <= 4;
+  auto lrow = [](int lb, int ln, int k) -> int {
+    return STRIDED ? lb * 32 * KP + k * 32 + ln : (lb * 32 + ln) * KP + k;
+  };
   long long r_lo, r_hi;
   unit_range(A, r_lo, r_hi);
   if (r_lo >= r_hi) return;
@@ -377,6 +414,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   long long gu = 0;
   uint32_t gab = 0u;  // a << 16 | b
   int glb = 0;
+  uint32_t gsub = 0xffffffffu;  // row-pair masks of unit gu's column blocks, 2 bits each
   auto next_step = [&](Step& st) -> bool {
     while (grem == 0u) {
       if (gpos >= cb_hi) {  // switch to the prefetched batch, prefetch the one after
@@ -394,14 +432,16 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
         const int src = (int)(u - cb_lo);
         gab = __shfl_sync(0xffffffffu, cent.x, src);
         const uint32_t ey = __shfl_sync(0xffffffffu, cent.y, src);
-        glb = (int)(ey >> 16);
+        glb = (int)((ey >> 16) & 0xfu);
         m = ey & 0xffffu;
+        gsub = KP == 4 ? ey >> 20 : 0xffffffffu;
       } else {
         int a, b;
         decode_item(u / LB, T, a, b);
         glb = (int)(u % LB);
         gab = ((uint32_t)a << 16) | (uint32_t)b;
         m = struct_mask(n, KP, a, b, glb);
+        gsub = 0xffffffffu;  // up to 16 column blocks, all rows
       }
       gu = u;
       if (lane < WPR && !((m >> lane) & 1u)) A.uchunks[u * WPR + lane] = make_uint2(0u, 0u);
@@ -413,6 +453,8 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
     st.lb = glb;
     st.jw = __ffs(grem) - 1;
     grem &= grem - 1u;
+    st.pm = STRIDED ? (int)(gsub & 3u) : 3;
+    gsub >>= 2;
     return true;
   };
   auto issue = [&](const Step& st, int buf) {  // all lanes: record `lane` of the block
@@ -445,7 +487,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
     if (la < 0) return;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
-      if (lcnt[k]) atomicAdd(&A.cnt[la * TILE + (llb * 32 + lane) * KP + k], (int)lcnt[k]);
+      if (lcnt[k]) atomicAdd(&A.cnt[la * TILE + lrow(llb, lane, k)], (int)lcnt[k]);
       lcnt[k] = 0u;
     }
   };
@@ -463,7 +505,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
       const int na = min(TILE, n - la * TILE);
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
-        const int il = (llb * 32 + lane) * KP + k;  // 32*KP consecutive points per block
+        const int il = lrow(llb, lane, k);
         lvalid[k] = il < na;
         const int i = la * TILE + (lvalid[k] ? il : 0);
         const float4* r4 = reinterpret_cast<const float4*>(A.rec + (size_t)i * S);
@@ -494,25 +536,14 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
     uint32_t acc[KP];
 #pragma unroll
     for (int k = 0; k < KP; ++k) acc[k] = 0u;
-    // full unroll for d <= 4; wider records unroll by 8 to keep the independent
-    // warps' code inside the instruction cache
-#pragma unroll(G::UNROLL)
-    for (int jj = 0; jj < 32; ++jj) {
-      const float4* p4 = reinterpret_cast<const float4*>(st + jj * S);
-      float xj[S];
-#pragma unroll
-      for (int v = 0; v < S / 4; ++v) {
-        const float4 x = p4[v];
-        xj[4 * v + 0] = x.x;
-        xj[4 * v + 1] = x.y;
-        xj[4 * v + 2] = x.z;
-        xj[4 * v + 3] = x.w;
-      }
-      float d2[KP];
-      eval_d2<D, F, KP>(L, xj, xj[D], d2);
-      pack_bits<KP, SAFE, D>(d2, eps32, jj, acc);
+    if constexpr (STRIDED) {  // warp-uniform: the step's row-pair mask
+      if (cur.pm == 3) pair_loop<D, F, SAFE, 0, 4>(L, st, eps32, acc);
+      else if (cur.pm == 1) pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, acc);
+      else pair_loop<D, F, SAFE, 2, 4>(L, st, eps32, acc);
+    } else {
+      pair_loop<D, F, SAFE, 0, KP>(L, st, eps32, acc);
     }
-    ++steps_done;
+    steps_done += (STRIDED && cur.pm != 3) ? 2 : KP;  // lane points evaluated
 
     const int nb = min(TILE, n - cur.b * TILE);
     const uint32_t vm = valid_mask(nb - cur.jw * 32);
@@ -521,7 +552,8 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
     uint32_t any = 0u;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
-      w[k] = lvalid[k] ? ((k < KC ? acc[k] : ~acc[k]) & vm) : 0u;
+      const bool ev = !STRIDED || ((cur.pm >> (k >> 1)) & 1);  // lane point k evaluated
+      w[k] = (lvalid[k] && ev) ? ((k < KC ? acc[k] : ~acc[k]) & vm) : 0u;
       lcnt[k] += __popc(w[k]);
       any |= w[k];
     }
@@ -534,7 +566,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
       } else {
 #pragma unroll
         for (int k = 0; k < KP; ++k)  // keep columns j >= row (incl. the self pair)
-          w[k] &= diag_keep((llb * 32 + lane) * KP + k - cur.jw * 32);
+          w[k] &= diag_keep(lrow(llb, lane, k) - cur.jw * 32);
       }
       // append the non-zero words into the warp's reserved run
       // word order: lane-major, then k; offsets from one ballot per k (no shuffle chain)
@@ -557,11 +589,11 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
       wpos += (unsigned long long)total;
       if (base + (unsigned long long)total <= A.words_cap) {  // else dropped: the host re-runs
         uint2* dst = A.words + base + excl;
-        const uint32_t tag = ((uint32_t)((llb * 32 + lane) * KP) << 4) | (uint32_t)cur.jw;
+        const uint32_t tag = ((uint32_t)lrow(llb, lane, 0) << 4) | (uint32_t)cur.jw;
         int o = 0;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
-          if (w[k]) dst[o] = make_uint2(w[k], tag + ((uint32_t)k << 4));
+          if (w[k]) dst[o] = make_uint2(w[k], tag + ((uint32_t)(lrow(0, 0, k)) << 4));
           o += w[k] ? 1 : 0;
         }
       }
@@ -576,7 +608,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   }
   flush();
   if (lane == 0 && steps_done)
-    atomicAdd(A.pairs_done, steps_done * 32ull * 32ull * (unsigned long long)KP);
+    atomicAdd(A.pairs_done, steps_done * 32ull * 32ull);
 }
 
 // One launch serves both number ranges: the prep kernel's device flag selects the
@@ -592,78 +624,102 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, Geo<D>::MINB) eps_unit_kernel
 
 // ---- culled schedule: row-unit list ----------------------------------------------------
 // Column block jw of lane block lb in kept tile pair (a, b) is evaluated unless it is
-// structurally empty (struct_mask) or, for d <= 4, the union box of the lane block's
-// KP 32-point blocks and the box of the column block are provably out of range: the
-// bound of keep_item, in double, on the block boxes (block_bounds_kernel).
-// Box test of (lane block lb of tile a) x (column block jw of tile b), d <= 4 (KP = 4):
-// all loads independent (fully unrolled), so one round trip per test.
+// structurally empty (struct_mask) or, for d <= 4, every 32-point row block of the lane
+// block is provably out of range of it: the bound of keep_item, in double, on the row
+// block box and the column block box (block_bounds_kernel). The row blocks that are not
+// also give the step's row-pair mask: lane point k of every lane is row block k of the
+// lane block, so a pair of row blocks (0-1, 2-3) without a possible pair is skipped by
+// the eps kernel (C2: 28 % of the pairs of the kept column blocks).
+// Row-pair mask of (lane block lb of tile a) x (column block jw of tile b), d <= 4 (KP =
+// 4): bit 0 if row block 0 or 1 may hold an in-range pair, bit 1 for row blocks 2-3.
+// rb: the lane block's 4 row-block boxes (BS floats each), nrb of them valid; cb: the
+// column block's box (both staged in shared memory by pair_masks).
 template <int DP>
-__device__ __forceinline__ bool box_keep(const float* __restrict__ blk, int64_t n, int a, int b,
-                                         int lb, int jw, float eps32, int formula) {
+__device__ __forceinline__ uint32_t box_pairs(const float* rb, int nrb, const float* cb, float eps32,
+                                              int formula) {
+  // keep_item's bound in float with directed rounding: every operation rounds toward a
+  // smaller bound (gaps, squares and sums down, the subtracted rounding slack up), so
+  // the float bound is below the exact one and culling stays exact; the constants carry
+  // an extra 1e-6 / 0.1 % margin for their own rounding
   constexpr int BS = 2 * DP + 1;
-  constexpr int KPB = 4;  // 32-point blocks per lane block
-  const int64_t nblk = (n + 31) / 32;
-  const float* cb = blk + ((int64_t)b * WPR + jw) * BS;
-  const int64_t l0 = (int64_t)a * WPR + (int64_t)lb * KPB;
-  float lo[DP], hi[DP], c[BS];
-  float wn = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < DP; ++q) {
-    lo[q] = INFINITY;
-    hi[q] = -INFINITY;
-  }
+  constexpr float u = 1.0f / 16777216.0f;
+  constexpr float C1 = 1.0f - 12.0f * DP * u - 1e-6f;                   // (1 - 12 DP u)(1 - 1e-12)
+  constexpr float C2 = 8.0f * (2.0f * DP + 3.0f) * u * 1.001f * 1.001f;  // 4 (2DP+3) u 2 w 1.001
+  float c[BS];
 #pragma unroll
   for (int q = 0; q < BS; ++q) c[q] = cb[q];
+  uint32_t pm = 0u;
 #pragma unroll
-  for (int k = 0; k < KPB; ++k) {
-    if (l0 + k < nblk) {
-      const float* lk = blk + (l0 + k) * BS;
+  for (int k = 0; k < 4; ++k) {
+    if (k >= nrb) break;
+    const float* r = rb + k * BS;
+    float L = 0.f;
 #pragma unroll
-      for (int q = 0; q < DP; ++q) {
-        lo[q] = fminf(lo[q], lk[q]);
-        hi[q] = fmaxf(hi[q], lk[DP + q]);
-      }
-      wn = fmaxf(wn, lk[2 * DP]);
+    for (int q = 0; q < DP; ++q) {
+      const float g = fmaxf(0.f, fmaxf(__fsub_rd(c[q], r[DP + q]), __fsub_rd(r[q], c[DP + q])));
+      L = __fadd_rd(L, __fmul_rd(g, g));
     }
+    float bound = __fmul_rd(L, C1);
+    if (formula == DS_FORMULA_ALGEBRAIC) bound = __fsub_rd(bound, __fmul_ru(fmaxf(r[2 * DP], c[2 * DP]), C2));
+    if (!(bound > eps32)) pm |= 1u << (k >> 1);  // NaN bounds keep the block
   }
-  const double u = 1.0 / 16777216.0;
-  double L = 0.0;
-#pragma unroll
-  for (int q = 0; q < DP; ++q) {
-    const double g = fmax(0.0, fmax((double)c[q] - (double)hi[q], (double)lo[q] - (double)c[DP + q]));
-    L += g * g;
-  }
-  const double w = fmax((double)wn, (double)c[2 * DP]);
-  double bound = L * (1.0 - 4.0 * 3.0 * DP * u) * (1.0 - 1e-12);
-  if (formula == DS_FORMULA_ALGEBRAIC) bound -= 4.0 * (2.0 * DP + 3.0) * u * w * 2.0 * 1.001;
-  return !(bound > (double)eps32);  // NaN bounds keep the unit
+  return pm;
 }
 
-__device__ __forceinline__ bool unit_keep(const float* __restrict__ blk, int dpad, int64_t n, int KP,
-                                          int a, int b, int lb, int jw, float eps32, int formula,
-                                          bool unsafe) {
+// 0: not evaluated; else the row-pair mask (3 where no box test applies)
+__device__ __forceinline__ uint32_t unit_pairs(const float* __restrict__ blk, const float* rb, int nrb,
+                                               const float* cb, int dpad, int64_t n, int KP, int a,
+                                               int b, int lb, int jw, float eps32, int formula,
+                                               bool unsafe) {
   const int64_t na = min((int64_t)TILE, n - (int64_t)a * TILE);
   const int64_t nb = min((int64_t)TILE, n - (int64_t)b * TILE);
-  if (jw * 32 >= nb || lb * 32 * KP >= na) return false;
-  if (a == b && jw < lb * KP) return false;
-  if (unsafe || !blk || KP != 4 || (a == b && jw < (lb + 1) * KP)) return true;
+  if (jw * 32 >= nb || lb * 32 * KP >= na) return 0u;
+  if (a == b && jw < lb * KP) return 0u;
+  if (unsafe || !blk || KP != 4 || (a == b && jw < (lb + 1) * KP)) return 3u;
   switch (dpad) {
-    case 1: return box_keep<1>(blk, n, a, b, lb, jw, eps32, formula);
-    case 2: return box_keep<2>(blk, n, a, b, lb, jw, eps32, formula);
-    case 3: return box_keep<3>(blk, n, a, b, lb, jw, eps32, formula);
-    case 4: return box_keep<4>(blk, n, a, b, lb, jw, eps32, formula);
-    default: return true;
+    case 1: return box_pairs<1>(rb, nrb, cb, eps32, formula);
+    case 2: return box_pairs<2>(rb, nrb, cb, eps32, formula);
+    case 3: return box_pairs<3>(rb, nrb, cb, eps32, formula);
+    case 4: return box_pairs<4>(rb, nrb, cb, eps32, formula);
+    default: return 3u;
   }
 }
 
 // Column masks of two lane blocks (2p, 2p + 1) of item (a, b): lanes 0-15 test the 16
-// column blocks of the first, lanes 16-31 those of the second.
-__device__ __forceinline__ uint32_t pair_masks(const float* __restrict__ blk, int dpad, int64_t n,
-                                               int KP, int a, int b, int p, float eps32, int formula,
-                                               bool unsafe, int lane) {
-  const int lb = 2 * p + (lane >> 4);
-  const bool keep = unit_keep(blk, dpad, n, KP, a, b, lb, lane & 15, eps32, formula, unsafe);
-  return __ballot_sync(0xffffffffu, keep);
+// column blocks of the first, lanes 16-31 those of the second. keep: evaluated column
+// blocks; pair0 / pair1: those whose row-pair mask has bit 0 / bit 1. rb / cbs: the
+// item's 16 row-block boxes and 16 column-block boxes, staged by stage_boxes.
+struct PairMasks {
+  uint32_t keep, pair0, pair1;
+};
+__device__ __forceinline__ void stage_boxes(const float* __restrict__ blk, float* rb, float* cbs,
+                                            int dpad, int64_t n, int KP, int a, int b, int lane) {
+  if (!(blk && KP == 4 && dpad <= 4)) return;
+  const int BS = 2 * dpad + 1;
+  const int64_t nblk = (n + 31) / 32;
+  const int64_t r0 = (int64_t)a * WPR, c0 = (int64_t)b * WPR;  // first row / column block
+  __syncwarp();  // the previous item's readers are done
+  for (int i = lane; i < WPR * BS; i += 32) {  // all loads issued together: one round trip
+    rb[i] = r0 + i / BS < nblk ? blk[r0 * BS + i] : 0.f;
+    cbs[i] = c0 + i / BS < nblk ? blk[c0 * BS + i] : 0.f;
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ PairMasks pair_masks(const float* __restrict__ blk, const float* rb,
+                                                const float* cbs, int dpad, int64_t n, int KP, int a,
+                                                int b, int p, float eps32, int formula, bool unsafe,
+                                                int lane) {
+  const int BS = 2 * dpad + 1;
+  const int64_t nblk = (n + 31) / 32;
+  const int64_t r0 = (int64_t)a * WPR + (int64_t)(2 * p) * 4;  // first row block (KP = 4)
+  rb += (2 * p) * 4 * BS;
+  const int h = lane >> 4;
+  const int lb = 2 * p + h;
+  const int nrb = (int)min((int64_t)4, nblk - (r0 + 4 * h));
+  const uint32_t pm = unit_pairs(blk, rb + 4 * BS * h, nrb, cbs + (lane & 15) * BS, dpad, n, KP, a,
+                                 b, lb, lane & 15, eps32, formula, unsafe);
+  return {__ballot_sync(0xffffffffu, pm != 0u), __ballot_sync(0xffffffffu, (pm & 1u) != 0u),
+          __ballot_sync(0xffffffffu, (pm & 2u) != 0u)};
 }
 
 // For KP = 4 (d <= 8) a (lane block, tile pair) with many kept column blocks is
@@ -677,7 +733,7 @@ __device__ __forceinline__ int unit_cols(int KP) { return KP == 4 ? 4 : 16; }
 // the sparse regions evenly), masks by pair_masks, split into pieces, one atomic per
 // item reserves its list run. The order of the runs is arbitrary; item_units[q]
 // records {first unit, units} for the directory.
-__global__ void __launch_bounds__(256) unit_list_kernel(
+__global__ void __launch_bounds__(256, 4) unit_list_kernel(
     const float* __restrict__ blk, int dpad, int64_t n, int KP, float eps32, int formula,
     const uint32_t* __restrict__ unsafe_flag, const uint32_t* __restrict__ items,
     const unsigned long long* __restrict__ kept, int rank, int world, uint2* __restrict__ list,
@@ -687,6 +743,9 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
   constexpr int W = 8;  // warps per CTA; one list reservation per CTA and round
   __shared__ int wcnt[W];
   __shared__ unsigned long long wpos[W];
+  __shared__ uint32_t msk[W][3][8];  // per warp and lane-block pair: keep, pair0, pair1
+  __shared__ float rbs[W][WPR * 9];  // per warp: the row-block boxes of tile a
+  __shared__ float cbs[W][WPR * 9];  // per warp: the column-block boxes of tile b
   const int64_t K = (int64_t)*kept;
   const bool unsafe = *unsafe_flag != 0;
   const int LB = TILE / (32 * KP);
@@ -697,15 +756,20 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
     const int64_t t = t0 + warp;
     const int64_t q = rank + t * world;
     uint32_t ab = 0u;
-    uint32_t bal[8];
     int c = 0;
     if (t < mine) {  // warp-uniform
       ab = items[q];
       const int a = (int)(ab >> 16), b = (int)(ab & 0xffffu);
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        bal[p] = p < LB / 2 ? pair_masks(blk, dpad, n, KP, a, b, p, eps32, formula, unsafe, lane) : 0u;
-        c += (__popc(bal[p] & 0xffffu) + uc - 1) / uc + (__popc(bal[p] >> 16) + uc - 1) / uc;
+      stage_boxes(blk, rbs[warp], cbs[warp], dpad, n, KP, a, b, lane);
+      for (int p = 0; p < LB / 2; ++p) {
+        const PairMasks pmk = pair_masks(blk, rbs[warp], cbs[warp], dpad, n, KP, a, b, p, eps32,
+                                         formula, unsafe, lane);
+        if (lane == 0) {
+          msk[warp][0][p] = pmk.keep;
+          msk[warp][1][p] = pmk.pair0;
+          msk[warp][2][p] = pmk.pair1;
+        }
+        c += (__popc(pmk.keep & 0xffffu) + uc - 1) / uc + (__popc(pmk.keep >> 16) + uc - 1) / uc;
       }
     }
     if (lane == 0) wcnt[warp] = c;
@@ -720,26 +784,35 @@ __global__ void __launch_bounds__(256) unit_list_kernel(
       }
     }
     __syncthreads();
-    if (t < mine && lane == 0) {
+    if (t < mine) {  // warp-uniform; lane j of half h writes the unit starting at column j
       unsigned long long pos = wpos[warp];
-      const uint2 iu = make_uint2((uint32_t)pos, (uint32_t)c | ((uint32_t)(pos >> 32) << 16));
-      item_units[q] = iu;
-      if ((ab >> 16) == (ab & 0xffffu)) diag_range[ab >> 16] = iu;  // for union_diag
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t m = h ? bal[p] >> 16 : bal[p] & 0xffffu;
-          while (m) {  // pieces of at most unit_cols(KP) column blocks
-            uint32_t piece = 0u;
-            for (int k = 0; k < uc && m; ++k) {
-              piece |= m & (0u - m);
-              m &= m - 1u;
-            }
-            if (pos < cap) list[pos] = make_uint2(ab, ((uint32_t)(2 * p + h) << 16) | piece);
-            ++pos;
+      if (lane == 0) {
+        const uint2 iu = make_uint2((uint32_t)pos, (uint32_t)c | ((uint32_t)(pos >> 32) << 16));
+        item_units[q] = iu;
+        if ((ab >> 16) == (ab & 0xffffu)) diag_range[ab >> 16] = iu;  // for union_diag
+      }
+      const int h = lane >> 4, j = lane & 15;
+      for (int p = 0; p < LB / 2; ++p) {
+        const uint32_t keep = msk[warp][0][p];
+        const uint32_t m = h ? keep >> 16 : keep & 0xffffu;
+        const int np0 = (__popc(keep & 0xffffu) + uc - 1) / uc;  // units of lane block 2p
+        const int np1 = (__popc(keep >> 16) + uc - 1) / uc;
+        const int r = __popc(m & ((1u << j) - 1u));  // rank of column j among kept ones
+        if (((m >> j) & 1u) && r % uc == 0) {  // first column of a unit: up to uc columns
+          const uint32_t m0 = h ? msk[warp][1][p] >> 16 : msk[warp][1][p] & 0xffffu;
+          const uint32_t m1 = h ? msk[warp][2][p] >> 16 : msk[warp][2][p] & 0xffffu;
+          uint32_t rest = m & ~((1u << j) - 1u), piece = 0u, sub = 0u;  // sub: 2-bit row-pair
+          for (int k = 0; k < uc && rest; ++k) {                         // masks in column order
+            const uint32_t bit = rest & (0u - rest);
+            piece |= bit;
+            if (k < 4) sub |= (((m0 & bit) ? 1u : 0u) | ((m1 & bit) ? 2u : 0u)) << (2 * k);
+            rest &= rest - 1u;
           }
+          const unsigned long long at = pos + (h ? np0 : 0) + r / uc;
+          // {a << 16 | b, column mask | lane block << 16 | row-pair masks << 20 (KP = 4)}
+          if (at < cap) list[at] = make_uint2(ab, ((uint32_t)(2 * p + h) << 16) | piece | (sub << 20));
         }
+        pos += (unsigned long long)(np0 + np1);
       }
     }
     __syncthreads();  // wcnt / wpos are rewritten by the next round
@@ -1179,8 +1252,23 @@ cudaError_t launch_unit_list(const float* blk, int64_t n, int d, float eps32, in
   const int dp = pad_dim(d);
   const int KP = unit_kp(d);
   const float* box = dp <= 4 ? blk : nullptr;  // block boxes only pay off in low dimension
+  // one resident wave (the kernel strides over the kept items): empty CTAs beyond it
+  // would only add launch waves
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::atomic<int> wave_dev[DS_MAX_DEVICES] = {};
+  int wave = dev < DS_MAX_DEVICES ? wave_dev[dev].load() : 0;
+  if (wave == 0) {
+    int sms = 148, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, unit_list_kernel, 256, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 2;
+    wave = sms * per_sm;
+    if (dev < DS_MAX_DEVICES) wave_dev[dev].store(wave);
+  }
   int64_t blocks = (all_items / world * 32 + 255) / 256 + 1;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > wave) blocks = wave;
   return launch_pdl(unit_list_kernel, dim3((unsigned)blocks), dim3(256), 0, s, box, dp, n, KP, eps32,
                     formula, unsafe_flag, item_list, kept, rank, world, unit_list, units_cap,
                     unit_count, item_units, diag_range);

@@ -140,12 +140,14 @@ def test_capacity_cap_still_raises(ds):
         ctx.close()
 
 
-@pytest.mark.parametrize("name,pairs,tiles", [("C2", 211_812_352, 3823)])
+@pytest.mark.parametrize("name,pairs,tiles", [("C2", 152_918_016, 3823)])
 def test_spatial_sort_is_the_stable_key_order(ds, name, pairs, tiles):
     """The hand-written LSD radix sort (ds_sort.cu) must give the stable (key, index)
     order — the one round 1's library sort produced: the work counters of the culled
-    schedule depend on the exact permutation, so they must equal round 1's numbers, on
-    two independent contexts and on repeated calls."""
+    schedule depend on the exact permutation, so they must equal the pinned numbers, on
+    two independent contexts and on repeated calls. (Kept tile pairs: round 1's 3823.
+    Pairs: round 1's 211,812,352 before the row-pair culling of the unit list, 152,918,016
+    with it.)"""
     cfg = ds.CONFIGS[name]
     pts = cfg.points()
     params = ds.validate_params(cfg.eps, cfg.min_pts)
