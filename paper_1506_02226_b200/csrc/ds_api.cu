@@ -61,7 +61,7 @@ struct Scalars {  // a whole number of 8-byte words (the label kernel copies it 
   unsigned int label_blocks;                // label_kernel blocks finished
   unsigned long long stamps[ST_COUNT];      // device stage boundaries (Stamp)
 };
-static_assert(sizeof(Scalars) % 8 == 0, "Scalars is copied in 8-byte words");
+static_assert(sizeof(Scalars) % 8 == 0 && sizeof(Scalars) / 8 <= 1024, "Scalars is copied in 8-byte words, one per label-kernel thread");
 
 // The per-call zero region: one memset clears the scalars, the spatial-sort bounding
 // box, the diagonal directory index and the label scan's look-back state.

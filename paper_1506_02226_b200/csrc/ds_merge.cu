@@ -1090,18 +1090,22 @@ __global__ void __launch_bounds__(SCAN_T) scan_label_kernel(
     if (base + k < n) labels[base + k] = lab;
   }
   if (stamps || host_scalars) {  // the last block to finish: end-of-stage-3 stamp, scalars
+    __shared__ bool last_sh;
+    __threadfence();  // this block's writes (ids, the cluster count) before its arrival
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
-      if (stamps) {
+    if (threadIdx.x == 0) last_sh = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last_sh) {  // block-uniform
+      if (threadIdx.x == 0 && stamps) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         stamps[ST_LABELS_DONE] = t;
       }
-      if (host_scalars) {
-        __threadfence();
+      __syncthreads();
+      // one word per thread; the kernel's completion makes them visible to the host
+      if (host_scalars && (int)threadIdx.x < scalar_words) {
         const volatile unsigned long long* src = dev_scalars;
-        for (int i = 0; i < scalar_words; ++i) host_scalars[i] = src[i];
-        __threadfence_system();
+        host_scalars[threadIdx.x] = src[threadIdx.x];
       }
     }
   }

@@ -212,7 +212,10 @@ struct Geo {
 #ifndef DS_MINB16
 #define DS_MINB16 3
 #endif
-  static constexpr int UNROLL = D <= 4 ? 32 : DS_UNROLL_WIDE;
+#ifndef DS_UNROLL_SMALL
+#define DS_UNROLL_SMALL 32
+#endif
+  static constexpr int UNROLL = D <= 4 ? DS_UNROLL_SMALL : DS_UNROLL_WIDE;
   // resident CTAs (x 4 warps) per SM: 16-D holds 4 lane points x 17 floats per lane
 #ifndef DS_MINB_SMALL
 #define DS_MINB_SMALL 4
