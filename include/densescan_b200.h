@@ -65,7 +65,8 @@ typedef struct {
   double total_ms;          /* whole call, host wall clock                           */
   double tile_ms;           /* the eps-tile kernel alone                             */
   double h2d_ms;            /* host->device copy of the coordinates                  */
-  double d2h_ms;            /* device->host copy of the labels                       */
+  double d2h_ms;            /* device->host copy of the labels (event timing only,  */
+                            /* DS_OPT_EVENT_TIMING; 0 otherwise)                     */
   int64_t pairs_evaluated;  /* ordered pair evaluations executed by the tile kernel  */
   int64_t tiles_total;      /* tile pairs processed (upper triangle incl. diagonal)  */
   int64_t tiles_nonempty;   /* tile pairs with at least one in-range pair            */

@@ -561,14 +561,17 @@ ds_status enqueue_device(ds_ctx* c, const double* d_coords, int64_t n, int d, do
   DS_CK(launch_union_chunks(w, c->units, c->unit_lb, diag_range(c), core_init_args(w, min_pts), s));
   DS_CK(launch_finalize(w, d_labels, s));
   if (d_counts64) DS_CK(launch_counts_i64((const int32_t*)c->cnt.p, n, w.perm, d_counts64, s));
+  if (c->event_timing) DS_CK(rec(c->ev[4]));
   if (!c->h_scalars_dev)
     DS_CK(cudaMemcpyAsync(c->h_scalars, c->scalars.p, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
-  DS_CK(rec(c->ev[4]));
+  // no event nodes around the copies out: an event-record node between the label
+  // kernel and the copy cost ~10 us of device time per call (C2; ev7 is recorded on the
+  // stream after the launch instead)
   if (io && io->labels)
     DS_CK(cudaMemcpyAsync(io->labels, d_labels, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
   if (io && io->counts && d_counts64)
     DS_CK(cudaMemcpyAsync(io->counts, d_counts64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-  DS_CK(rec(c->ev[7]));
+
   c->capturing = false;
   return DS_OK;
 }
@@ -625,6 +628,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[1] |= (unsigned long long)(io && io->coords) << 41 | (unsigned long long)(io && io->labels) << 42 |
               (unsigned long long)(io && io->counts) << 43;
     const bool use_graph = c->use_graph && io_graphable && !c->no_graph_key;
+
     const bool graph_hit = use_graph && c->gexec && std::memcmp(key, c->gkey, sizeof key) == 0;
     if (graph_hit) {
       if (io && io->coords && c->gn_h2d)
@@ -710,6 +714,7 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       DS_CK(cudaEventSynchronize(c->ev[0]));
       DS_CK(cudaEventElapsedTime(&io->h2d_ms, c->ev[5], c->ev[0]));
     }
+    DS_CK(cudaEventRecord(c->ev[7], s));  // end of the device span (after the graph)
     DS_CK(cudaStreamSynchronize(s));
     bool retry = false;
     ds_status st = check_words(c, pl, mem_cap, &retry);
@@ -741,9 +746,11 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
       k = (float)((st[ST_MERGE] - st[ST_TILE]) * 1e-6);
       m = (float)((st[ST_LABELS_DONE] - st[ST_MERGE]) * 1e-6);
     } else {  // no split available: the whole device part as stage 1+2
-      DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[4]));
+      DS_CK(cudaEventElapsedTime(&f, c->ev[0], c->ev[7]));
     }
-    if (io && (io->labels || io->counts))  // host copies after the label kernel
+    // the host copies after the label kernel: timed only with event timing (one more
+    // cudaEventElapsedTime, a few us of host time after the sync, otherwise)
+    if (c->event_timing && io && (io->labels || io->counts))
       DS_CK(cudaEventElapsedTime(&o, c->ev[4], c->ev[7]));
     t->fused_ms = f;
     t->merge_ms = m;

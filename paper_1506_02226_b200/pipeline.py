@@ -74,8 +74,10 @@ class StageTimings:
     """Per-stage times in ms (pipeline.py:52-67) plus device counters.
 
     dist/cluster are None for the fused rungs, fused_ms None otherwise; stage
-    times are CUDA-event times of the device work, total_ms the wall time of
-    the whole call (host<->device copies included).
+    times are device times of the device work (%globaltimer stamps at kernel
+    boundaries), total_ms the wall time of the whole call (host<->device copies
+    included). h2d_ms is timed with CUDA events while the pipeline runs; d2h_ms
+    only with event timing (DS_OPT_EVENT_TIMING), 0.0 otherwise.
     """
 
     dist_ms: float | None = None

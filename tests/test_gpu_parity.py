@@ -450,7 +450,8 @@ def test_stage_timings_stamps_and_events(ds):
         try:
             for _ in range(3):  # eager, recorded, replayed
                 labels, _, t = ctx.run_dbscan(pts.coords_aos, params.eps_sq, 5, 1, 0)
-                assert 0 < t.tile_ms <= t.fused_ms and t.merge_ms > 0 and t.d2h_ms > 0
+                assert 0 < t.tile_ms <= t.fused_ms and t.merge_ms > 0
+                assert t.d2h_ms > 0 if ev else t.d2h_ms == 0  # copies timed with events only
                 assert t.fused_ms + t.merge_ms < t.total_ms
         finally:
             ctx.set_event_timing(False)
