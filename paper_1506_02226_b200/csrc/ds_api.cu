@@ -77,7 +77,9 @@ inline int link_tab_bits(int64_t n) {
   return b;
 }
 inline size_t zr_links(int64_t n) { return zr_round(zr_scan(n) + (size_t)scan_partials_len(n) * 4); }
-inline size_t zr_bytes(int64_t n) { return zr_links(n) + ((size_t)8 << link_tab_bits(n)); }
+// the super-tile boxes of the hierarchical culling (d <= 4)
+inline size_t zr_super(int64_t n) { return zr_round(zr_links(n) + ((size_t)8 << link_tab_bits(n))); }
+inline size_t zr_bytes(int64_t n) { return zr_super(n) + (size_t)n_supers(n_tiles(n)) * SUPER_BS * 4; }
 
 }  // namespace
 
@@ -354,6 +356,7 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
       bnd.hi = bnd.lo + (size_t)T * dp;
       bnd.maxnorm = bnd.lo + (size_t)T * 2 * dp;
       bnd.blk = dp <= 4 ? (float*)c->blk.p : nullptr;  // block boxes only pay off at d <= 4
+      bnd.super = (unsigned int*)((char*)c->scalars.p + zr_super(n));
     }
   }
   if (do_sort) {  // Morton order: compact tiles (ds_sort.cu)
@@ -379,8 +382,9 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     DS_CK(ensure(c->ipartials, (size_t)scan_partials_len(pl.all_items) * 4));
     float* lo = (float*)c->tbox.p;
     DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo, lo + (size_t)T * dp,
-                      lo + (size_t)T * 2 * dp, (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p,
-                      &sc->kept32, (uint32_t*)c->items.p, &sc->kept, bnd.lo != nullptr, s));
+                      lo + (size_t)T * 2 * dp, (unsigned int*)((char*)c->scalars.p + zr_super(n)),
+                      (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p, &sc->kept32,
+                      (uint32_t*)c->items.p, &sc->kept, bnd.lo != nullptr, s));
   }
   UnitArgs a;
   a.rec = rec;

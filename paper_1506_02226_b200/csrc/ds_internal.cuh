@@ -156,6 +156,27 @@ __device__ __forceinline__ unsigned int ord_bits(float f) {
   const unsigned int u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+__device__ __forceinline__ float unord_bits(unsigned int u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Super tiles: 32 consecutive tiles (16k points). Their boxes (d <= 4) let the tile
+// culling test a tile row against a super tile first (T^2 / 32 instead of T^2 / 2 box
+// tests at C5). Layout per super tile (uint, zeroed per call, reduced with atomicMax):
+// {~ord lo[dpad], ord hi[dpad], ord maxnorm}; SUPER_BS words per super tile.
+constexpr int SUPER = 32;
+constexpr int SUPER_BS = 2 * 4 + 1;
+inline int64_t n_supers(int64_t T) { return (T + SUPER - 1) / SUPER; }
+__device__ __forceinline__ void super_box_add(unsigned int* super, int64_t tile, int dpad, int k,
+                                              float mn, float mx) {
+  unsigned int* sb = super + (tile / SUPER) * SUPER_BS;
+  if (k < dpad) {
+    atomicMax(&sb[k], ~ord_bits(mn));
+    atomicMax(&sb[dpad + k], ord_bits(mx));
+  } else {
+    atomicMax(&sb[2 * dpad], ord_bits(mx));
+  }
+}
 
 // ---- launchers (ds_tile.cu) ---------------------------------------------------
 // bbox (nullable): 8 uints {~ord lo[4], ord hi[4]} of the first min(d, 4) dimensions
@@ -200,8 +221,9 @@ cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, 
 // bounds_ready: lo / hi / maxnorm were filled by the spatial sort (SortBounds)
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
-                        int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
-                        unsigned long long* count, bool bounds_ready, cudaStream_t s);
+                        unsigned int* super, int32_t* flags, int32_t* partials,
+                        int32_t* total_kept, uint32_t* list, unsigned long long* count,
+                        bool bounds_ready, cudaStream_t s);
 // exclusive prefix sum of int32 data in place (3 kernels); *total = sum
 cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
                                   cudaStream_t s);
@@ -269,6 +291,7 @@ struct SortBounds {
   float* hi = nullptr;
   float* maxnorm = nullptr;  // T max squared norms
   float* blk = nullptr;      // 32-point block boxes (nullptr: skip)
+  unsigned int* super = nullptr;  // super-tile boxes, zeroed (nullptr: skip; d <= 4)
 };
 cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
                                 int32_t* perm, int32_t* inv, unsigned long long* keys,

@@ -70,11 +70,14 @@ __global__ void __launch_bounds__(RS_T) morton_kernel(
   hist[0][t] = 0;
   __syncthreads();
   const int bits = total_bits / kd;
-  const double levels = (double)((1ull << bits) - 1);
-  double lo[4], span[4];
+  const float levels = (float)((1u << bits) - 1);
+  // quantisation in float (any deterministic, monotone map is fine: the order only
+  // schedules work); the scale is computed once per CTA instead of a division per item
+  float lo[4], scale[4];
   for (int k = 0; k < kd; ++k) {
     lo[k] = unord(~lo_bits[k]);  // lo is stored inverted
-    span[k] = (double)unord(hi_bits[k]) - lo[k];
+    const float span = unord(hi_bits[k]) - lo[k];
+    scale[k] = span > 0.f ? levels / span : 0.f;
   }
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; ++r) {
@@ -82,8 +85,8 @@ __global__ void __launch_bounds__(RS_T) morton_kernel(
     if (i >= n) break;
     uint32_t q[4] = {0, 0, 0, 0};
     for (int k = 0; k < kd; ++k) {
-      double v = span[k] > 0 ? ((double)rec[i * S + k] - lo[k]) / span[k] * levels : 0.0;
-      v = v < 0 ? 0 : (v > levels ? levels : v);
+      float v = (rec[i * S + k] - lo[k]) * scale[k];
+      v = v < 0.f ? 0.f : (v > levels ? levels : v);
       q[k] = (v == v) ? (uint32_t)v : 0u;  // NaN -> 0
     }
     uint32_t key = 0;  // <= 24 bits
@@ -230,7 +233,8 @@ __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
 __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
     const float* __restrict__ rec, int64_t n, int S, int dpad, const int32_t* __restrict__ perm,
     float* __restrict__ out, float* __restrict__ lo,
-    float* __restrict__ hi, float* __restrict__ maxnorm, float* __restrict__ blk) {
+    float* __restrict__ hi, float* __restrict__ maxnorm, float* __restrict__ blk,
+    unsigned int* __restrict__ super) {
   griddep_wait();
   __shared__ float smn[TILE / 32], smx[TILE / 32];
   const int64_t tile = blockIdx.x;
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
       } else {
         maxnorm[tile] = mx;
       }
+      if (super) super_box_add(super, tile, dpad, k, mn, mx);
     }
     __syncthreads();
   }
@@ -335,7 +340,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   }
   if (bnd.lo) {
     e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(TILE), 0, s, rec, n, S, dp,
-                   (const int32_t*)perm, rec_sorted, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk);
+                   (const int32_t*)perm, rec_sorted, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk,
+                   dp <= 4 ? bnd.super : (unsigned int*)nullptr);
     if (e != cudaSuccess) return e;
   } else {
     const unsigned blocks = (unsigned)((n + 255) / 256);

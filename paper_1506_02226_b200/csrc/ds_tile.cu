@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ co
 // Per tile: coordinate bounding box (float32, exact) and max squared norm.
 __global__ void tile_bounds_kernel(const float* __restrict__ rec, int64_t n, int dpad, int S,
                                    float* __restrict__ lo, float* __restrict__ hi,
-                                   float* __restrict__ maxnorm) {
+                                   float* __restrict__ maxnorm, unsigned int* __restrict__ super) {
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * TILE;
   const int cnt = (int)min((int64_t)TILE, n - base);
@@ -976,6 +976,7 @@ __global__ void tile_bounds_kernel(const float* __restrict__ rec, int64_t n, int
       } else {
         maxnorm[tile] = mx;
       }
+      if (super) super_box_add(super, tile, dpad, k, mn, mx);
     }
     __syncthreads();
   }
@@ -1142,6 +1143,150 @@ __global__ void __launch_bounds__(CULL_T) cull_write_kernel(
   }
 }
 
+// keep_item's bound in float with directed rounding (every operation rounds toward a
+// smaller bound; see box_pairs), on box a = {alo, ahi, wa} and box b: the test of the
+// hierarchical culling, d <= 4. Exact culling as keep_item (never drops a pair whose
+// float32 result could be <= eps32).
+template <int DP>
+__device__ __forceinline__ bool keep_box(const float* alo, const float* ahi, float wa, const float* blo,
+                                         const float* bhi, float wb, float eps32, int formula) {
+  constexpr float u = 1.0f / 16777216.0f;
+  constexpr float C1 = 1.0f - 12.0f * DP * u - 1e-6f;                   // (1 - 12 DP u)(1 - 1e-12)
+  constexpr float C2 = 4.0f * (2.0f * DP + 3.0f) * u * 1.001f * 1.001f;  // 4 (2DP+3) u 1.001
+  float L = 0.f;
+#pragma unroll
+  for (int k = 0; k < DP; ++k) {
+    const float g = fmaxf(0.f, fmaxf(__fsub_rd(blo[k], ahi[k]), __fsub_rd(alo[k], bhi[k])));
+    L = __fadd_rd(L, __fmul_rd(g, g));
+  }
+  float bound = __fmul_rd(L, C1);
+  if (formula == DS_FORMULA_ALGEBRAIC) bound = __fsub_rd(bound, __fmul_ru(__fadd_ru(wa, wb), C2));
+  return !(bound > eps32);  // NaN bounds keep the pair
+}
+
+// Hierarchical row culling (d <= 4): a CTA per tile row a tests the super tiles at or
+// after a's first (one thread each), then one warp per kept super tile tests its 32
+// tiles b >= a — the kept pairs come out in item order (super tiles in order, tiles in
+// order within one), the same list as cull_rows / cull_write. write = false counts the
+// row's kept pairs (rowcnt), write = true writes them at the row's offset.
+template <int DP, bool WRITE>
+__global__ void __launch_bounds__(CULL_T) cull_super_kernel(
+    const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
+    const unsigned int* __restrict__ super, int64_t T, float eps32, int formula,
+    const uint32_t* __restrict__ unsafe_flag, int32_t* __restrict__ rowcnt, uint32_t* __restrict__ list,
+    int32_t* __restrict__ total_kept, unsigned long long* __restrict__ count) {
+  griddep_wait();
+  constexpr int W = CULL_T / 32;
+  __shared__ int red[W];
+  __shared__ int wsum[W];
+  __shared__ int ks[CULL_T];  // kept super tiles of the row, in order
+  __shared__ int nks;
+  const bool unsafe = *unsafe_flag != 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t NS = (T + SUPER - 1) / SUPER;
+  for (int64_t a = blockIdx.x; a < T; a += gridDim.x) {
+    float alo[DP], ahi[DP];
+#pragma unroll
+    for (int k = 0; k < DP; ++k) {
+      alo[k] = lo[a * DP + k];
+      ahi[k] = hi[a * DP + k];
+    }
+    const float wa = maxnorm[a];
+    int pos = 0;
+    if (WRITE) {  // kept pairs of the rows before a (O(T) reads, L2-resident)
+      int p = 0;
+      for (int64_t r = threadIdx.x; r < a; r += blockDim.x) p += rowcnt[r];
+      pos = block_sum(p, red);
+    }
+    int row_total = 0;
+    for (int64_t s0 = a / SUPER; s0 < NS; s0 += CULL_T) {  // super tiles, CULL_T at a time
+      const int64_t sb = s0 + threadIdx.x;
+      bool k = false;
+      if (sb < NS) {
+        if (unsafe) {
+          k = true;
+        } else {
+          const unsigned int* b = super + sb * SUPER_BS;
+          float blo[DP], bhi[DP];
+#pragma unroll
+          for (int q = 0; q < DP; ++q) {
+            blo[q] = unord_bits(~b[q]);
+            bhi[q] = unord_bits(b[DP + q]);
+          }
+          k = keep_box<DP>(alo, ahi, wa, blo, bhi, unord_bits(b[2 * DP]), eps32, formula);
+        }
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      __syncthreads();  // ks / wsum of the previous round are consumed
+      if (lane == 0) wsum[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, all = 0;
+      for (int w = 0; w < W; ++w) {
+        before += w < wid ? wsum[w] : 0;
+        all += wsum[w];
+      }
+      if (k) ks[before + __popc(bal & ((1u << lane) - 1u))] = (int)sb;
+      if (threadIdx.x == 0) nks = all;
+      __syncthreads();
+      const int nk = nks;
+      for (int i0 = 0; i0 < nk; i0 += W) {  // one warp per kept super tile
+        const int i = i0 + wid;
+        const int64_t b = i < nk ? (int64_t)ks[i] * SUPER + lane : T;
+        bool kt = false;
+        if (b < T && b >= a) {
+          if (unsafe || b == a) {
+            kt = true;
+          } else {
+            float blo[DP], bhi[DP];
+#pragma unroll
+            for (int q = 0; q < DP; ++q) {
+              blo[q] = lo[b * DP + q];
+              bhi[q] = hi[b * DP + q];
+            }
+            kt = keep_box<DP>(alo, ahi, wa, blo, bhi, maxnorm[b], eps32, formula);
+          }
+        }
+        const uint32_t tb = __ballot_sync(0xffffffffu, kt);
+        if (!WRITE) {
+          row_total += lane == 0 ? __popc(tb) : 0;
+        } else {
+          __syncthreads();
+          if (lane == 0) wsum[wid] = __popc(tb);
+          __syncthreads();
+          int bw = 0, aw = 0;
+          for (int w = 0; w < W; ++w) {
+            bw += w < wid ? wsum[w] : 0;
+            aw += wsum[w];
+          }
+          if (kt) list[pos + bw + __popc(tb & ((1u << lane) - 1u))] = ((uint32_t)a << 16) | (uint32_t)b;
+          pos += aw;
+        }
+      }
+    }
+    if (!WRITE) {
+      const int t = block_sum(row_total, red);
+      if (threadIdx.x == 0) rowcnt[a] = t;
+    } else if (a == T - 1 && threadIdx.x == 0) {
+      *total_kept = pos;
+      *count = (unsigned long long)pos;
+    }
+  }
+}
+
+template <int DP>
+cudaError_t launch_cull_super(const float* lo, const float* hi, const float* maxnorm,
+                              const unsigned int* super, int64_t T, float eps32, int formula,
+                              const uint32_t* unsafe_flag, int32_t* rowcnt, uint32_t* list,
+                              int32_t* total_kept, unsigned long long* count, cudaStream_t s) {
+  const unsigned g = (unsigned)std::min<int64_t>(T, 148 * 8);
+  cudaError_t e = launch_pdl(cull_super_kernel<DP, false>, dim3(g), dim3(CULL_T), 0, s, lo, hi,
+                             maxnorm, super, T, eps32, formula, unsafe_flag, rowcnt,
+                             (uint32_t*)nullptr, (int32_t*)nullptr, (unsigned long long*)nullptr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(cull_super_kernel<DP, true>, dim3(g), dim3(CULL_T), 0, s, lo, hi, maxnorm, super,
+                    T, eps32, formula, unsafe_flag, rowcnt, list, total_kept, count);
+}
+
 int pad_dim(int d) {
   if (d <= 4) return d;
   if (d <= 8) return 8;
@@ -1196,12 +1341,27 @@ cudaError_t launch_prep(const double* coords, int64_t n, int d, float* rec, uint
 
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
-                        int32_t* flags, int32_t* partials, int32_t* total_kept, uint32_t* list,
-                        unsigned long long* count, bool bounds_ready, cudaStream_t s) {
+                        unsigned int* super, int32_t* flags, int32_t* partials,
+                        int32_t* total_kept, uint32_t* list, unsigned long long* count,
+                        bool bounds_ready, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int64_t T = (n + TILE - 1) / TILE;
-  if (!bounds_ready) tile_bounds_kernel<<<(unsigned)T, 256, 0, s>>>(rec, n, dp, S, lo, hi, maxnorm);
+  if (dp > 4) super = nullptr;
+  if (!bounds_ready)
+    tile_bounds_kernel<<<(unsigned)T, 256, 0, s>>>(rec, n, dp, S, lo, hi, maxnorm, super);
+  if (super && T <= CULL_ROWS_MAX) {  // hierarchical: super tiles first (d <= 4)
+    switch (dp) {
+      case 1: return launch_cull_super<1>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
+                                          flags, list, total_kept, count, s);
+      case 2: return launch_cull_super<2>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
+                                          flags, list, total_kept, count, s);
+      case 3: return launch_cull_super<3>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
+                                          flags, list, total_kept, count, s);
+      default: return launch_cull_super<4>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
+                                           flags, list, total_kept, count, s);
+    }
+  }
   if (T <= CULL_ROWS_MAX) {  // rowcnt lives in the flags buffer (T <= T(T+1)/2 ints)
     const unsigned g = (unsigned)std::min<int64_t>(T, 148 * 8);
     cudaError_t e = launch_pdl(cull_rows_kernel, dim3(g), dim3(CULL_T), 0, s, (const float*)lo,
