@@ -7,7 +7,6 @@ For each kernel (in launch order): first and last block start after griddep_wait
 (i.e. after the predecessor completed), and the time until the next kernel's first
 block start — the kernel's share of the pipeline including its drain.
 """
-import collections
 import sys
 
 path = sys.argv[1]
@@ -22,17 +21,20 @@ for l in open(path):
         f, ln, blk, t = map(int, l.split())
         cur.append((f, ln, blk, t))
 rec = calls[-1]
-by = collections.OrderedDict()
+# launches in time order: consecutive records of the same kernel site (a kernel's blocks
+# stamp after griddepcontrol.wait, i.e. after its predecessor completed)
+runs = []
 for f, ln, blk, t in sorted(rec, key=lambda r: r[3]):
-    by.setdefault((f, ln), []).append(t)
-order = sorted(by.items(), key=lambda kv: min(kv[1]))
-t0 = min(order[0][1])
+    if runs and runs[-1][0] == (f, ln):
+        runs[-1][1].append(t)
+    else:
+        runs.append(((f, ln), [t]))
+t0 = min(runs[0][1])
 print(f"{len(calls)} calls; last call {len(rec)} block records")
 print(f"{'kernel':34s} {'blocks':>6s} {'first':>8s} {'last':>8s} {'to next':>8s}")
-tot = 0.0
-for i, ((f, ln), ts) in enumerate(order):
+for i, ((f, ln), ts) in enumerate(runs):
     first, last = (min(ts) - t0) / 1e3, (max(ts) - t0) / 1e3
-    nxt = (min(order[i + 1][1]) - t0) / 1e3 if i + 1 < len(order) else None
+    nxt = (min(runs[i + 1][1]) - t0) / 1e3 if i + 1 < len(runs) else None
     name = names.get(f"{f}:{ln}", f"{f}:{ln}")
     span = "" if nxt is None else f"{nxt - first:8.2f}"
     print(f"{name[:34]:34s} {len(ts):6d} {first:8.2f} {last:8.2f} {span}")
