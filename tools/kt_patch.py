@@ -42,6 +42,14 @@ __device__ unsigned long long* g_kt;  // per translation unit, set by ds_kt_set_
     if (i_ + 4 < {KT_CAP}u) {{ \\
       ::ds::kt::g_kt[2 + i_] = ((unsigned long long)KT_FILE << 48) | ((unsigned long long)__LINE__ << 32) | blockIdx.x; \\
       ::ds::kt::g_kt[3 + i_] = t_; }} }} }} while (0)""")
+hs = hs.replace("#define griddep_wait()", """#define KT_MARK(site) do { if (::ds::kt::g_kt) { unsigned long long t_; \\
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \\
+    const unsigned i_ = atomicAdd(reinterpret_cast<unsigned*>(::ds::kt::g_kt), 2u); \\
+    if (i_ + 4 < """ + str(KT_CAP) + """u) { \\
+      ::ds::kt::g_kt[2 + i_] = ((unsigned long long)KT_FILE << 48) | ((unsigned long long)(site) << 32) | \\
+                               (blockIdx.x * 32u + (threadIdx.x >> 5)); \\
+      ::ds::kt::g_kt[3 + i_] = t_; } } } while (0)
+#define griddep_wait()""", 1)
 open(h, "w").write(hs)
 
 for fi, f in enumerate(FILES):
@@ -51,6 +59,13 @@ for fi, f in enumerate(FILES):
     s = f"#define KT_FILE {fi}\n" + s + f"""
 extern "C" void ds_kt_set_{name}(void* p) {{ cudaMemcpyToSymbol(ds::kt::g_kt, &p, sizeof p); }}
 """
+    if f == "ds_tile.cu":  # per-warp end of the eps kernel: site 60000
+        anchor = """  flush();
+  if (lane == 0 && steps_done)"""
+        assert anchor in s
+        s = s.replace(anchor, """  flush();
+  if (lane == 0) KT_MARK(60000);
+  if (lane == 0 && steps_done)""", 1)
     if f == "ds_api.cu":
         decl = "".join(f'extern "C" void ds_kt_set_{g[3:-3]}(void* p);\n' for g in FILES)
         s = s.replace('#include "ds_internal.cuh"', '#include "ds_internal.cuh"\n#include <cstdio>\n#include <cstdlib>\n' + decl, 1)
@@ -91,15 +106,16 @@ if r.returncode:
 # kernel names by (file, line): the kernel enclosing each griddep_wait call
 names = {}
 import re
-for fi, f in enumerate(FILES):
-    lines = open(os.path.join(SRC, f)).read().split("\n")
+for fi, f in enumerate(FILES):  # line numbers of the patched copy (what __LINE__ saw)
+    lines = open(os.path.join(TMP, f)).read().split("\n")
     cur = None
     for ln, l in enumerate(lines, start=1):
         m = re.search(r"__global__ void(?: __launch_bounds__\([^)]*\))? (\w+)", l)
         if m:
             cur = m.group(1)
         if "griddep_wait();" in l and cur:
-            names[f"{fi}:{ln + 1}"] = cur  # +1: the KT_FILE line prepended
+            names[f"{fi}:{ln}"] = cur
+names["0:60000"] = "eps_warp_end"
 with open(os.path.join(ROOT, "variants", "kt_names.txt"), "w") as fo:
     for k, v in names.items():
         fo.write(f"{k} {v}\n")

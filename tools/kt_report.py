@@ -21,6 +21,8 @@ for l in open(path):
         f, ln, blk, t = map(int, l.split())
         cur.append((f, ln, blk, t))
 rec = calls[-1]
+ends = sorted(t for f, ln, blk, t in rec if ln == 60000)  # eps kernel warp ends
+rec = [r for r in rec if r[1] != 60000]
 # launches in time order: consecutive records of the same kernel site (a kernel's blocks
 # stamp after griddepcontrol.wait, i.e. after its predecessor completed)
 runs = []
@@ -38,3 +40,10 @@ for i, ((f, ln), ts) in enumerate(runs):
     name = names.get(f"{f}:{ln}", f"{f}:{ln}")
     span = "" if nxt is None else f"{nxt - first:8.2f}"
     print(f"{name[:34]:34s} {len(ts):6d} {first:8.2f} {last:8.2f} {span}")
+if ends:
+    import statistics
+    e0 = min(t for (f, ln), ts in runs if names.get(f"{f}:{ln}") == "eps_unit_kernel" for t in ts)
+    rel = [(t - e0) / 1e3 for t in ends]
+    q = lambda p: rel[min(len(rel) - 1, int(p * len(rel)))]
+    print(f"eps_unit_kernel warp ends (us after its first block): p10 {q(0.1):.1f} p50 {q(0.5):.1f} "
+          f"p90 {q(0.9):.1f} p99 {q(0.99):.1f} max {rel[-1]:.1f} ({len(rel)} warps)")
