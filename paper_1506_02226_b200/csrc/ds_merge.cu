@@ -544,9 +544,15 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
         const int k = hist[lp[u]];
         const uint32_t cross = um & ~M[k * WPR + w];
         if (!cross) continue;
-        uint32_t bits = 0;
-        for (int j = 0; j < ntrees; ++j)
-          if (cross & M[j * WPR + w]) bits |= 1u << j;
+        // the trees the word crosses into: per iteration the tree of its lowest remaining
+        // bit, whose columns are then removed (iterations = distinct crossed trees, not
+        // ntrees)
+        uint32_t bits = 0, rest = cross;
+        while (rest) {
+          const int j = hist[lp[w * 32 + __clz(rest)]];
+          bits |= 1u << j;
+          rest &= ~M[j * WPR + w];
+        }
         atomicOr(&adj[k], bits);
       }
       __syncthreads();

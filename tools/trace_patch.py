@@ -90,9 +90,9 @@ rep("""      __syncwarp();  // cols / groups / pair masks are rewritten by the n
 # union_diag: stamps after the setup, the word scatter and the column-minimum scan
 rep("""  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int base = (int)tile * TILE;""", """  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    unsigned long long t_start, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0; """ + GT + """(t_start));
+    unsigned long long t_start, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t4a = 0, t4b = 0, t4c = 0, t4d = 0; """ + GT + """(t_start));
 #define DT(msg, ...) if (tid == 0) { unsigned long long t_end; """ + GT + """(t_end)); \\
-    printf("DT %lld %llu %llu %llu %llu %llu %llu %llu " msg "\\n", (long long)tile, t_start, t1, t2, t3, t4, t5, t_end, __VA_ARGS__); }
+    printf("DT %lld %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu " msg "\\n", (long long)tile, t_start, t1, t2, t3, t4, t5, t_end, t4a, t4b, t4c, t4d, __VA_ARGS__); }
     const int base = (int)tile * TILE;""")
 rep("""    if (tid == 0) slot_root[0] = -1;  // atomicMax target of the single-root fast path
     __syncthreads();""", """    if (tid == 0) slot_root[0] = -1;  // atomicMax target of the single-root fast path
@@ -132,6 +132,32 @@ rep("""    __syncthreads();
     """ + GT + """(t5));
     {
       const int v = tid;""")
+
+# tree-merge sub-phases (slow tiles): slots assigned, tree masks, crossing scan, closure
+rep("""      if (k < 32) slot_root[k] = tid;    // slot -> root node
+    }
+    __syncthreads();""", """      if (k < 32) slot_root[k] = tid;    // slot -> root node
+    }
+    __syncthreads();
+    """ + GT + """(t4a));""")
+rep("""        if (is_core && (tid & 31) == __ffs(grp) - 1) M[key * WPR + (tid >> 5)] = __brev(grp);
+      }
+      __syncthreads();""", """        if (is_core && (tid & 31) == __ffs(grp) - 1) M[key * WPR + (tid >> 5)] = __brev(grp);
+      }
+      __syncthreads();
+      """ + GT + """(t4b));""")
+rep("""        atomicOr(&adj[k], bits);
+      }
+      __syncthreads();""", """        atomicOr(&adj[k], bits);
+      }
+      __syncthreads();
+      """ + GT + """(t4c));""")
+rep("""        adj[tid] = row;
+      }
+      __syncthreads();""", """        adj[tid] = row;
+      }
+      __syncthreads();
+      """ + GT + """(t4d));""")
 open(p, "w").write(s)
 os.makedirs(os.path.join(ROOT, "variants"), exist_ok=True)
 r = subprocess.run(["make", "-s", "-C", TMP, "OUT=" + os.path.join(ROOT, "variants", "trace.so"),

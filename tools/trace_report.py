@@ -28,7 +28,8 @@ if lt:
         print(f"  slow warp {blk[k]}.{w[k]} {dur[k]:.1f} us units {units[k]} shortcut {uni[k]} "
               f"full {full[k]} words {words[k]} links {links[k]}")
 if dt:
-    rows = [(int(x[0]), *map(int, x[1:8]), x[8], int(x[9]), int(x[10])) for x in dt]
+    sub = [list(map(int, x[8:12])) for x in dt]  # t4a..t4d of the tree merge
+    rows = [(int(x[0]), *map(int, x[1:8]), x[12], int(x[13]), int(x[14])) for x in dt]
     ts = np.array([r[1] for r in rows])
     keep = ts >= ts.max() - 5_000_000
     rows = [r for r, k in zip(rows, keep) if k]
@@ -44,6 +45,13 @@ if dt:
     for nm, sel in (("fast", fast), ("slow", ~fast)):
         if sel.any():
             print(f"    {nm}: median {np.median(ph[sel], axis=0).round(2)} p90 {np.percentile(ph[sel], 90, axis=0).round(2)}")
+    sub = [sb for sb, k in zip(sub, keep) if k]
+    sl = [(r, sb) for r, sb, f in zip(rows, sub, fast) if not f and sb[0]]
+    if sl:
+        seg = np.array([[sb[0] - r[5], sb[1] - sb[0], sb[2] - sb[1], sb[3] - sb[2], r[6] - sb[3]]
+                        for r, sb in sl]) / 1e3
+        print("  tree merge (slots, tree masks, crossing scan, closure, root update) median",
+              np.median(seg, axis=0).round(2), "p90", np.percentile(seg, 90, axis=0).round(2))
     ent = np.array([r[9] for r in rows])
     tr = np.array([r[10] for r in rows])
     print(f"  entries p50/max {np.percentile(ent, [50, 100])}, trees (slow) p50/90/max "
