@@ -56,8 +56,7 @@ constexpr int RS_MAXP = 3;              // passes (24-bit keys)
 __host__ __device__ inline int64_t rs_chunks(int64_t n) { return (n + RS_CHUNK - 1) / RS_CHUNK; }
 
 // Keys of chunk c (items c*CHUNK + r*256 + t) and the chunk's pass-0 digit counts
-// (counts0[d * nch + c]); the per-chunk counts of passes >= 1 are zeroed here (the
-// previous pass's radix_scatter adds to them once this kernel has completed).
+// (counts0[d * nch + c]).
 __global__ void __launch_bounds__(RS_T) morton_kernel(
     const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits, int npass,
     const unsigned int* __restrict__ lo_bits, const unsigned int* __restrict__ hi_bits,
@@ -96,17 +95,19 @@ __global__ void __launch_bounds__(RS_T) morton_kernel(
     atomicAdd(&hist[0][key & 255u], 1);
   }
   __syncthreads();
-  const int64_t stride = 256 * nch;  // counts of one pass
-  counts[(int64_t)t * nch + c] = hist[0][t];
-  for (int p = 1; p < npass; ++p) counts[p * stride + (int64_t)t * nch + c] = 0;
+  counts[(int64_t)t * nch + c] = hist[0][t];  // the next passes' rows: zeroed by digit_scan
 }
 
 // One CTA per digit d: exclusive scan over the chunks of the digit's counts (in
 // place) and the digit's total (totals[d]); the scatter adds the digit bases.
+// next (nullable): the next pass's counts, whose row d this CTA zeroes (coalesced; that
+// pass's radix_scatter of this pass adds to them once this kernel has completed).
 __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ counts,
                                                           int32_t* __restrict__ totals,
-                                                          int64_t nch) {
+                                                          int64_t nch, int32_t* __restrict__ next) {
   griddep_wait();
+  if (next)
+    for (int64_t c = threadIdx.x; c < nch; c += RS_T) next[(int64_t)blockIdx.x * nch + c] = 0;
   __shared__ int warp_sum[RS_T / 32];
   const int d = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   int carry = 0;
@@ -225,12 +226,16 @@ __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
   for (int v = 0; v < S / 4; ++v) dst[v] = src[v];
 }
 
-// permute_kernel fused with the culling bounds (stage 1+2 with culling on): one CTA
-// per 512-point tile copies its records into sorted order, then reduces per
-// 32-point block (one warp) the box and max squared norm (blk, the layout of
-// block_bounds_kernel in ds_tile.cu; nullptr: skip) and per tile the box and max
-// norm (lo / hi / maxnorm, the layout of tile_bounds_kernel).
-__global__ void __launch_bounds__(TILE) permute_bounds_kernel(
+// permute_kernel fused with the culling bounds (stage 1+2 with culling on): one CTA of
+// PB_T threads per 512-point tile (4 points per thread, their loads in flight
+// together: at C5's 3,907 tiles two resident waves instead of seven of 512-thread
+// CTAs) copies its records into sorted order, then reduces per 32-point block (one
+// warp and round) the box and max squared norm (blk, the layout of block_bounds_kernel
+// in ds_tile.cu; nullptr: skip) and per tile the box and max norm (lo / hi / maxnorm,
+// the layout of tile_bounds_kernel), and adds the tile box to its super tile's.
+constexpr int PB_T = 128;
+constexpr int PB_P = TILE / PB_T;
+__global__ void __launch_bounds__(PB_T) permute_bounds_kernel(
     const float* __restrict__ rec, int64_t n, int S, int dpad, const int32_t* __restrict__ perm,
     float* __restrict__ out, float* __restrict__ lo,
     float* __restrict__ hi, float* __restrict__ maxnorm, float* __restrict__ blk,
@@ -238,40 +243,52 @@ __global__ void __launch_bounds__(TILE) permute_bounds_kernel(
   griddep_wait();
   __shared__ float smn[TILE / 32], smx[TILE / 32];
   const int64_t tile = blockIdx.x;
-  const int64_t s = tile * TILE + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool valid = s < n;
-  if (valid) {
-    const int64_t o = perm[s];
-    const float4* src = reinterpret_cast<const float4*>(rec + o * S);
-    float4* dst = reinterpret_cast<float4*>(out + s * S);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int64_t o[PB_P];
+#pragma unroll
+  for (int j = 0; j < PB_P; ++j) {
+    const int64_t sj = tile * TILE + j * PB_T + t;
+    o[j] = sj < n ? perm[sj] : -1;
+  }
+#pragma unroll
+  for (int j = 0; j < PB_P; ++j) {
+    if (o[j] < 0) continue;
+    const int64_t sj = tile * TILE + j * PB_T + t;
+    const float4* src = reinterpret_cast<const float4*>(rec + o[j] * S);
+    float4* dst = reinterpret_cast<float4*>(out + sj * S);
     for (int v = 0; v < S / 4; ++v) dst[v] = src[v];
   }
-  const int64_t wb = tile * (TILE / 32) + warp;  // global 32-point block
-  const bool wvalid = wb * 32 < n;
   const int BS = 2 * dpad + 1;
   for (int k = 0; k <= dpad; ++k) {  // k == dpad: the norm column
-    const float v = valid ? out[s * S + k] : 0.f;
-    float mn = valid ? v : INFINITY, mx = valid ? v : -INFINITY;
 #pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    }
-    if (lane == 0) {
-      if (blk && wvalid) {
-        if (k < dpad) {
-          blk[wb * BS + k] = mn;
-          blk[wb * BS + dpad + k] = mx;
-        } else {
-          blk[wb * BS + 2 * dpad] = mx;
-        }
+    for (int j = 0; j < PB_P; ++j) {  // block j * (PB_T / 32) + warp of the tile
+      const int64_t sj = tile * TILE + j * PB_T + t;
+      const bool valid = o[j] >= 0;
+      const float v = valid ? out[sj * S + k] : 0.f;
+      float mn = valid ? v : INFINITY, mx = valid ? v : -INFINITY;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
       }
-      smn[warp] = mn;
-      smx[warp] = mx;
+      const int bw = j * (PB_T / 32) + warp;
+      const int64_t wb = tile * (TILE / 32) + bw;  // global 32-point block
+      if (lane == 0) {
+        if (blk && wb * 32 < n) {
+          if (k < dpad) {
+            blk[wb * BS + k] = mn;
+            blk[wb * BS + dpad + k] = mx;
+          } else {
+            blk[wb * BS + 2 * dpad] = mx;
+          }
+        }
+        smn[bw] = mn;
+        smx[bw] = mx;
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (t == 0) {
+      float mn = smn[0], mx = smx[0];
       for (int w = 1; w < TILE / 32; ++w) {
         mn = fminf(mn, smn[w]);
         mx = fmaxf(mx, smx[w]);
@@ -323,7 +340,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   const int32_t* vin = nullptr;
   for (int p = 0; p < npass; ++p) {
     int32_t* cp = counts + (int64_t)p * 256 * nch;
-    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp, totals + p * 256, nch);
+    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp, totals + p * 256, nch,
+                   p + 1 < npass ? counts + (int64_t)(p + 1) * 256 * nch : (int32_t*)nullptr);
     if (e != cudaSuccess) return e;
     const bool last = p == npass - 1;
     uint32_t* kout = (p & 1) ? kA : kB;
@@ -339,7 +357,7 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
     vin = vout;
   }
   if (bnd.lo) {
-    e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(TILE), 0, s, rec, n, S, dp,
+    e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(PB_T), 0, s, rec, n, S, dp,
                    (const int32_t*)perm, rec_sorted, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk,
                    dp <= 4 ? bnd.super : (unsigned int*)nullptr);
     if (e != cudaSuccess) return e;

@@ -888,8 +888,37 @@ __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ co
   float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i_gen = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d == 2 && dpad == 2 && S == 4 && (reinterpret_cast<uintptr_t>(coords) & 15u) == 0) {
+    // 2-D: one 16-byte load and one 16-byte store per point, four points per thread in
+    // flight (the general loop below is a chain of dependent loads per point)
+    const double2* src2 = reinterpret_cast<const double2*>(coords);
+    float4* dst4 = reinterpret_cast<float4*>(rec);
+    for (; i_gen < n; i_gen += 4 * stride) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i_gen + u * stride;
+        v[u] = i < n ? src2[i] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i_gen + u * stride;
+        if (i >= n) continue;
+        const float x = __double2float_rn(v[u].x), y = __double2float_rn(v[u].y);  // kernels.py:148-150
+        const float p = __fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y));  // kernels.py:388-391
+        dst4[i] = make_float4(x, y, p, 0.f);
+        mn[0] = fminf(mn[0], x);
+        mx[0] = fmaxf(mx[0], x);
+        mn[1] = fminf(mn[1], y);
+        mx[1] = fmaxf(mx[1], y);
+        bad |= !(fabsf(x) <= SAFE_ABS) || !(fabsf(y) <= SAFE_ABS);
+        if (cnt) cnt[i] = 0;
+      }
+    }
+  }
+  for (int64_t i = i_gen; i < n; i += stride) {
     const double* src = coords + i * d;
     float* dst = rec + i * S;
     float p = 0.f;
