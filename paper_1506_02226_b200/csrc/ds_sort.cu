@@ -46,17 +46,17 @@ __device__ __forceinline__ float unord(unsigned int u) {
 }
 
 constexpr int RS_T = 256;               // threads per radix CTA
-#ifndef DS_RS_ITEMS
-#define DS_RS_ITEMS 2
-#endif
-constexpr int RS_ITEMS = DS_RS_ITEMS;   // items per thread
-constexpr int RS_CHUNK = RS_T * RS_ITEMS;  // items per chunk (one CTA)
 constexpr int RS_MAXP = 3;              // passes (24-bit keys)
-
-__host__ __device__ inline int64_t rs_chunks(int64_t n) { return (n + RS_CHUNK - 1) / RS_CHUNK; }
+// items per thread (chunk = RS_T * items per CTA): 2 up to 2^18 points (more, shorter
+// CTAs: C2 best), 4 above (C5: fewer per-chunk counts and CTA waves, -17 us)
+inline int rs_items(int64_t n) { return n <= (1 << 18) ? 2 : 4; }
+__host__ __device__ inline int64_t rs_chunks(int64_t n, int items) {
+  return (n + RS_T * items - 1) / (RS_T * items);
+}
 
 // Keys of chunk c (items c*CHUNK + r*256 + t) and the chunk's pass-0 digit counts
 // (counts0[d * nch + c]).
+template <int RS_ITEMS>
 __global__ void __launch_bounds__(RS_T) morton_kernel(
     const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits, int npass,
     const unsigned int* __restrict__ lo_bits, const unsigned int* __restrict__ hi_bits,
@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(RS_T) morton_kernel(
   griddep_wait();
   __shared__ int hist[1][256];
   const int t = threadIdx.x;
-  const int64_t nch = rs_chunks(n);
+  constexpr int RS_CHUNK = RS_T * RS_ITEMS;
+  const int64_t nch = rs_chunks(n, RS_ITEMS);
   const int64_t c = blockIdx.x;
   hist[0][t] = 0;
   __syncthreads();
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(RS_T) digit_scan_kernel(int32_t* __restrict__ 
 // implicit = index on pass 0). Items are ranked in index order; on the last pass the
 // permutation goes to perm / inv, otherwise keys / values to the output arrays and the
 // next pass's digit is counted for the output chunk.
+template <int RS_ITEMS>
 __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(
     int64_t n, int shift, const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
     const int32_t* __restrict__ offs, uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
@@ -151,7 +153,8 @@ __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(
   __shared__ int wsum[RS_T / 32];
   __shared__ int wcnt[2][RS_T / 32][256];  // double-buffered over the rounds
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t nch = rs_chunks(n);
+  constexpr int RS_CHUNK = RS_T * RS_ITEMS;
+  const int64_t nch = rs_chunks(n, RS_ITEMS);
   const int64_t c = blockIdx.x;
   {  // digit base = exclusive scan of the digit totals, plus this chunk's offset
     const int x = totals[t];
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(PB_T) permute_bounds_kernel(
 }  // namespace
 
 size_t sort_temp_bytes(int64_t n) {
-  return ((size_t)RS_MAXP * 256 * rs_chunks(n) + RS_MAXP * 256) * 4;  // counts + totals
+  return ((size_t)RS_MAXP * 256 * rs_chunks(n, rs_items(n)) + RS_MAXP * 256) * 4;  // counts + totals
 }
 
 cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_sorted,
@@ -323,7 +326,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   const int kb = key_bits(n, kd);
   const int end_bit = (kb / kd) * kd;
   const int npass = (end_bit + 7) / 8;
-  const int64_t nch = rs_chunks(n);
+  const int items = rs_items(n);
+  const int64_t nch = rs_chunks(n, items);
   if (temp_bytes < sort_temp_bytes(n)) return cudaErrorInvalidValue;
   int32_t* counts = reinterpret_cast<int32_t*>(temp);
   int32_t* totals = counts + (int64_t)RS_MAXP * 256 * nch;  // per pass, written by the scans
@@ -332,7 +336,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   uint32_t* kB = kA + n;
   int32_t* vA = idx;
   int32_t* vB = reinterpret_cast<int32_t*>(keys_alt);
-  cudaError_t e = launch_pdl(morton_kernel, dim3((unsigned)nch), dim3(RS_T), 0, s, rec, n, S, kd, kb,
+  cudaError_t e = launch_pdl(items == 2 ? morton_kernel<2> : morton_kernel<4>, dim3((unsigned)nch),
+                             dim3(RS_T), 0, s, rec, n, S, kd, kb,
                              npass, (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA,
                              counts);
   if (e != cudaSuccess) return e;
@@ -346,7 +351,8 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
     const bool last = p == npass - 1;
     uint32_t* kout = (p & 1) ? kA : kB;
     int32_t* vout = (p & 1) ? vA : vB;
-    e = launch_pdl(radix_scatter_kernel, dim3((unsigned)nch), dim3(RS_T), 0, s, n, 8 * p, kin, vin,
+    e = launch_pdl(items == 2 ? radix_scatter_kernel<2> : radix_scatter_kernel<4>, dim3((unsigned)nch),
+                   dim3(RS_T), 0, s, n, 8 * p, kin, vin,
                    (const int32_t*)cp, last ? (uint32_t*)nullptr : kout,
                    last ? (int32_t*)nullptr : vout,
                    last ? (int32_t*)nullptr : counts + (int64_t)(p + 1) * 256 * nch,
