@@ -127,12 +127,14 @@ class ClockSampler:
 
 def tile_traffic(config: str):
     """DRAM bytes per launch of the eps-tile kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_tile_traffic.json")) as fh:
-            t = json.load(fh)[config]
-        return t["dram_read_bytes"] + t["dram_write_bytes"]
-    except (OSError, KeyError, ValueError):
-        return None
+    for path in (("profiles", "r02", "tile_traffic.json"), ("profiles", "r01_tile_traffic.json")):
+        try:
+            with open(os.path.join(ROOT, *path)) as fh:
+                t = json.load(fh)[config]
+            return t["dram_read_bytes"] + t["dram_write_bytes"]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def golden_labels(config: str):
@@ -404,7 +406,7 @@ def run_b200(args):
         "roofline": {"bound": "fp32", "kernel": "eps_unit_kernel", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": tile_traffic(args.config),
-                     "traffic_source": "dram__bytes_read+write per launch, profiles/r01_tile_traffic.json",
+                     "traffic_source": "dram__bytes_read+write per launch, profiles/r02/tile_traffic.json",
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz "
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
                      "ops_per_pair": ops, "pairs_per_launch": pairs,
