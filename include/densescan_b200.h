@@ -114,9 +114,14 @@ void ds_ctx_destroy(ds_ctx* ctx);
  * DS_OPT_TEST_CAPACITY (default 0; test hook): > 0 starts the next stage 1+2 from
  * a unit-list and adjacency-word capacity of `value` entries and at most doubles it
  * per re-run, so one call walks through many capacity grow steps. Every launch that
- * overflowed is discarded and re-run; a call never returns results from one. */
+ * overflowed is discarded and re-run; a call never returns results from one.
+ * DS_OPT_STABLE_ORDER (default 0): with 0, inputs of 1-2 dimensions up to 2^18 points
+ * take the spatial order from a counting sort whose order among points of the same
+ * grid cell is arbitrary (the work counters may differ between calls; labels, counts
+ * and bits never do); 1 always uses the stable radix sort (the multi-GPU shard stages
+ * always do: every rank must build the same order). */
 enum { DS_OPT_TILE_CULL = 1, DS_OPT_SPATIAL_SORT = 2, DS_OPT_CUDA_GRAPH = 3, DS_OPT_EVENT_TIMING = 4,
-       DS_OPT_TEST_CAPACITY = 5 };
+       DS_OPT_TEST_CAPACITY = 5, DS_OPT_STABLE_ORDER = 6 };
 ds_status ds_ctx_set_option(ds_ctx* ctx, int32_t option, int64_t value);
 int64_t ds_ctx_get_option(ds_ctx* ctx, int32_t option);
 

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 DS_OK, DS_EINVAL, DS_ECAPACITY, DS_ECUDA, DS_EINCONSISTENT, DS_ENCCL = range(6)
 DS_OPT_TILE_CULL, DS_OPT_SPATIAL_SORT, DS_OPT_CUDA_GRAPH, DS_OPT_EVENT_TIMING = 1, 2, 3, 4
 DS_OPT_TEST_CAPACITY = 5
+DS_OPT_STABLE_ORDER = 6
 FORMULA_DIRECT, FORMULA_ALGEBRAIC = 0, 1
 
 # every symbol the header declares; tests/test_abi.py checks the .so exports them
@@ -227,6 +228,13 @@ class Context:
         """Test hook: start the next stage 1+2 from `entries` unit-list / word slots and
         at most double them per re-run (0: normal sizing)."""
         raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_TEST_CAPACITY, int(entries)),
+                  self.lib)
+
+    def set_stable_order(self, on: bool) -> None:
+        """DS_OPT_STABLE_ORDER: always the stable radix sort for the spatial order (the
+        default counting sort of small 1-2-D inputs orders points of one grid cell
+        arbitrarily; results are identical, work counters may differ between calls)."""
+        raise_for(self.lib.ds_ctx_set_option(self.handle, DS_OPT_STABLE_ORDER, 1 if on else 0),
                   self.lib)
 
     def configure(self, prune: bool = True, spatial_order: bool = True) -> None:

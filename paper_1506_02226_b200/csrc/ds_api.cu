@@ -79,7 +79,14 @@ inline int link_tab_bits(int64_t n) {
 inline size_t zr_links(int64_t n) { return zr_round(zr_scan(n) + (size_t)scan_partials_len(n) * 4); }
 // the super-tile boxes of the hierarchical culling (d <= 4)
 inline size_t zr_super(int64_t n) { return zr_round(zr_links(n) + ((size_t)8 << link_tab_bits(n))); }
-inline size_t zr_bytes(int64_t n) { return zr_super(n) + (size_t)n_supers(n_tiles(n)) * SUPER_BS * 4; }
+// the counting sort's 65536 cell counters (inputs up to 2^18 points)
+inline size_t zr_bins(int64_t n) {
+  return zr_round(zr_super(n) + (size_t)n_supers(n_tiles(n)) * SUPER_BS * 4);
+}
+inline size_t zr_bytes(int64_t n) {
+  return zr_bins(n) + (n <= ((int64_t)1 << 18) ? (size_t)SORT_BINS * 4 + scan_zeroed_bytes(SORT_BINS)
+                                                : 0);
+}
 
 }  // namespace
 
@@ -104,6 +111,7 @@ struct ds_ctx {
   bool stamp_timing = false;  // stage timings from device stamps: no events inside
   int sort = 1;          // DS_OPT_SPATIAL_SORT
   int event_timing = 0;  // DS_OPT_EVENT_TIMING
+  int stable = 0;        // DS_OPT_STABLE_ORDER
   bool sorted = false;   // perm / inv describe the last stage 1+2
   unsigned long long words_cap = 0;  // in words (8-byte records)
   unsigned long long units_cap = 0;  // culled unit list capacity (units)
@@ -372,6 +380,10 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
                               (int32_t*)c->inv.p, (unsigned long long*)c->keys.p,
                               (unsigned long long*)c->keys_alt.p, (int32_t*)c->kidx.p,
                               c->sort_temp.p, c->sort_temp.bytes, bbox, bnd,
+                              // one GPU: the counting sort where it applies (16-bit keys)
+                              (world == 1 && !c->stable && n <= ((int64_t)1 << 18))
+                                  ? (unsigned int*)((char*)c->scalars.p + zr_bins(n))
+                                  : nullptr,
                               s));
     rec = (const float*)c->rec_sorted.p;
     c->sorted = true;
@@ -618,7 +630,8 @@ ds_status pipeline(ds_ctx* c, const double* d_coords, int64_t n, int d, double e
     key[0] = (unsigned long long)n;
     key[1] = (unsigned long long)d | ((unsigned long long)formula << 8) |
              ((unsigned long long)c->cull << 16) | ((unsigned long long)c->sort << 17) |
-             ((unsigned long long)c->event_timing << 18) | 1ull << 40;
+             ((unsigned long long)c->event_timing << 18) | ((unsigned long long)c->stable << 19) |
+             1ull << 40;
     key[2] = eps_bits;
     key[3] = (unsigned long long)min_pts;
     key[4] = (unsigned long long)(uintptr_t)d_coords;
@@ -985,6 +998,10 @@ ds_status ds_ctx_set_option(ds_ctx* c, int32_t option, int64_t value) {
     c->event_timing = value ? 1 : 0;
     return DS_OK;
   }
+  if (option == DS_OPT_STABLE_ORDER) {
+    c->stable = value ? 1 : 0;
+    return DS_OK;
+  }
   if (option == DS_OPT_TEST_CAPACITY) {
     if (value < 0) {
       set_error("DS_OPT_TEST_CAPACITY: value must be >= 0");
@@ -1009,6 +1026,7 @@ int64_t ds_ctx_get_option(ds_ctx* c, int32_t option) {
   if (c && option == DS_OPT_CUDA_GRAPH) return c->use_graph;
   if (c && option == DS_OPT_EVENT_TIMING) return c->event_timing;
   if (c && option == DS_OPT_TEST_CAPACITY) return c->test_cap;
+  if (c && option == DS_OPT_STABLE_ORDER) return c->stable;
   return -1;
 }
 

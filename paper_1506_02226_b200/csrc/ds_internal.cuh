@@ -297,7 +297,15 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
                                 int32_t* perm, int32_t* inv, unsigned long long* keys,
                                 unsigned long long* keys_alt, int32_t* idx, void* temp,
                                 size_t temp_bytes, unsigned int* bbox, const SortBounds& bnd,
-                                cudaStream_t s);
+                                unsigned int* bins, cudaStream_t s);
+// bins (nullable, 65536 zeroed words): with 16-bit keys a counting sort whose order
+// within a key is arbitrary (one GPU); nullptr: the stable radix sort (same order on
+// every rank)
+constexpr int SORT_BINS = 1 << 16;
+// in-place exclusive scan of n int32 (decoupled look-back) whose look-back state of
+// scan_zeroed_bytes(n) bytes is zeroed by the caller (the per-call zero region)
+cudaError_t launch_scan_zeroed(int32_t* data, int64_t n, void* state, cudaStream_t s);
+size_t scan_zeroed_bytes(int64_t n);
 cudaError_t launch_bswap_rows(uint32_t* bits32, int64_t n, int64_t stride_words, cudaStream_t s);
 
 // ---- Warshall backend building blocks (ds_closure.cu) -----------------------------

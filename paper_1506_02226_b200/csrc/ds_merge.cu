@@ -1316,6 +1316,15 @@ cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, i
   return cudaGetLastError();
 }
 
+cudaError_t launch_scan_zeroed(int32_t* data, int64_t n, void* state, cudaStream_t s) {
+  const int64_t tiles = (n + SCAN_BLK - 1) / SCAN_BLK;
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(state);
+  return launch_pdl(scan_lookback_kernel<ScanInPlace>, dim3((unsigned)tiles), dim3(SCAN_T), 0, s,
+                    ScanInPlace{data}, data, n, reinterpret_cast<unsigned int*>(st), st + 1,
+                    reinterpret_cast<int32_t*>(st + 1 + tiles));
+}
+size_t scan_zeroed_bytes(int64_t n) { return (size_t)((n + SCAN_BLK - 1) / SCAN_BLK + 2) * 8; }
+
 cudaError_t launch_counts_i64(const int32_t* cnt, int64_t n, const int32_t* perm, int64_t* out,
                               cudaStream_t s) {
   counts_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(cnt, n, perm, out);

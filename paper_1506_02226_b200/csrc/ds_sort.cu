@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "ds_internal.cuh"
 
 namespace ds {
@@ -219,6 +221,72 @@ __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(
   }
 }
 
+// ---- counting sort on 16-bit keys (one GPU): the order within a key is arbitrary ----
+// The key grid cell (~1 point per cell at n <= 2^18) is the unit of locality; the order
+// of the points inside a cell does not matter for the tiles' compactness, and labels do
+// not depend on the order at all. Three kernels instead of the radix
+// sort's five: keys + a global histogram over the 65536 cells, a look-back exclusive
+// scan of it (16 CTAs), and a scatter with one atomic per (warp, cell) group. bins is
+// followed by the scan's look-back state; both zeroed per call.
+constexpr int CS_BINS = 1 << 16;
+
+__global__ void __launch_bounds__(RS_T) morton_count_kernel(
+    const float* __restrict__ rec, int64_t n, int S, int kd, int total_bits,
+    const unsigned int* __restrict__ lo_bits, const unsigned int* __restrict__ hi_bits,
+    uint32_t* __restrict__ keys, unsigned int* __restrict__ bins) {
+  griddep_wait();
+  const int bits = total_bits / kd;
+  const float levels = (float)((1u << bits) - 1);
+  float lo[4], scale[4];
+  for (int k = 0; k < kd; ++k) {
+    lo[k] = unord(~lo_bits[k]);  // lo is stored inverted
+    const float span = unord(hi_bits[k]) - lo[k];
+    scale[k] = span > 0.f ? levels / span : 0.f;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    uint32_t key = 0xffffffffu;
+    if (i < n) {
+      uint32_t q[4] = {0, 0, 0, 0};
+      for (int k = 0; k < kd; ++k) {
+        float v = (rec[i * S + k] - lo[k]) * scale[k];
+        v = v < 0.f ? 0.f : (v > levels ? levels : v);
+        q[k] = (v == v) ? (uint32_t)v : 0u;  // NaN -> 0
+      }
+      key = 0;
+      for (int b = bits - 1; b >= 0; --b)
+        for (int k = 0; k < kd; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
+      keys[i] = key;
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (i < n && lane == __ffs(grp) - 1) atomicAdd(&bins[key], (unsigned int)__popc(grp));
+  }
+}
+
+// positions: one atomic per (warp, cell) group on the cell's running start
+__global__ void __launch_bounds__(RS_T) count_scatter_kernel(int64_t n, const uint32_t* __restrict__ keys,
+                                                             unsigned int* __restrict__ bins,
+                                                             int32_t* __restrict__ perm,
+                                                             int32_t* __restrict__ inv) {
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint32_t key = i < n ? keys[i] : 0xffffffffu;
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(grp) - 1;
+    unsigned int base = 0;
+    if (i < n && lane == leader) base = atomicAdd(&bins[key], (unsigned int)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (i < n) {
+      const int64_t pos = (int64_t)base + __popc(grp & ((1u << lane) - 1u));
+      perm[pos] = (int32_t)i;
+      inv[i] = (int32_t)pos;
+    }
+  }
+}
+
 __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
                                const int32_t* __restrict__ perm, float* __restrict__ out) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -318,7 +386,7 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
                                 int32_t* perm, int32_t* inv, unsigned long long* keys,
                                 unsigned long long* keys_alt, int32_t* idx, void* temp,
                                 size_t temp_bytes, unsigned int* bbox, const SortBounds& bnd,
-                                cudaStream_t s) {
+                                unsigned int* bins, cudaStream_t s) {
   const int dp = padded_dim(d);
   const int S = rec_stride(d);
   const int kd = d < 4 ? d : 4;
@@ -336,31 +404,44 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
   uint32_t* kB = kA + n;
   int32_t* vA = idx;
   int32_t* vB = reinterpret_cast<int32_t*>(keys_alt);
-  cudaError_t e = launch_pdl(items == 2 ? morton_kernel<2> : morton_kernel<4>, dim3((unsigned)nch),
-                             dim3(RS_T), 0, s, rec, n, S, kd, kb,
-                             npass, (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA,
-                             counts);
-  if (e != cudaSuccess) return e;
-  const uint32_t* kin = kA;
-  const int32_t* vin = nullptr;
-  for (int p = 0; p < npass; ++p) {
-    int32_t* cp = counts + (int64_t)p * 256 * nch;
-    e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp, totals + p * 256, nch,
-                   p + 1 < npass ? counts + (int64_t)(p + 1) * 256 * nch : (int32_t*)nullptr);
+  cudaError_t e = cudaSuccess;
+  if (bins && kb == 16) {  // counting sort (zeroed bins): keys + histogram, scan, scatter
+    const unsigned g = (unsigned)std::min<int64_t>((n + RS_T - 1) / RS_T, 148 * 8);
+    e = launch_pdl(morton_count_kernel, dim3(g), dim3(RS_T), 0, s, rec, n, S, kd, kb,
+                   (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA, bins);
     if (e != cudaSuccess) return e;
-    const bool last = p == npass - 1;
-    uint32_t* kout = (p & 1) ? kA : kB;
-    int32_t* vout = (p & 1) ? vA : vB;
-    e = launch_pdl(items == 2 ? radix_scatter_kernel<2> : radix_scatter_kernel<4>, dim3((unsigned)nch),
-                   dim3(RS_T), 0, s, n, 8 * p, kin, vin,
-                   (const int32_t*)cp, last ? (uint32_t*)nullptr : kout,
-                   last ? (int32_t*)nullptr : vout,
-                   last ? (int32_t*)nullptr : counts + (int64_t)(p + 1) * 256 * nch,
-                   last ? perm : (int32_t*)nullptr, last ? inv : (int32_t*)nullptr,
-                   (const int32_t*)(totals + p * 256));
+    e = launch_scan_zeroed(reinterpret_cast<int32_t*>(bins), CS_BINS, bins + CS_BINS, s);
     if (e != cudaSuccess) return e;
-    kin = kout;
-    vin = vout;
+    e = launch_pdl(count_scatter_kernel, dim3(g), dim3(RS_T), 0, s, n, (const uint32_t*)kA, bins, perm,
+                   inv);
+    if (e != cudaSuccess) return e;
+  } else {  // stable LSD radix sort (deterministic order: every rank the same)
+    e = launch_pdl(items == 2 ? morton_kernel<2> : morton_kernel<4>, dim3((unsigned)nch),
+                               dim3(RS_T), 0, s, rec, n, S, kd, kb,
+                               npass, (const unsigned int*)bbox, (const unsigned int*)(bbox + 4), kA,
+                               counts);
+    if (e != cudaSuccess) return e;
+    const uint32_t* kin = kA;
+    const int32_t* vin = nullptr;
+    for (int p = 0; p < npass; ++p) {
+      int32_t* cp = counts + (int64_t)p * 256 * nch;
+      e = launch_pdl(digit_scan_kernel, dim3(256), dim3(RS_T), 0, s, cp, totals + p * 256, nch,
+                     p + 1 < npass ? counts + (int64_t)(p + 1) * 256 * nch : (int32_t*)nullptr);
+      if (e != cudaSuccess) return e;
+      const bool last = p == npass - 1;
+      uint32_t* kout = (p & 1) ? kA : kB;
+      int32_t* vout = (p & 1) ? vA : vB;
+      e = launch_pdl(items == 2 ? radix_scatter_kernel<2> : radix_scatter_kernel<4>, dim3((unsigned)nch),
+                     dim3(RS_T), 0, s, n, 8 * p, kin, vin,
+                     (const int32_t*)cp, last ? (uint32_t*)nullptr : kout,
+                     last ? (int32_t*)nullptr : vout,
+                     last ? (int32_t*)nullptr : counts + (int64_t)(p + 1) * 256 * nch,
+                     last ? perm : (int32_t*)nullptr, last ? inv : (int32_t*)nullptr,
+                     (const int32_t*)(totals + p * 256));
+      if (e != cudaSuccess) return e;
+      kin = kout;
+      vin = vout;
+    }
   }
   if (bnd.lo) {
     e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(PB_T), 0, s, rec, n, S, dp,

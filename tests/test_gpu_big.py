@@ -155,9 +155,35 @@ def test_spatial_sort_is_the_stable_key_order(ds, name, pairs, tiles):
     for _ in range(2):
         ctx = ds._native.Context(0)
         try:
+            ctx.set_stable_order(True)  # the radix sort (C2 would take the counting sort)
             for _ in range(2):
                 _, _, t = ctx.run_dbscan(pts.coords_aos, params.eps_sq, cfg.min_pts, 1, MEM_CAP)
                 seen.add((t.pairs_evaluated, t.tiles_total))
         finally:
             ctx.close()
     assert seen == {(pairs, tiles)}
+
+
+def test_counting_sort_order_gives_identical_results(ds):
+    """C2 takes the counting-sort spatial order by default (arbitrary order inside a grid
+    cell) and the stable radix sort with DS_OPT_STABLE_ORDER: labels and counts are
+    identical (the reference's), only the schedule may differ."""
+    cfg = ds.CONFIGS["C2"]
+    pts = cfg.points()
+    params = ds.validate_params(cfg.eps, cfg.min_pts)
+    out = {}
+    for stable in (False, True):
+        ctx = ds._native.Context(0)
+        try:
+            ctx.set_stable_order(stable)
+            for _ in range(3):  # eager, recorded, replayed
+                labels, counts, t = ctx.run_dbscan(pts.coords_aos, params.eps_sq, cfg.min_pts, 1,
+                                                   MEM_CAP, want_counts=True)
+                out.setdefault(stable, []).append((labels.copy(), counts.copy()))
+        finally:
+            ctx.close()
+    ref_labels, ref_counts = out[True][0]
+    for stable in (False, True):
+        for labels, counts in out[stable]:
+            assert np.array_equal(labels, ref_labels)
+            assert np.array_equal(counts, ref_counts)
