@@ -298,19 +298,19 @@ __global__ void permute_kernel(const float* __restrict__ rec, int64_t n, int S,
 }
 
 // permute_kernel fused with the culling bounds (stage 1+2 with culling on): one CTA of
-// PB_T threads per 512-point tile (4 points per thread, their loads in flight
-// together: at C5's 3,907 tiles two resident waves instead of seven of 512-thread
-// CTAs) copies its records into sorted order, then reduces per 32-point block (one
+// PB_T threads per 512-point tile (TILE / PB_T points per thread, their loads in
+// flight together; 128 threads at C5's 3,907 tiles: two resident waves instead of
+// seven of 512-thread CTAs) copies its records into sorted order, then reduces per 32-point block (one
 // warp and round) the box and max squared norm (blk, the layout of block_bounds_kernel
 // in ds_tile.cu; nullptr: skip) and per tile the box and max norm (lo / hi / maxnorm,
 // the layout of tile_bounds_kernel), and adds the tile box to its super tile's.
-constexpr int PB_T = 128;
-constexpr int PB_P = TILE / PB_T;
+template <int PB_T>
 __global__ void __launch_bounds__(PB_T) permute_bounds_kernel(
     const float* __restrict__ rec, int64_t n, int S, int dpad, const int32_t* __restrict__ perm,
     float* __restrict__ out, float* __restrict__ lo,
     float* __restrict__ hi, float* __restrict__ maxnorm, float* __restrict__ blk,
     unsigned int* __restrict__ super) {
+  constexpr int PB_P = TILE / PB_T;
   griddep_wait();
   __shared__ float smn[TILE / 32], smx[TILE / 32];
   const int64_t tile = blockIdx.x;
@@ -444,7 +444,11 @@ cudaError_t launch_spatial_sort(const float* rec, int64_t n, int d, float* rec_s
     }
   }
   if (bnd.lo) {
-    e = launch_pdl(permute_bounds_kernel, dim3((unsigned)n_tiles(n)), dim3(PB_T), 0, s, rec, n, S, dp,
+    // one 512-thread CTA per tile while the tiles fit one resident wave (C2: faster),
+    // 128-thread CTAs with four points per thread beyond (C5: fewer waves)
+    const bool wide = n_tiles(n) <= 148 * 4;
+    e = launch_pdl(wide ? permute_bounds_kernel<TILE> : permute_bounds_kernel<128>,
+                   dim3((unsigned)n_tiles(n)), dim3(wide ? TILE : 128), 0, s, rec, n, S, dp,
                    (const int32_t*)perm, rec_sorted, bnd.lo, bnd.hi, bnd.maxnorm, bnd.blk,
                    dp <= 4 ? bnd.super : (unsigned int*)nullptr);
     if (e != cudaSuccess) return e;
