@@ -373,12 +373,13 @@ def run_b200(args):
     tile_s = statistics.mean(tile_ms) / 1e3
     achieved = pairs * ops / tile_s / 1e12
     # kernels per step (1 GPU, culled schedule; the ncu launch list in profiles/): prep,
-    # morton, (digit scan + radix scatter) per 8-bit key digit (2 passes for 1-2-D inputs
-    # up to 2^18 points, else 3), permute + bounds, 2 cull-row kernels, unit list,
-    # eps-unit, union diag (+ core init), union links, roots, scan + labels; a capacity
-    # re-run repeats the pipeline; sharded runs add the shard-stage kernels and folds
-    passes = 2 if (min(d, 4) <= 2 and n <= (1 << 18)) else 3
-    launches_per_step = (11 + 2 * passes) * last[3] if world == 1 else 18
+    # the spatial sort — for 1-2-D inputs up to 2^18 points the counting sort (keys +
+    # histogram, scan, scatter: 3), else morton + (digit scan + radix scatter) per 8-bit
+    # key digit (3 passes: 7) — permute + bounds, 2 culling kernels, unit list, eps-unit,
+    # union diag (+ core init), union links, roots, scan + labels; a capacity re-run
+    # repeats the pipeline; sharded runs add the shard-stage kernels and folds
+    sort_kernels = 3 if (min(d, 4) <= 2 and n <= (1 << 18)) else 7
+    launches_per_step = (10 + sort_kernels) * last[3] if world == 1 else 18
 
     line = {
         "metric": METRIC,
