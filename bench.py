@@ -375,11 +375,11 @@ def run_b200(args):
     # kernels per step (1 GPU, culled schedule; the ncu launch list in profiles/): prep,
     # the spatial sort — for 1-2-D inputs up to 2^18 points the counting sort (keys +
     # histogram, scan, scatter: 3), else morton + (digit scan + radix scatter) per 8-bit
-    # key digit (3 passes: 7) — permute + bounds, 2 culling kernels, unit list, eps-unit,
+    # key digit (3 passes: 7) — permute + bounds, the culling kernel, unit list, eps-unit,
     # union diag (+ core init), union links, roots, scan + labels; a capacity re-run
     # repeats the pipeline; sharded runs add the shard-stage kernels and folds
     sort_kernels = 3 if (min(d, 4) <= 2 and n <= (1 << 18)) else 7
-    launches_per_step = (10 + sort_kernels) * last[3] if world == 1 else 18
+    launches_per_step = (9 + sort_kernels) * last[3] if world == 1 else 18
 
     line = {
         "metric": METRIC,

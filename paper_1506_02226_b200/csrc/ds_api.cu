@@ -396,7 +396,8 @@ ds_status stage12_enqueue(ds_ctx* c, const double* d_coords, int64_t n, int d, d
     DS_CK(launch_cull(rec, n, d, eps32, formula, &sc->unsafe_flag, lo, lo + (size_t)T * dp,
                       lo + (size_t)T * 2 * dp, (unsigned int*)((char*)c->scalars.p + zr_super(n)),
                       (int32_t*)c->iflags.p, (int32_t*)c->ipartials.p, &sc->kept32,
-                      (uint32_t*)c->items.p, &sc->kept, bnd.lo != nullptr, s));
+                      (uint32_t*)c->items.p, &sc->kept, bnd.lo != nullptr,
+                      /*ordered: every rank reads the same list*/ world > 1, s));
   }
   UnitArgs a;
   a.rec = rec;

@@ -219,11 +219,12 @@ cudaError_t launch_unit_dir(const UnitArgs& a, int d, int64_t all_items, const u
 cudaError_t launch_block_bounds(const float* rec, int64_t n, int d, float* blk, cudaStream_t s);
 // tile bounding boxes + list of tile pairs that are not provably empty
 // bounds_ready: lo / hi / maxnorm were filled by the spatial sort (SortBounds)
+// ordered = false (one GPU): the hierarchical cull may append the kept pairs in any order
 cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int formula,
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
                         unsigned int* super, int32_t* flags, int32_t* partials,
                         int32_t* total_kept, uint32_t* list, unsigned long long* count,
-                        bool bounds_ready, cudaStream_t s);
+                        bool bounds_ready, bool ordered, cudaStream_t s);
 // exclusive prefix sum of int32 data in place (3 kernels); *total = sum
 cudaError_t launch_exclusive_scan(int32_t* data, int64_t n, int32_t* partials, int32_t* total,
                                   cudaStream_t s);

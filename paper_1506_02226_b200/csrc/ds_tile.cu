@@ -1196,9 +1196,11 @@ __device__ __forceinline__ bool keep_box(const float* alo, const float* ahi, flo
 // Hierarchical row culling (d <= 4): a CTA per tile row a tests the super tiles at or
 // after a's first (one thread each), then one warp per kept super tile tests its 32
 // tiles b >= a — the kept pairs come out in item order (super tiles in order, tiles in
-// order within one), the same list as cull_rows / cull_write. write = false counts the
-// row's kept pairs (rowcnt), write = true writes them at the row's offset.
-template <int DP, bool WRITE>
+// order within one), the same list as cull_rows / cull_write. MODE 0 counts the row's
+// kept pairs (rowcnt), MODE 1 writes them at the row's offset (two kernels: the order
+// every rank of a sharded run must share); MODE 2 (one GPU) appends them in any order,
+// one list reservation per row (one kernel; count = the kept total).
+template <int DP, int MODE>
 __global__ void __launch_bounds__(CULL_T) cull_super_kernel(
     const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
     const unsigned int* __restrict__ super, int64_t T, float eps32, int formula,
@@ -1210,6 +1212,10 @@ __global__ void __launch_bounds__(CULL_T) cull_super_kernel(
   __shared__ int wsum[W];
   __shared__ int ks[CULL_T];  // kept super tiles of the row, in order
   __shared__ int nks;
+  constexpr int KB = 1024;    // MODE 2: the row's kept tiles, flushed to the list in batches
+  __shared__ uint32_t kb[MODE == 2 ? KB : 1];
+  __shared__ int nkb;
+  __shared__ unsigned long long kbase;
   const bool unsafe = *unsafe_flag != 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t NS = (T + SUPER - 1) / SUPER;
@@ -1222,7 +1228,8 @@ __global__ void __launch_bounds__(CULL_T) cull_super_kernel(
     }
     const float wa = maxnorm[a];
     int pos = 0;
-    if (WRITE) {  // kept pairs of the rows before a (O(T) reads, L2-resident)
+    if (MODE == 2 && threadIdx.x == 0) nkb = 0;
+    if (MODE == 1) {  // kept pairs of the rows before a (O(T) reads, L2-resident)
       int p = 0;
       for (int64_t r = threadIdx.x; r < a; r += blockDim.x) p += rowcnt[r];
       pos = block_sum(p, red);
@@ -1276,8 +1283,22 @@ __global__ void __launch_bounds__(CULL_T) cull_super_kernel(
           }
         }
         const uint32_t tb = __ballot_sync(0xffffffffu, kt);
-        if (!WRITE) {
+        if (MODE == 0) {
           row_total += lane == 0 ? __popc(tb) : 0;
+        } else if (MODE == 2) {
+          int at = 0;
+          if (lane == 0 && tb) at = atomicAdd(&nkb, __popc(tb));
+          at = __shfl_sync(0xffffffffu, at, 0);
+          if (kt) kb[at + __popc(tb & ((1u << lane) - 1u))] = ((uint32_t)a << 16) | (uint32_t)b;
+          __syncthreads();
+          if (nkb > KB - CULL_T || i0 + W >= nk) {  // flush before the buffer could overflow
+            if (threadIdx.x == 0) kbase = nkb ? atomicAdd(count, (unsigned long long)nkb) : 0ull;
+            __syncthreads();
+            for (int e = threadIdx.x; e < nkb; e += CULL_T) list[kbase + e] = kb[e];
+            __syncthreads();
+            if (threadIdx.x == 0) nkb = 0;
+            __syncthreads();
+          }
         } else {
           __syncthreads();
           if (lane == 0) wsum[wid] = __popc(tb);
@@ -1292,10 +1313,10 @@ __global__ void __launch_bounds__(CULL_T) cull_super_kernel(
         }
       }
     }
-    if (!WRITE) {
+    if (MODE == 0) {
       const int t = block_sum(row_total, red);
       if (threadIdx.x == 0) rowcnt[a] = t;
-    } else if (a == T - 1 && threadIdx.x == 0) {
+    } else if (MODE == 1 && a == T - 1 && threadIdx.x == 0) {
       *total_kept = pos;
       *count = (unsigned long long)pos;
     }
@@ -1306,13 +1327,18 @@ template <int DP>
 cudaError_t launch_cull_super(const float* lo, const float* hi, const float* maxnorm,
                               const unsigned int* super, int64_t T, float eps32, int formula,
                               const uint32_t* unsafe_flag, int32_t* rowcnt, uint32_t* list,
-                              int32_t* total_kept, unsigned long long* count, cudaStream_t s) {
+                              int32_t* total_kept, unsigned long long* count, bool ordered,
+                              cudaStream_t s) {
   const unsigned g = (unsigned)std::min<int64_t>(T, 148 * 8);
-  cudaError_t e = launch_pdl(cull_super_kernel<DP, false>, dim3(g), dim3(CULL_T), 0, s, lo, hi,
+  if (!ordered)  // count starts at zero (the per-call zero region)
+    return launch_pdl(cull_super_kernel<DP, 2>, dim3(g), dim3(CULL_T), 0, s, lo, hi, maxnorm,
+                      super, T, eps32, formula, unsafe_flag, (int32_t*)nullptr, list,
+                      (int32_t*)nullptr, count);
+  cudaError_t e = launch_pdl(cull_super_kernel<DP, 0>, dim3(g), dim3(CULL_T), 0, s, lo, hi,
                              maxnorm, super, T, eps32, formula, unsafe_flag, rowcnt,
                              (uint32_t*)nullptr, (int32_t*)nullptr, (unsigned long long*)nullptr);
   if (e != cudaSuccess) return e;
-  return launch_pdl(cull_super_kernel<DP, true>, dim3(g), dim3(CULL_T), 0, s, lo, hi, maxnorm, super,
+  return launch_pdl(cull_super_kernel<DP, 1>, dim3(g), dim3(CULL_T), 0, s, lo, hi, maxnorm, super,
                     T, eps32, formula, unsafe_flag, rowcnt, list, total_kept, count);
 }
 
@@ -1372,7 +1398,7 @@ cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int for
                         const uint32_t* unsafe_flag, float* lo, float* hi, float* maxnorm,
                         unsigned int* super, int32_t* flags, int32_t* partials,
                         int32_t* total_kept, uint32_t* list, unsigned long long* count,
-                        bool bounds_ready, cudaStream_t s) {
+                        bool bounds_ready, bool ordered, cudaStream_t s) {
   const int dp = pad_dim(d);
   const int S = ((dp + 1) + 3) / 4 * 4;
   const int64_t T = (n + TILE - 1) / TILE;
@@ -1382,13 +1408,13 @@ cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int for
   if (super && T <= CULL_ROWS_MAX) {  // hierarchical: super tiles first (d <= 4)
     switch (dp) {
       case 1: return launch_cull_super<1>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
-                                          flags, list, total_kept, count, s);
+                                          flags, list, total_kept, count, ordered, s);
       case 2: return launch_cull_super<2>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
-                                          flags, list, total_kept, count, s);
+                                          flags, list, total_kept, count, ordered, s);
       case 3: return launch_cull_super<3>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
-                                          flags, list, total_kept, count, s);
+                                          flags, list, total_kept, count, ordered, s);
       default: return launch_cull_super<4>(lo, hi, maxnorm, super, T, eps32, formula, unsafe_flag,
-                                           flags, list, total_kept, count, s);
+                                           flags, list, total_kept, count, ordered, s);
     }
   }
   if (T <= CULL_ROWS_MAX) {  // rowcnt lives in the flags buffer (T <= T(T+1)/2 ints)
