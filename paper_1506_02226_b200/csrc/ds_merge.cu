@@ -535,13 +535,16 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
         const int key = is_core ? hist[lp[tid]] : -1;
         const uint32_t grp = __match_any_sync(0xffffffffu, key);
         if (is_core && (tid & 31) == __ffs(grp) - 1) M[key * WPR + (tid >> 5)] = __brev(grp);
+        __syncthreads();
+        hist[tid] = key;  // hist becomes node -> tree slot (one load less per lookup)
       }
       __syncthreads();
+#pragma unroll 4
       for (int r = 0; r < RB; ++r) {
         const int u = cblk * RB + r;
-        const uint32_t um = R[w * DIAG_RS + u];
+        const uint32_t um = R[w * DIAG_RS + u];  // zero for non-core rows
+        const int k = hist[u];
         if (!um) continue;
-        const int k = hist[lp[u]];
         const uint32_t cross = um & ~M[k * WPR + w];
         if (!cross) continue;
         // the trees the word crosses into: per iteration the tree of its lowest remaining
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
         // ntrees)
         uint32_t bits = 0, rest = cross;
         while (rest) {
-          const int j = hist[lp[w * 32 + __clz(rest)]];
+          const int j = hist[w * 32 + __clz(rest)];
           bits |= 1u << j;
           rest &= ~M[j * WPR + w];
         }
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(512, 4) union_diag_kernel(
       }
       __syncthreads();
       if (is_core) {  // lowest slot of the merged component = its smallest root
-        const int kmin = __ffs(adj[hist[lp[tid]]]) - 1;
+        const int kmin = __ffs(adj[hist[tid]]) - 1;
         lp[tid] = slot_root[kmin];
       }
     } else {

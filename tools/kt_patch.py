@@ -52,6 +52,24 @@ hs = hs.replace("#define griddep_wait()", """#define KT_MARK(site) do { if (::ds
 #define griddep_wait()""", 1)
 open(h, "w").write(hs)
 
+# DS_KT_PHASES=1: thread 0 of every union_diag CTA also stamps its phase boundaries
+# (sites 61001..), reported by tools/kt_phases.py
+PHASES = [
+    (61001, "    if (tid == 0) slot_root[0] = -1;  // atomicMax target of the single-root fast path\n    __syncthreads();", True),
+    (61002, "    // minimum neighbour of every core column", False),
+    (61003, "    // Fast path: a core point without a smaller core neighbour", False),
+    (61004, "        __syncthreads();  // smem is reused by the next tile\n        continue;", False),
+    (61005, "    // merge the min-neighbour trees.", False),
+    (61006, "    __syncthreads();\n    {\n      const int v = tid;", True),
+    (61007, "    __syncthreads();\n  }\n}\n\n// Round 2, off-diagonal", False),
+    (61008, "      for (int r = 0; r < RB; ++r) {\n        const int u = cblk * RB + r;\n        uint32_t um = R[w * DIAG_RS + u];", False),
+    (61009, "      auto locate = [&](int j) -> unsigned long long {", False),
+    (61010, "      for (int r = 0; r < RB; ++r) {\n        const int u = cblk * RB + r;\n        const uint32_t um = R[w * DIAG_RS + u];", False),
+    (61011, "      if (tid < 32) {  // symmetric transitive closure", False),
+    # union_links: per-warp end (61100)
+    (61101, "    const int a = na, b = nb, lb = nlb;\n    const uint2 ce = nce;", False),
+    (61100, "      __syncwarp();  // cols / groups / pair masks are rewritten by the next column block\n    }\n  }", True),
+]
 for fi, f in enumerate(FILES):
     p = os.path.join(TMP, f)
     s = open(p).read()
@@ -66,6 +84,12 @@ extern "C" void ds_kt_set_{name}(void* p) {{ cudaMemcpyToSymbol(ds::kt::g_kt, &p
         s = s.replace(anchor, """  flush();
   if (lane == 0) KT_MARK(60000);
   if (lane == 0 && steps_done)""", 1)
+    if f == "ds_merge.cu" and os.environ.get("DS_KT_PHASES"):  # union_diag phase marks
+        M = lambda site: (f"if (threadIdx.x == 0) KT_MARK({site});" if site < 61100 else
+                          f"if ((threadIdx.x & 31) == 0) KT_MARK({site});")
+        for site, anchor, after in PHASES:
+            assert anchor in s, anchor
+            s = s.replace(anchor, anchor + "\n" + M(site) if after else M(site) + "\n" + anchor, 1)
     if f == "ds_api.cu":
         decl = "".join(f'extern "C" void ds_kt_set_{g[3:-3]}(void* p);\n' for g in FILES)
         s = s.replace('#include "ds_internal.cuh"', '#include "ds_internal.cuh"\n#include <cstdio>\n#include <cstdlib>\n' + decl, 1)
