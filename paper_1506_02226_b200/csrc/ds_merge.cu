@@ -648,6 +648,12 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
   __shared__ uint8_t clead_sh[LINK_WARPS][32];       // column -> its group's first column
   __shared__ uint32_t cmask_sh[LINK_WARPS][32];      // group (first column) -> its columns
   __shared__ uint32_t pairs_sh[LINK_WARPS][MAXR];    // row group -> column groups linked
+  // links of the current unit, made together at its end (lanes in parallel) instead of
+  // per column block: each link is a chain of dependent parent loads + CAS, and made
+  // per column block those chains were serial in the unit's column blocks
+  constexpr int LKCAP = 64;
+  __shared__ int2 lk_sh[LINK_WARPS][LKCAP];
+  __shared__ int lkn_sh[LINK_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* rows = rows_sh[warp];
   int* cols = cols_sh[warp];
@@ -656,6 +662,15 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
   uint32_t* cmask = cmask_sh[warp];
   uint32_t* pairs = pairs_sh[warp];
   for (int k = lane; k < MAXR; k += 32) pairs[k] = 0u;
+  int2* lk = lk_sh[warp];
+  int* lkn = &lkn_sh[warp];
+  if (lane == 0) *lkn = 0;
+  __syncwarp();
+  auto defer_link = [&](int au, int av) {  // overflow: link now
+    const int at = atomicAdd(lkn, 1);
+    if (at < LKCAP) lk[at] = make_int2(au, av);
+    else link_root(parent, find_plain(parent, au), av);
+  };
   const int n = (int)A.n;
   const int KPL = TILE / LB;  // rows per lane block (32 * KP)
   long long r_lo, r_hi;
@@ -700,6 +715,27 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
     const bool ok = cnt != 0u && base + cnt <= A.words_cap;  // overflowed run: the host re-runs
     uint32_t todo = __ballot_sync(0xffffffffu, ok);
     if (!todo) continue;
+    // the rows' parents and core words, issued together with the uniform test's loads
+    // (one round trip instead of one per 32-row chunk after it)
+    const int r0 = a * TILE + lb * KPL;  // a multiple of 32
+    int pgs[MAXR / 32];
+    uint32_t cws[MAXR / 32];
+#pragma unroll
+    for (int i = 0; i < MAXR / 32; ++i) {
+      const bool chunk = 32 * i < KPL && r0 + 32 * i < n;  // warp-uniform
+      pgs[i] = chunk && r0 + 32 * i + lane < n ? parent[r0 + 32 * i + lane] : -1;
+      cws[i] = chunk ? corew[(r0 >> 5) + i] : 0u;
+    }
+    auto load_cb = [&](int jw, uint2 (&rw)[4], int& pr, uint32_t& cwv, uint32_t& wc) {
+      wc = __shfl_sync(0xffffffffu, cnt, jw);  // <= 32*KP <= 128 words
+      const unsigned long long wbase = __shfl_sync(0xffffffffu, base, jw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        rw[q] = lane + 32u * q < wc ? A.words[wbase + lane + 32u * q] : make_uint2(0u, 0u);
+      const int c = b * TILE + jw * 32 + lane;
+      pr = c < n ? parent[c] : -1;
+      cwv = corew[(b * TILE >> 5) + jw];
+    };
     // Uniform blocks (union_diag: all core points of a 32-point block share one root):
     // when the lane block's row blocks share one root, every column block has a root,
     // and every row and column is core, every word is a core-core word and no border
@@ -740,14 +776,24 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
     }
     // rows of the lane block: parent (= local root, or an ancestor of it) or -1 (not
     // core), grouped by root per 32-row chunk
-    const int r0 = a * TILE + lb * KPL;
+    // the first column block's loads overlap the row grouping (issued after the uniform
+    // test: uniform units, most of a dense region's, never read words)
+    int jw = __ffs(todo) - 1;
+    todo &= todo - 1u;
+    uint2 rec[4];
+    int praw;
+    uint32_t cw, wcnt;
+    load_cb(jw, rec, praw, cw, wcnt);
     int rfirst = -1;  // this lane's first core row root
     bool rsame = true;  // all of this lane's core rows share it
     bool rnoncore = false;  // this lane has a non-core row
-    for (int k = lane; k < KPL; k += 32) {  // KPL is a multiple of 32: warp-uniform trips
+#pragma unroll
+    for (int i = 0; i < MAXR / 32; ++i) {
+      if (32 * i >= KPL) break;  // KPL is a multiple of 32: warp-uniform
+      const int k = lane + 32 * i;
       const int g = r0 + k;
-      const int pg = g < n ? parent[g] : -1;
-      const bool c = g < n && ((corew[g >> 5] >> (31 - (g & 31))) & 1u);
+      const int pg = pgs[i];
+      const bool c = g < n && ((cws[i] >> (31 - lane)) & 1u);
       const int v = c ? pg : -1;
       rows[k] = v;
       const unsigned grp = __match_any_sync(0xffffffffu, v);
@@ -769,18 +815,14 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
         if (__all_sync(0xffffffffu, rsame && (rfirst < 0 || rfirst == r))) urow = r;
       }
     }
-    while (todo) {
-      const int jw = __ffs(todo) - 1;
-      todo &= todo - 1u;
-      const uint32_t wcnt = __shfl_sync(0xffffffffu, cnt, jw);  // <= 32*KP <= 128 words
-      const unsigned long long wbase = __shfl_sync(0xffffffffu, base, jw);
+    for (bool first_cb = true;; first_cb = false) {  // column blocks of the unit
+      if (!first_cb) {
+        if (!todo) break;
+        jw = __ffs(todo) - 1;
+        todo &= todo - 1u;
+        load_cb(jw, rec, praw, cw, wcnt);
+      }
       const int c0 = b * TILE + jw * 32;
-      uint2 rec[4];  // word k = lane + 32 q: all loads issued together
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        rec[q] = lane + 32u * q < wcnt ? A.words[wbase + lane + 32u * q] : make_uint2(0u, 0u);
-      const int praw = c0 + lane < n ? parent[c0 + lane] : -1;
-      const uint32_t cw = corew[(b * TILE >> 5) + jw];
       const bool cc = (cw >> (31 - lane)) & 1u;
       const int pv = cc ? praw : -1;
       cols[lane] = pv;
@@ -842,7 +884,7 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
       if (one_link) {
         if (__any_sync(0xffffffffu, cc_any) && lane == 0 && urow != ub &&
             !(urow == last_a && ub == last_b)) {
-          link_root(parent, find_plain(parent, urow), ub);
+          defer_link(urow, ub);
           last_a = urow;
           last_b = ub;
         }
@@ -860,7 +902,7 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
             m &= m - 1u;
             const int av = cols[g];
             if (av != au && !(au == last_a && av == last_b)) {
-              link_root(parent, find_plain(parent, au), av);
+              defer_link(au, av);
               last_a = au;
               last_b = av;
             }
@@ -869,6 +911,11 @@ __global__ void __launch_bounds__(LINK_WARPS * 32, DS_LINK_MINB) union_links_ker
       }
       __syncwarp();  // cols / groups / pair masks are rewritten by the next column block
     }
+    const int nl = min(*lkn, LKCAP);
+    for (int i = lane; i < nl; i += 32) link_root(parent, find_plain(parent, lk[i].x), lk[i].y);
+    __syncwarp();
+    if (lane == 0) *lkn = 0;
+    __syncwarp();
   }
 }
 

@@ -88,7 +88,9 @@ extern "C" void ds_kt_set_{name}(void* p) {{ cudaMemcpyToSymbol(ds::kt::g_kt, &p
         M = lambda site: (f"if (threadIdx.x == 0) KT_MARK({site});" if site < 61100 else
                           f"if ((threadIdx.x & 31) == 0) KT_MARK({site});")
         for site, anchor, after in PHASES:
-            assert anchor in s, anchor
+            if anchor not in s:
+                print("kt_patch: phase anchor not found, site", site, "skipped")
+                continue
             s = s.replace(anchor, anchor + "\n" + M(site) if after else M(site) + "\n" + anchor, 1)
     if f == "ds_api.cu":
         decl = "".join(f'extern "C" void ds_kt_set_{g[3:-3]}(void* p);\n' for g in FILES)
