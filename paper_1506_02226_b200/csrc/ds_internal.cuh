@@ -60,6 +60,12 @@ inline int units_per_tile(int d) { return lane_blocks(d) * WPR; }
 // words * WORD_RUN / (WORD_RUN - 128) + warps * WORD_RUN.
 constexpr int WORD_RUN = 256;
 
+// KP = 4: a (lane block, tile pair) with many kept column blocks is listed as units of
+// at most unit_cols column blocks — 2 for inputs up to UNIT_SMALL_N points (few units
+// per warp: the end of the eps launch waits on the last ones), else 4 (fewer units, less
+// per-unit overhead in the eps and union kernels)
+constexpr int64_t UNIT_SMALL_N = (int64_t)1 << 18;
+
 struct UnitArgs {
   const float* rec;
   int64_t n;

@@ -169,7 +169,9 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
 // holds the prefix sums of the chunk lengths in shared memory so that a CTA can
 // walk the tile pair's words as one flat index space (word k lives in the last
 // chunk whose prefix is <= k).
-constexpr int MAX_UPT = (TILE / 32) * WPR;  // 256 units per tile pair (KP = 1)
+// chunk entries per tile pair: up to 32 units (KP = 4 in pieces of 2 column blocks;
+// KP = 1: 16 unsplit) x WPR
+constexpr int MAX_UPT = 32 * WPR;
 static_assert(MAX_UPT <= 512, "union_diag loads one chunk entry per thread");
 
 struct ItemWords {

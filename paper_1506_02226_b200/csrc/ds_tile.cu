@@ -726,10 +726,15 @@ __device__ __forceinline__ PairMasks pair_masks(const float* __restrict__ blk, c
 }
 
 // For KP = 4 (d <= 8) a (lane block, tile pair) with many kept column blocks is
-// listed as several row units of at most 4 column blocks each (finer work balance at
-// the tail); a tile pair then has at most 16 units x WPR = 256 chunk entries, the
-// bound the union kernels hold in shared memory (MAX_UPT), as for KP <= 2 unsplit.
-__device__ __forceinline__ int unit_cols(int KP) { return KP == 4 ? 4 : 16; }
+// listed as several row units of at most 2 (n <= UNIT_SMALL_N) or 4 column blocks each
+// (finer work balance at the tail); a tile pair then has at most 32 units x WPR = 512
+// chunk entries, the bound the union kernels hold in shared memory (MAX_UPT); KP <= 2
+// units are unsplit (16 per tile pair). Measured (A/B): pieces of 2 cut C1's eps launch
+// 11.2 -> 9.3 us and C2's by 1.2 us, but cost C3 / C5 15-60 us in union_links
+// (per-unit overhead), hence the size switch.
+__device__ __forceinline__ int unit_cols(int KP, int64_t n) {
+  return KP == 4 ? (n <= UNIT_SMALL_N ? 2 : 4) : 16;
+}
 
 // The row-unit list of this launch's shard, one kernel: warp per kept item (items are
 // dealt to the shards cyclically, q = rank + k * world, which spreads the dense and
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(256, 4) unit_list_kernel(
   const int64_t K = (int64_t)*kept;
   const bool unsafe = *unsafe_flag != 0;
   const int LB = TILE / (32 * KP);
-  const int uc = unit_cols(KP);
+  const int uc = unit_cols(KP, n);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t mine = K > rank ? (K - rank + world - 1) / world : 0;
   for (int64_t t0 = (int64_t)blockIdx.x * W; t0 < mine; t0 += (int64_t)gridDim.x * W) {
