@@ -2,7 +2,7 @@
 # Full GPU iteration: smoke, GPU parity tests, bench (C2) + reference arm, all configs,
 # ncu launch list of the bench command and full captures of the top kernels.
 #   bash tools/gpu_round.sh [tag]
-TAG=${1:-r01}
+TAG=${1:-r02}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
