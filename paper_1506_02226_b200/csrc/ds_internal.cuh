@@ -71,6 +71,7 @@ struct UnitArgs {
   int64_t n;
   int32_t T;                            // tiles per side
   float eps32;
+  float negz = -0.0f;                   // the FFMA2 addend of exact products (ds_tile.cu)
   int32_t* cnt;
   uint2* words;                         // {32-bit word, local row << 4 | column word}
   unsigned long long words_cap;

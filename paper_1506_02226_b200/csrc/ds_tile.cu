@@ -79,23 +79,73 @@ __device__ __forceinline__ float d2_direct(const float (&lv)[D], const float* xj
 // ---- lane points in packed form ------------------------------------------------
 // ALG: v2[k][p] = {2c_{2p}, 2c_{2p+1}} (X = 2c is exact), t[k] = T = P_i.
 // DIR: v2[k][p] = {-c_{2p}, -c_{2p+1}} so that x_j + (-x_i) == fl(x_j - x_i).
+// KP even and d >= DS_PAIR_MIN_D (PAIRED): lane points 2h and 2h+1 share every packed register instead —
+// c2[h][q] = {c_q of 2h, c_q of 2h+1} (the ALG / DIR value above), t2[h] = {T_2h, T_2h+1}
+// — so every FP op of the pair loop is a two-lane-point FFMA2 / FADD2 with the staged
+// coordinate broadcast (`R.F32` operand): an FP32-pipe slot does two lane-ops for every
+// term, where the per-lane-point packing spent scalar FADDs on the cross sum.
+// Measured on B200 (A/B, round 2): the paired packing cuts the C4 (16-D) eps kernel
+// 20.2 -> 18.5 ms; at d = 2 (C2 / C3 / C5) it is neutral to +2 % — the culled 2-D
+// schedule is bound by the per-step epilogue, not the FP32 pipe — so d <= 4 keeps the
+// per-lane-point packing.
+#ifndef DS_PAIR_MIN_D
+#define DS_PAIR_MIN_D 5
+#endif
 template <int D, int KP>
 struct Lanes {
   static constexpr int DP = D / 2;
   static constexpr bool ODD = (D & 1) != 0;
-  float2 v2[KP][DP > 0 ? DP : 1];
+  static constexpr bool PAIRED = KP % 2 == 0 && D >= DS_PAIR_MIN_D;
+  static constexpr int H = PAIRED ? KP / 2 : 1;
+  float2 c2[H][PAIRED ? D : 1];
+  float2 t2[H];
+  float2 v2[PAIRED ? 1 : KP][DP > 0 && !PAIRED ? DP : 1];
   float v1[KP];
   float t[KP];
 };
 
+// fl(a * b) for two lanes as FFMA2(a, b, z) with z = {-0, -0} held in a register: the
+// exact product plus -0 rounds once to the product's own rounding (+0 + -0 = +0 in RN),
+// so it is bitwise the FMUL2 — but unlike FMUL2 it cannot be contracted with the FADD2
+// that consumes it (ptxas turns FMUL2 -> FADD2 into FFMA2 even at --fmad=false, which
+// would drop a rounding; tests/test_abi.py checks every FFMA2 of the pair loop adds z).
+__device__ __forceinline__ float2 mul2_exact(float2 a, float2 b, float2 z) { return __ffma2_rn(a, b, z); }
+
 // Squared distances of lane points K0 .. K1-1 to staged point j (xj: its record,
 // pj = P_j), in the reference's order with one rounding per operation.
 template <int D, int F, int KP, int K0 = 0, int K1 = KP>
-__device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, float pj,
+__device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, float pj, float2 z,
                                         float (&d2)[KP]) {
   constexpr int DP = Lanes<D, KP>::DP;
   constexpr bool ODD = Lanes<D, KP>::ODD;
-  if constexpr (F == DS_FORMULA_ALGEBRAIC) {
+  if constexpr (Lanes<D, KP>::PAIRED) {
+    static_assert(K0 % 2 == 0 && K1 % 2 == 0, "lane points are evaluated in pairs");
+#pragma unroll
+    for (int h = K0 / 2; h < K1 / 2; ++h) {
+      float2 acc;
+      if constexpr (F == DS_FORMULA_ALGEBRAIC) {
+        // cross = ((X0*x0 + X1*x1) + X2*x2) + ...          (kernels.py:409-414)
+        acc = mul2_exact(L.c2[h][0], make_float2(xj[0], xj[0]), z);
+#pragma unroll
+        for (int q = 1; q < D; ++q)
+          acc = __fadd2_rn(acc, mul2_exact(L.c2[h][q], make_float2(xj[q], xj[q]), z));
+        // d2 = (T + P) - cross                              (kernels.py:415-417)
+        const float2 tp = __fadd2_rn(L.t2[h], make_float2(pj, pj));
+        acc = __fadd2_rn(tp, make_float2(-acc.x, -acc.y));
+      } else {
+        // d2 = ((dx0^2 + dx1^2) + dx2^2) + ..., dx = x_col - x_row  (kernels.py:197-210)
+        float2 dx = __fadd2_rn(make_float2(xj[0], xj[0]), L.c2[h][0]);
+        acc = mul2_exact(dx, dx, z);
+#pragma unroll
+        for (int q = 1; q < D; ++q) {
+          dx = __fadd2_rn(make_float2(xj[q], xj[q]), L.c2[h][q]);
+          acc = __fadd2_rn(acc, mul2_exact(dx, dx, z));
+        }
+      }
+      d2[2 * h] = acc.x;
+      d2[2 * h + 1] = acc.y;
+    }
+  } else if constexpr (F == DS_FORMULA_ALGEBRAIC) {
     // cross = ((X0*x0 + X1*x1) + X2*x2) + ...            (kernels.py:409-414)
     float c[KP];
 #pragma unroll
@@ -172,7 +222,10 @@ __device__ __forceinline__ void eval_d2(const Lanes<D, KP>& L, const float* xj, 
 // lop3 to the same), the sign bit one FP op + one funnel shift.
 template <int KP, bool SAFE, int D>
 struct Pack {
-  static constexpr int KC = !SAFE ? KP : (D <= 4 ? (3 * KP) / 4 : 0);
+#ifndef DS_KC_SMALL
+#define DS_KC_SMALL 3
+#endif
+  static constexpr int KC = !SAFE ? KP : (D <= 4 ? (DS_KC_SMALL * KP) / 4 : 0);
 };
 
 template <int KP, bool SAFE, int D, int K0 = 0, int K1 = KP>
@@ -303,7 +356,7 @@ struct Step {
 // pairs of lane points; the row-pair mask of the unit list, see box_pairs).
 template <int D, int F, bool SAFE, int K0, int K1>
 __device__ __forceinline__ void pair_loop(const Lanes<D, Geo<D>::KP>& L, const float* st, float eps32,
-                                          uint32_t (&acc)[Geo<D>::KP]) {
+                                          float2 z, uint32_t (&acc)[Geo<D>::KP]) {
   using G = Geo<D>;
   constexpr int S = G::S;
   constexpr int KP = G::KP;
@@ -322,7 +375,7 @@ __device__ __forceinline__ void pair_loop(const Lanes<D, Geo<D>::KP>& L, const f
       xj[4 * v + 3] = x.w;
     }
     float d2[KP];
-    eval_d2<D, F, KP, K0, K1>(L, xj, xj[D], d2);
+    eval_d2<D, F, KP, K0, K1>(L, xj, xj[D], z, d2);
     pack_bits<KP, SAFE, D, K0, K1>(d2, eps32, jj, acc);
   }
 }
@@ -372,6 +425,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   const int n = (int)A.n;
   const int T = A.T;
   const float eps32 = A.eps32;
+  const float2 z2 = make_float2(A.negz, A.negz);  // {-0, -0}, see mul2_exact
   const uint2* list = A.unit_list;
   // tile-local row of lane point k of `lane` in lane block lb: with row-pair culling (d <=
   // 4) lane point k is row block k of the lane block (rows lb*128 + 32k + lane), else the
@@ -525,10 +579,20 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 #pragma unroll
         for (int q = 0; q < D; ++q)
           c[q] = (F == DS_FORMULA_ALGEBRAIC) ? __fadd_rn(tmp[q], tmp[q]) : -tmp[q];
+        if constexpr (Lanes<D, KP>::PAIRED) {
 #pragma unroll
-        for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
-        L.v1[k] = c[D - 1];
-        L.t[k] = tmp[D];
+          for (int q = 0; q < D; ++q) {
+            if (k & 1) L.c2[k >> 1][q].y = c[q];
+            else L.c2[k >> 1][q].x = c[q];
+          }
+          if (k & 1) L.t2[k >> 1].y = tmp[D];
+          else L.t2[k >> 1].x = tmp[D];
+        } else {
+#pragma unroll
+          for (int q = 0; q < Lanes<D, KP>::DP; ++q) L.v2[k][q] = make_float2(c[2 * q], c[2 * q + 1]);
+          L.v1[k] = c[D - 1];
+          L.t[k] = tmp[D];
+        }
       }
     }
 
@@ -540,11 +604,11 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 #pragma unroll
     for (int k = 0; k < KP; ++k) acc[k] = 0u;
     if constexpr (STRIDED) {  // warp-uniform: the step's row-pair mask
-      if (cur.pm == 3) pair_loop<D, F, SAFE, 0, 4>(L, st, eps32, acc);
-      else if (cur.pm == 1) pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, acc);
-      else pair_loop<D, F, SAFE, 2, 4>(L, st, eps32, acc);
+      if (cur.pm == 3) pair_loop<D, F, SAFE, 0, 4>(L, st, eps32, z2, acc);
+      else if (cur.pm == 1) pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, z2, acc);
+      else pair_loop<D, F, SAFE, 2, 4>(L, st, eps32, z2, acc);
     } else {
-      pair_loop<D, F, SAFE, 0, KP>(L, st, eps32, acc);
+      pair_loop<D, F, SAFE, 0, KP>(L, st, eps32, z2, acc);
     }
     steps_done += (STRIDED && cur.pm != 3) ? 2 : KP;  // lane points evaluated
 

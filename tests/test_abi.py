@@ -85,11 +85,13 @@ def test_no_cpu_fallback_when_library_missing(tmp_path):
 
 @pytest.mark.skipif(not shutil.which("cuobjdump"), reason="cuobjdump not available")
 def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
-    """Parity needs every product and sum rounded separately: the eps-tile
-    kernels must contain no FFMA/FFMA2 (ptxas would otherwise be free to fuse
-    packed mul+add, SURVEY §0 finding 4), and they must use the packed FP32
-    instructions and the asynchronous shared-memory staging (cp.async ->
-    LDGSTS) the design relies on."""
+    """Parity needs every product and sum rounded separately (SURVEY §0 finding 4):
+    the eps-tile kernels contain no scalar FFMA, and every FFMA2 is an exact product
+    -- its addend is the uniform register holding {-0, -0} (UnitArgs.negz, see
+    mul2_exact in ds_tile.cu), never a product's consumer contracted into it (ptxas
+    would be free to fuse a packed mul+add). With d >= 2 and two lane points per
+    register pair (d >= 5) the products are FFMA2 with the staged coordinate broadcast,
+    the sums FADD2; at d <= 4 a lane point's products are one FMUL2; the records are staged asynchronously (cp.async -> LDGSTS)."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True,
                           check=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
@@ -97,10 +99,14 @@ def test_sass_gate_no_fused_multiply_add_in_pair_kernels(lib):
     assert len(tile) >= 16
     for body in tile:
         name = body.split("\n")[0]
-        assert not re.search(r"\bFFMA2?\b", body), name
+        assert not re.search(r"\bFFMA\b", body), name
+        for ins in re.findall(r"FFMA2[^;]*;", body):
+            assert re.search(r", UR\d+\.F32 ;$", ins), (name, ins)
     k2 = [f for f in tile if "eps_unit_kernelILi2ELi1EE" in f.split("\n")[0]]
     assert k2 and "FMUL2" in k2[0] and "FADD2" in k2[0]
     assert "LDGSTS" in k2[0]
+    k16 = [f for f in tile if "eps_unit_kernelILi16ELi1EE" in f.split("\n")[0]]
+    assert k16 and "FFMA2" in k16[0] and "FADD2" in k16[0] and "FMUL2" not in k16[0]
 
 
 @pytest.mark.skipif(not shutil.which("cuobjdump"), reason="cuobjdump not available")
