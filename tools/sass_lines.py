@@ -22,7 +22,13 @@ rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
 ist = hdr.index("Warp Stall Sampling (All Samples)")
-ins = [(r[isrc].strip(), int(r[iex] or 0), int(r[ist] or 0)) for r in rows[2:] if len(r) > iex]
+ins = []
+for r in rows[2:]:  # the first kernel of the report only (a second one repeats the header)
+    if len(r) <= iex:
+        continue
+    if not (r[iex] or "0").isdigit():
+        break
+    ins.append((r[isrc].strip(), int(r[iex] or 0), int(r[ist] or 0)))
 with tempfile.TemporaryDirectory() as d:
     import os
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
