@@ -444,7 +444,13 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 #ifndef DS_BATCH_MIN
 #define DS_BATCH_MIN 1
 #endif
-  long long B = (r_hi - r_lo) / (nw * 16);
+  // wide records: a unit is tens of us (C4: ~33 us per warp), so the last batches set the
+  // end of the launch — smaller batches (~128 per warp) keep that tail short
+#ifndef DS_BATCHES_WIDE
+#define DS_BATCHES_WIDE 128
+#endif
+  constexpr long long BATCHES = D > 4 ? DS_BATCHES_WIDE : 16;
+  long long B = (r_hi - r_lo) / (nw * BATCHES);
   B = B < DS_BATCH_MIN ? DS_BATCH_MIN : (B > 32 ? 32 : B);
   unsigned int* const ctr = reinterpret_cast<unsigned int*>(A.work_ctr);
   auto load_entries = [&](long long lo) -> uint2 {
