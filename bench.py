@@ -363,6 +363,22 @@ def run_b200(args):
         ctx.configure(True, True)
         dense = {"tile_ms": statistics.mean(t.tile_ms for t in dts[1:]),
                  "pairs_per_launch": dts[-1].pairs_evaluated}
+    # the FP32-bound case of the same kernel: BASELINE configs C4 (500k points, 16-D),
+    # default culled schedule, stage 1+2 (a parity config, not a bench line)
+    wide = None
+    if world == 1 and not args.no_dense:
+        c4 = ds.CONFIGS["C4"]
+        p4 = c4.points()
+        v4 = ds.validate_params(c4.eps, c4.min_pts)
+        wts = []
+        for _ in range(3):
+            _, _, _, dt = ctx.fused_build(p4.coords_aos, v4.eps_sq, v4.min_pts, formula, mem_cap,
+                                          want_bits=False)
+            wts.append(dt)
+        wide = {"n": p4.n, "d": p4.d, "tile_ms": statistics.mean(t.tile_ms for t in wts[1:]),
+                "pairs_per_launch": wts[-1].pairs_evaluated,
+                "ops_per_pair": algorithmic_ops_per_pair(p4.d, formula)}
+        del p4
     peaks = load_peaks()
     clocks = clk.summary()
     sm_max = peaks.get("sm_max_mhz", 1965.0)
@@ -420,6 +436,15 @@ def run_b200(args):
             "achieved": dense["pairs_per_launch"] * ops / (dense["tile_ms"] / 1e3) / 1e12,
             "frac": dense["pairs_per_launch"] * ops / (dense["tile_ms"] / 1e3) / 1e12 / fp32_peak,
             "gpair_evals_per_s": dense["pairs_per_launch"] / (dense["tile_ms"] / 1e3) / 1e9}),
+        "wide_records": (None if wide is None else {
+            "what": "C4 (BASELINE configs[3]): n=%d, d=%d, default culled schedule, eps kernel "
+                    "only (stage-1 device stamps), mean of 2 runs after one warm-up"
+                    % (wide["n"], wide["d"]),
+            "tile_ms": wide["tile_ms"], "pairs_per_launch": wide["pairs_per_launch"],
+            "ops_per_pair": wide["ops_per_pair"],
+            "achieved": wide["pairs_per_launch"] * wide["ops_per_pair"] / (wide["tile_ms"] / 1e3) / 1e12,
+            "frac": wide["pairs_per_launch"] * wide["ops_per_pair"] / (wide["tile_ms"] / 1e3) / 1e12
+                    / fp32_peak}),
         "gpair_evals_per_s": pairs / tile_s / 1e9,
         "n2_decisions_per_s": (n * n if world == 1 else n * n / world) / tile_s / 1e9,
         "stages_ms": last[2],

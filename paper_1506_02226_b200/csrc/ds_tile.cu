@@ -610,9 +610,46 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 #pragma unroll
     for (int k = 0; k < KP; ++k) acc[k] = 0u;
     if constexpr (STRIDED) {  // warp-uniform: the step's row-pair mask
-      if (cur.pm == 3) pair_loop<D, F, SAFE, 0, 4>(L, st, eps32, z2, acc);
-      else if (cur.pm == 1) pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, z2, acc);
-      else pair_loop<D, F, SAFE, 2, 4>(L, st, eps32, z2, acc);
+#ifndef DS_HALF_SWAP
+#define DS_HALF_SWAP 1
+#endif
+      if (cur.pm == 3) {
+        pair_loop<D, F, SAFE, 0, 4>(L, st, eps32, z2, acc);
+      } else if (!DS_HALF_SWAP) {
+        if (cur.pm == 1) pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, z2, acc);
+        else pair_loop<D, F, SAFE, 2, 4>(L, st, eps32, z2, acc);
+      } else {
+        // one half-step loop body for both halves (less hot code: the 2-D kernel's warps
+        // stall on instruction fetch): lane points 2-3 are swapped into 0-1 and back
+        auto swap_halves = [&]() {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+#pragma unroll
+            for (int q = 0; q < Lanes<D, KP>::DP; ++q) {
+              const float2 t = L.v2[k][q];
+              L.v2[k][q] = L.v2[k + 2][q];
+              L.v2[k + 2][q] = t;
+            }
+            const float t1 = L.v1[k];
+            L.v1[k] = L.v1[k + 2];
+            L.v1[k + 2] = t1;
+            const float tt = L.t[k];
+            L.t[k] = L.t[k + 2];
+            L.t[k + 2] = tt;
+          }
+        };
+        if (cur.pm == 2) swap_halves();
+        pair_loop<D, F, SAFE, 0, 2>(L, st, eps32, z2, acc);
+        if (cur.pm == 2) {
+          swap_halves();
+          // lane points 0-1 are compared (bit = in range); the epilogue inverts lane
+          // points k >= KC (sign-bit words: bit = out of range), so those are stored inverted
+          acc[2] = 2 < KC ? acc[0] : ~acc[0];
+          acc[3] = 3 < KC ? acc[1] : ~acc[1];
+          acc[0] = 0u;
+          acc[1] = 0u;
+        }
+      }
     } else {
       pair_loop<D, F, SAFE, 0, KP>(L, st, eps32, z2, acc);
     }

@@ -8,6 +8,7 @@ line table of the same kernel disassembled from the object (nvdisasm -g).
 """
 import collections
 import csv
+import os
 import io
 import re
 import subprocess
@@ -23,11 +24,18 @@ hdr = rows[1]
 isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
 ist = hdr.index("Warp Stall Sampling (All Samples)")
 ins = []
-for r in rows[2:]:  # the first kernel of the report only (a second one repeats the header)
+kidx = int(os.environ.get("KIDX", "0"))  # which kernel of the report (each repeats the header)
+for r in rows[2:]:
     if len(r) <= iex:
         continue
     if not (r[iex] or "0").isdigit():
-        break
+        if r[iex] != "Instructions Executed":
+            continue
+        if kidx == 0:
+            break
+        kidx -= 1
+        ins = []
+        continue
     ins.append((r[isrc].strip(), int(r[iex] or 0), int(r[ist] or 0)))
 with tempfile.TemporaryDirectory() as d:
     import os
