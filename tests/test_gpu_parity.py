@@ -143,6 +143,27 @@ def test_oracle_any_dimension(ds, oracle, rng, d, fname):
         assert np.array_equal(labels, want), (d, n, fname)
 
 
+@pytest.mark.parametrize("d", [5, 8, 16, 24])
+@pytest.mark.parametrize("fname", ["alg", "dir"])
+def test_exact_products_signed_zeros_and_subnormals(ds, oracle, rng, d, fname):
+    """d >= 5 forms every product as FFMA2(a, b, -0): signed zeros,
+    float32 subnormals and products that underflow must give the FMUL bits exactly."""
+    n = 700
+    vals = np.array([0.0, -0.0, 1e-39, -1e-39, 3e-42, 1e-20, -1e-20, 1e-19, 0.5, -0.25],
+                    dtype=np.float64)
+    pts = rng.choice(vals, size=(n, d))
+    pts[: n // 2] += rng.normal(0.0, 1e-19, size=(n // 2, d))  # tiny spread: squares underflow
+    for eps in (1e-19, 3e-19, 0.3):
+        eps_sq = eps * eps
+        bits, counts, _ = gpu_stage12(ds, pts, eps, eps_sq, 2, fname)
+        obits, ocounts = oracle.neighborhood(pts, eps_sq, FORMULAS[fname])
+        assert np.array_equal(bits, obits), (d, eps, fname)
+        assert np.array_equal(counts, ocounts), (d, eps, fname)
+        labels = gpu_labels(ds, pts, eps, eps_sq, 2, fname)
+        want, _ = oracle.dbscan(pts, eps_sq, 2, FORMULAS[fname])
+        assert np.array_equal(labels, want), (d, eps, fname)
+
+
 def test_padding_is_bit_neutral(ds):
     pts = ds.generate_blobs(3000, 5, 0.4, 0.1, 11, 2).coords_aos
     for fname in FORMULAS:
