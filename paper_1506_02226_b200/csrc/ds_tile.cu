@@ -393,7 +393,8 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // The eps-tile kernel. Warps work independently (no block-level synchronisation):
-//   * units come in batches of B consecutive units (about 16 batches per warp): the
+//   * units come in batches of B consecutive units (about 16 batches per warp, 128 for
+//     records wider than 4 dimensions): the
 //     first two batches of a warp are static, later ones come from a global atomic
 //     counter; each batch's index and its list entries (one per lane, coalesced) are
 //     fetched one batch ahead, so neither the atomic nor the list load is on the
@@ -439,7 +440,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   if (r_lo >= r_hi) return;
 
   // ---- batches of row units: [lo, hi) + list entries (lane i: entry lo + i) ----
-  // about 16 batches per warp; batch indices come from a 32-bit atomic counter
+  // about 16 (d <= 4) or 128 (wider) batches per warp; indices from a 32-bit atomic counter
   const long long nw = (long long)gridDim.x * G::WARPS;
 #ifndef DS_BATCH_MIN
 #define DS_BATCH_MIN 1
