@@ -125,16 +125,28 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
-def tile_traffic(config: str):
-    """DRAM bytes per launch of the eps-tile kernel from the committed ncu capture."""
+def tile_capture(config: str):
+    """The eps-tile kernel's entry in the committed ncu capture summary, or {}."""
     for path in (("profiles", "r02", "tile_traffic.json"), ("profiles", "r01_tile_traffic.json")):
         try:
             with open(os.path.join(ROOT, *path)) as fh:
-                t = json.load(fh)[config]
-            return t["dram_read_bytes"] + t["dram_write_bytes"]
+                return json.load(fh)[config]
         except (OSError, KeyError, ValueError):
             continue
-    return None
+    return {}
+
+
+def tile_traffic(config: str):
+    """DRAM bytes per launch of the eps-tile kernel from the committed ncu capture."""
+    t = tile_capture(config)
+    return t["dram_read_bytes"] + t["dram_write_bytes"] if t else None
+
+
+def tile_pipes(config: str):
+    """FMA / ALU pipe and issue-active percentages of the same ncu capture."""
+    t = tile_capture(config)
+    keys = ("fma_pipe_pct", "alu_pipe_pct", "issue_active_pct")
+    return {k: t[k] for k in keys if k in t} or None
 
 
 def golden_labels(config: str):
@@ -424,6 +436,7 @@ def run_b200(args):
                      "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": tile_traffic(args.config),
                      "traffic_source": "dram__bytes_read+write per launch, profiles/r02/tile_traffic.json",
+                     "ncu_pipes": tile_pipes(args.config),
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz "
                                      "(no measured FP32 figure in MEASURED_PEAKS.json)"),
                      "ops_per_pair": ops, "pairs_per_launch": pairs,
@@ -442,6 +455,7 @@ def run_b200(args):
                     % (wide["n"], wide["d"]),
             "tile_ms": wide["tile_ms"], "pairs_per_launch": wide["pairs_per_launch"],
             "ops_per_pair": wide["ops_per_pair"],
+            "traffic": tile_traffic("C4"), "ncu_pipes": tile_pipes("C4"),
             "achieved": wide["pairs_per_launch"] * wide["ops_per_pair"] / (wide["tile_ms"] / 1e3) / 1e12,
             "frac": wide["pairs_per_launch"] * wide["ops_per_pair"] / (wide["tile_ms"] / 1e3) / 1e12
                     / fp32_peak}),
