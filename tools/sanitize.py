@@ -7,6 +7,7 @@
 c1:    C1 (10k, 2-D) through run_dbscan (default schedule, graph recorded on the 2nd
        call and replayed on the 3rd), the dense schedule, fused_build with the
        reference-layout export and merge_iterative from those bits.
+wide:  20k 16-D blobs through run_dbscan (the d >= 5 pair loop).
 chain: a 100k-point serpentine chain + blobs (the C5 generator scaled down): the
        union-find's long-path case, default schedule.
 Every result is compared with the C oracle; the script exits 1 on a mismatch.
@@ -31,6 +32,9 @@ def main():
         cfg = ds.CONFIGS["C1"]
         pts = cfg.points()
         params = ds.validate_params(cfg.eps, cfg.min_pts)
+    elif which == "wide":  # 16-D: the paired FFMA2 packing, wide unit batches
+        pts = ds.generate_blobs(20_000, 6, 0.3, 0.1, 7, 16)
+        params = ds.validate_params(1.5, 8)
     else:
         pts = ds.generate_chain(100_000, 4_000, 8, 2_000, 5)
         params = ds.validate_params(0.3, 8)
