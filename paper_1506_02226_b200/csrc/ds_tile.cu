@@ -393,7 +393,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // The eps-tile kernel. Warps work independently (no block-level synchronisation):
-//   * units come in batches of B consecutive units (about 16 batches per warp, 128 for
+//   * units come in batches of B consecutive units (about 32 batches per warp, 128 for
 //     records wider than 4 dimensions): the
 //     first two batches of a warp are static, later ones come from a global atomic
 //     counter; each batch's index and its list entries (one per lane, coalesced) are
@@ -440,7 +440,7 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
   if (r_lo >= r_hi) return;
 
   // ---- batches of row units: [lo, hi) + list entries (lane i: entry lo + i) ----
-  // about 16 (d <= 4) or 128 (wider) batches per warp; indices from a 32-bit atomic counter
+  // about 32 (d <= 4) or 128 (wider) batches per warp; indices from a 32-bit atomic counter
   const long long nw = (long long)gridDim.x * G::WARPS;
 #ifndef DS_BATCH_MIN
 #define DS_BATCH_MIN 1
@@ -450,7 +450,13 @@ __device__ __forceinline__ void eps_unit_body(const UnitArgs& A) {
 #ifndef DS_BATCHES_WIDE
 #define DS_BATCHES_WIDE 128
 #endif
-  constexpr long long BATCHES = D > 4 ? DS_BATCHES_WIDE : 16;
+// d <= 4: ~32 batches per warp (A/B, round 2: 16 -> 32 cut the C5 eps kernel's tail,
+// 1.351 -> 1.324 ms, C3 0.622 -> 0.613 ms; 64 about the same, 128+ slower — the batches
+// reach one unit and the counter traffic grows)
+#ifndef DS_BATCHES_SMALL
+#define DS_BATCHES_SMALL 32
+#endif
+  constexpr long long BATCHES = D > 4 ? DS_BATCHES_WIDE : DS_BATCHES_SMALL;
   long long B = (r_hi - r_lo) / (nw * BATCHES);
   B = B < DS_BATCH_MIN ? DS_BATCH_MIN : (B > 32 ? 32 : B);
   unsigned int* const ctr = reinterpret_cast<unsigned int*>(A.work_ctr);
