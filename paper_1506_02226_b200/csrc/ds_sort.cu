@@ -312,7 +312,9 @@ __global__ void __launch_bounds__(PB_T) permute_bounds_kernel(
     unsigned int* __restrict__ super) {
   constexpr int PB_P = TILE / PB_T;
   griddep_wait();
-  __shared__ float smn[TILE / 32], smx[TILE / 32];
+  // per column (dpad <= 64, + the norm) and 32-point block: the block's min / max; the
+  // tile's box is reduced from them after one barrier, one column per thread
+  __shared__ float smn[65][TILE / 32], smx[65][TILE / 32];
   const int64_t tile = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   int64_t o[PB_P];
@@ -353,26 +355,25 @@ __global__ void __launch_bounds__(PB_T) permute_bounds_kernel(
             blk[wb * BS + 2 * dpad] = mx;
           }
         }
-        smn[bw] = mn;
-        smx[bw] = mx;
+        smn[k][bw] = mn;
+        smx[k][bw] = mx;
       }
     }
-    __syncthreads();
-    if (t == 0) {
-      float mn = smn[0], mx = smx[0];
-      for (int w = 1; w < TILE / 32; ++w) {
-        mn = fminf(mn, smn[w]);
-        mx = fmaxf(mx, smx[w]);
-      }
-      if (k < dpad) {
-        lo[tile * dpad + k] = mn;
-        hi[tile * dpad + k] = mx;
-      } else {
-        maxnorm[tile] = mx;
-      }
-      if (super) super_box_add(super, tile, dpad, k, mn, mx);
+  }
+  __syncthreads();
+  for (int k = t; k <= dpad; k += PB_T) {  // k == dpad: the norm column
+    float mn = smn[k][0], mx = smx[k][0];
+    for (int w = 1; w < TILE / 32; ++w) {
+      mn = fminf(mn, smn[k][w]);
+      mx = fmaxf(mx, smx[k][w]);
     }
-    __syncthreads();
+    if (k < dpad) {
+      lo[tile * dpad + k] = mn;
+      hi[tile * dpad + k] = mx;
+    } else {
+      maxnorm[tile] = mx;
+    }
+    if (super) super_box_add(super, tile, dpad, k, mn, mx);
   }
 }
 
