@@ -1302,6 +1302,40 @@ __global__ void __launch_bounds__(CULL_T) cull_rows_kernel(
   }
 }
 
+// One GPU (no shard needs the same order): each row's kept pairs are gathered in shared
+// memory (T <= CULL_ROWS_MAX entries) and appended to the list with one reservation per
+// row — one launch instead of cull_rows + cull_write; the list order across rows then
+// depends on scheduling, which no result does.
+__global__ void __launch_bounds__(CULL_T) cull_append_kernel(
+    const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
+    int dpad, int64_t T, float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
+    uint32_t* __restrict__ list, unsigned long long* __restrict__ count) {
+  griddep_wait();
+  extern __shared__ uint32_t kb[];  // T entries
+  __shared__ int nkb;
+  __shared__ unsigned long long kbase;
+  const bool unsafe = *unsafe_flag != 0;
+  const int lane = threadIdx.x & 31;
+  for (int64_t a = blockIdx.x; a < T; a += gridDim.x) {
+    if (threadIdx.x == 0) nkb = 0;
+    __syncthreads();
+    for (int64_t b0 = a; b0 < T; b0 += blockDim.x) {
+      const int64_t b = b0 + threadIdx.x;
+      const bool k = b < T && keep_item(lo, hi, maxnorm, dpad, (int)a, (int)b, eps32, formula, unsafe);
+      const uint32_t bal = __ballot_sync(0xffffffffu, k);
+      int at = 0;
+      if (lane == 0 && bal) at = atomicAdd(&nkb, __popc(bal));
+      at = __shfl_sync(0xffffffffu, at, 0);
+      if (k) kb[at + __popc(bal & ((1u << lane) - 1u))] = ((uint32_t)a << 16) | (uint32_t)b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) kbase = nkb ? atomicAdd(count, (unsigned long long)nkb) : 0ull;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nkb; e += blockDim.x) list[kbase + e] = kb[e];
+    __syncthreads();  // nkb / kb are rewritten by the next row
+  }
+}
+
 __global__ void __launch_bounds__(CULL_T) cull_write_kernel(
     const float* __restrict__ lo, const float* __restrict__ hi, const float* __restrict__ maxnorm,
     int dpad, int64_t T, float eps32, int formula, const uint32_t* __restrict__ unsafe_flag,
@@ -1585,6 +1619,10 @@ cudaError_t launch_cull(const float* rec, int64_t n, int d, float eps32, int for
   }
   if (T <= CULL_ROWS_MAX) {  // rowcnt lives in the flags buffer (T <= T(T+1)/2 ints)
     const unsigned g = (unsigned)std::min<int64_t>(T, 148 * 8);
+    if (!ordered)  // count starts at zero (the per-call zero region)
+      return launch_pdl(cull_append_kernel, dim3(g), dim3(CULL_T), (size_t)T * 4, s,
+                        (const float*)lo, (const float*)hi, (const float*)maxnorm, dp, T, eps32,
+                        formula, unsafe_flag, list, count);
     cudaError_t e = launch_pdl(cull_rows_kernel, dim3(g), dim3(CULL_T), 0, s, (const float*)lo,
                                (const float*)hi, (const float*)maxnorm, dp, T, eps32, formula,
                                unsafe_flag, flags);
